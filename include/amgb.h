@@ -1,0 +1,186 @@
+/*
+ * amgb.h -- C ABI of the B200 smoothed-aggregation AMG solve phase.
+ *
+ * What it computes (arXiv 1811.05704, "AMGCL", PAPER.md):
+ *   the solution of A u = f (Eq. (1)) by a Krylov method (CG, or
+ *   BiCGStab for non-symmetric A) preconditioned by one AMG
+ *   V-cycle (Algorithm 2; "single V-cycle is used as a
+ *   preconditioning step").  The hierarchy is built on the host
+ *   inside amg_setup (Algorithm 1; "the AMG hierarchy is always
+ *   constructed on the main processor (CPU)") with smoothed (or
+ *   plain) aggregation and then uploaded to the GPU, where the
+ *   solve phase runs entirely in this library's sm_100a kernels.
+ *   The readings of the paper this implementation commits to are listed in
+ *   DESIGN.md §3 (strength test, aggregation order, smoother constants, ...).
+ *
+ * Conventions common to every call:
+ *   - Return value: amg_status; 0 = OK, > 0 = result valid but flagged,
+ *     < 0 = error (nothing was computed; amg_last_error() has a message).
+ *   - Matrices: square CSR with int64 row pointers (n+1), int32 column indices
+ *     strictly increasing within each row and in [0, n), fp64 values.  Empty rows
+ *     are legal; every row must hold a positive diagonal entry (the strength test
+ *     a_ij^2 > eps^2 a_ii a_jj needs it).
+ *   - "device" pointers are CUDA global-memory fp64 arrays on the handle's
+ *     device, 16-byte aligned, length n, not aliased with each other; "host"
+ *     pointers are ordinary (pageable or pinned) host memory.
+ *   - Work is issued on the handle's stream (amg_set_stream; default: the legacy
+ *     default stream).  Calls that return results (amg_solve*) synchronise that
+ *     stream before returning; amg_precond_apply and amg_level_op are
+ *     asynchronous.
+ *   - A handle is not re-entrant; distinct handles may be used concurrently.
+ *   - amg_last_error() is thread-local.
+ */
+#ifndef AMGB_H
+#define AMGB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    AMG_OK = 0,
+    AMG_NOT_CONVERGED = 1,      /* maxiter reached; outputs valid */
+    AMG_BREAKDOWN = 2,          /* CG (r,Mr) <= 0 or (p,Ap) <= 0; BiCGStab rho/omega underflow */
+    AMG_E_INVALID_ARG = -1,
+    AMG_E_BAD_CSR = -2,         /* CSR invariants violated (message names the row) */
+    AMG_E_ZERO_DIAG = -3,       /* a diagonal entry is missing or not positive */
+    AMG_E_SINGULAR_COARSE = -4, /* coarsest LU pivot below 1e-14 max|A_L| */
+    AMG_E_COARSE_TOO_LARGE = -5,/* coarsest level larger than dense_max */
+    AMG_E_OOM = -6,
+    AMG_E_NO_DEVICE = -7,       /* solve requested on a host-only handle */
+    AMG_E_CUDA = -10
+} amg_status;
+
+typedef struct amg_hierarchy *amg_handle;
+
+/* Parameters; names follow the paper's runtime keys where it
+ * has them.  Defaults (amg_params_default) in brackets; DESIGN.md §3 cites each. */
+typedef struct {
+    uint32_t struct_size;   /* = sizeof(amg_params) (ABI check) */
+    int32_t coarsening;     /* "precond.coarsening.type": 0 smoothed_aggregation [0], 1 aggregation */
+    double eps_strong;      /* strength threshold on the finest level [0.08] */
+    double eps_decay;       /* eps on level l+1 = eps on level l * eps_decay [0.5] */
+    double p_omega;         /* prolongation-smoother damping [2/3] */
+    int32_t relax;          /* "precond.relax.type": 0 spai0 [0], 1 damped_jacobi, 2 chebyshev */
+    double jacobi_omega;    /* damped Jacobi weight [0.72] */
+    int32_t cheb_degree;    /* Chebyshev polynomial degree K [5] */
+    double cheb_lower;      /* lambda_min = lambda_max * cheb_lower [1/30] */
+    int32_t cheb_scaled;    /* 1: polynomial in D^-1 A [1]; 0: in A */
+    int32_t npre, npost;    /* smoothing sweeps per level [1, 1] */
+    int64_t coarse_enough;  /* stop coarsening at <= this many rows [3000] */
+    int32_t max_levels;     /* [30] */
+    int64_t dense_max;      /* error if the coarsest level is larger [20000] */
+    int32_t solver;         /* "solver.type": 0 cg [0], 1 bicgstab */
+    int32_t device;         /* CUDA device ordinal [0]; -1 = host-only handle (setup + export) */
+    int32_t use_graph;      /* 1: replay Krylov iterations as a CUDA graph [1] */
+} amg_params;
+
+/* Per-level statistics (amg_level_info). */
+typedef struct {
+    int64_t rows, nnz_A, nnz_P, cols_P; /* nnz_P = nnz(R); 0 on the coarsest level */
+    int64_t aggregates;                 /* = cols_P */
+    int32_t is_coarsest;
+    int32_t reserved;
+    int64_t dev_bytes;                  /* device bytes of this level's store */
+    int64_t padded_nnz_A;               /* stored (sliced-ELL) entries of A incl. padding */
+    double alg_bytes_vcycle;            /* algorithmic HBM bytes of this level per V-cycle */
+} amg_level_info;
+
+/* Test/export hook (amg_export_level): caller-owned HOST buffers, sized from
+ * amg_level_info; any pointer may be NULL to skip that array.  R = P^T. */
+typedef struct {
+    int64_t *A_ptr; int32_t *A_col; double *A_val;  /* rows+1, nnz_A, nnz_A */
+    int64_t *P_ptr; int32_t *P_col; double *P_val;  /* rows+1, nnz_P, nnz_P */
+    int64_t *R_ptr; int32_t *R_col; double *R_val;  /* cols_P+1, nnz_P, nnz_P */
+    int32_t *aggregates;                            /* rows */
+    double *smoother;   /* spai0/jacobi: m (rows); chebyshev: lmax, lmin, d, c */
+    double *coarse_inverse; /* coarsest level only: rows*rows, row-major A_L^-1 */
+} amg_level_export;
+
+/* Solve statistics (amg_solve_stats), filled by the last amg_solve*. */
+typedef struct {
+    int32_t iters;          /* Krylov iterations (loop trips, DESIGN.md §3 R19) */
+    int32_t vcycles;        /* preconditioner applications */
+    int32_t status;
+    int32_t reserved;
+    int64_t kernel_launches;/* kernels this library launched during the solve */
+    double solve_ms;        /* device time of the solve (events on the handle stream) */
+    double rel_resid;       /* true |f - A x| / |f| */
+    double alg_bytes;       /* algorithmic HBM bytes of the whole solve */
+    double prof_ms[8];      /* profile mode: device ms per kernel class (see AMG_PROF_*) */
+    double prof_bytes[8];   /* profile mode: algorithmic bytes per kernel class */
+    int64_t prof_launches[8];
+} amg_solve_stats;
+
+/* kernel classes timed in profile mode */
+enum { AMG_PROF_A0_PASS = 0,   /* level-0 A passes (smoother/residual/CG direction) */
+       AMG_PROF_A_COARSE = 1,  /* A passes on levels >= 1 */
+       AMG_PROF_TRANSFER = 2,  /* restriction / prolongation */
+       AMG_PROF_VECTOR = 3,    /* Krylov vector updates and norms */
+       AMG_PROF_COARSE_SOLVE = 4 };
+
+/* Fill *p with the defaults above (struct_size set). */
+void amg_params_default(amg_params *p);
+
+/* Build the hierarchy of A (host arrays: ptr[n+1], col[nnz], val[nnz], nnz =
+ * ptr[n]) and, unless prm->device == -1, upload it to the current CUDA device
+ * (prm->device).  The caller keeps ownership of the inputs and may free them on
+ * return; *out owns every allocation (release with amg_destroy).  prm may be NULL
+ * (defaults).  Errors: AMG_E_INVALID_ARG (n <= 0, NULL pointers, bad params),
+ * AMG_E_BAD_CSR, AMG_E_ZERO_DIAG, AMG_E_SINGULAR_COARSE, AMG_E_COARSE_TOO_LARGE,
+ * AMG_E_OOM, AMG_E_CUDA.  Cite: Algorithm 1. */
+amg_status amg_setup(int64_t n, const int64_t *ptr, const int32_t *col, const double *val,
+                     const amg_params *prm, amg_handle *out);
+
+/* Solve A x = f to |f - A x| <= tol |f| (recurrence residual; R17) with
+ * the handle's Krylov method, at most maxiter iterations.  f, x: DEVICE pointers;
+ * x holds the initial guess on entry and the solution on return.  f = 0 gives
+ * x = 0, 0 iterations.  *iters = loop trips, *rel_resid = true |f - A x|/|f|
+ * recomputed at exit.  Returns AMG_OK, AMG_NOT_CONVERGED or AMG_BREAKDOWN (outputs
+ * filled in all three cases) or an error.  Synchronous.  Cite: PAPER.md:141-143,
+ * 209-215. */
+amg_status amg_solve(amg_handle h, const double *f, double *x, double tol, int32_t maxiter,
+                     int32_t *iters, double *rel_resid);
+
+/* Same as amg_solve with HOST f and x: copies f and x to the device, solves,
+ * copies x back, all inside the call (the end-to-end path). */
+amg_status amg_solve_host(amg_handle h, const double *f, double *x, double tol, int32_t maxiter,
+                          int32_t *iters, double *rel_resid);
+
+/* z = M r: one V-cycle from a zero initial guess.  r, z:
+ * DEVICE pointers (length n, distinct).  Asynchronous on the handle stream. */
+amg_status amg_precond_apply(amg_handle h, const double *r, double *z);
+
+/* Issue subsequent work on `stream` (a cudaStream_t of the handle's device). */
+amg_status amg_set_stream(amg_handle h, void *stream);
+
+/* Profile mode: 1 = time kernel classes with CUDA events during amg_solve*
+ * (results in amg_solve_stats.prof_*), 0 = off [default]. */
+amg_status amg_set_profile(amg_handle h, int32_t on);
+
+amg_status amg_level_count(amg_handle h, int32_t *nlevels);
+amg_status amg_level_info_get(amg_handle h, int32_t level, amg_level_info *out);
+/* Copy the host-side hierarchy data of `level` into caller buffers. */
+amg_status amg_export_level(amg_handle h, int32_t level, const amg_level_export *out);
+amg_status amg_solve_stats_get(amg_handle h, amg_solve_stats *out);
+
+/* TEST HOOK: one device operation of level `level` on DEVICE vectors (async):
+ *   AMG_OP_SPMV_A   y = A_l x           AMG_OP_SPMV_P  y = P_l x   AMG_OP_SPMV_R  y = R_l x
+ *   AMG_OP_RESIDUAL y = f - A_l x       AMG_OP_RELAX   y = S_l(A_l, f, x) (one smoother call)
+ *   AMG_OP_COARSE   y = A_L^-1 f (coarsest level)     AMG_OP_VCYCLE y = V-cycle from level l, f, x = 0 */
+enum { AMG_OP_SPMV_A = 0, AMG_OP_SPMV_P = 1, AMG_OP_SPMV_R = 2, AMG_OP_RESIDUAL = 3,
+       AMG_OP_RELAX = 4, AMG_OP_COARSE = 5, AMG_OP_VCYCLE = 6 };
+amg_status amg_level_op(amg_handle h, int32_t level, int32_t op, const double *x, const double *f,
+                        double *y);
+
+void amg_destroy(amg_handle h);
+const char *amg_last_error(void);
+/* Library build identification string (compile flags, arch). */
+const char *amg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AMGB_H */

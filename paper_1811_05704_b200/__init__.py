@@ -1,0 +1,311 @@
+"""B200-native smoothed-aggregation AMG solve phase (arXiv 1811.05704, AMGCL).
+
+Thin Python binding of ``_lib/libamgb.so`` (C ABI: ``include/amgb.h``).  This
+module only marshals arguments: the hierarchy is built by the library's C++ host
+setup (Algorithm 1) and every step of the solve phase
+(Algorithm 2, inside CG / BiCGStab) runs in
+the library's sm_100a kernels.  PyTorch is used for device memory and streams
+only.  There is no CPU fallback: if the shared library is missing, importing
+this package raises.
+
+Parameters use the paper's runtime key names (Listing 2)
+where it has them, e.g. ``{"solver.type": "bicgstab", "precond.relax.type":
+"chebyshev"}``; see ``PARAM_KEYS``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libamgb.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(or `make -C paper_1811_05704_b200`). There is no CPU fallback.")
+
+_lib = C.CDLL(LIB_PATH)
+
+# ---- status codes (amg_status) ----
+OK, NOT_CONVERGED, BREAKDOWN = 0, 1, 2
+E_INVALID_ARG, E_BAD_CSR, E_ZERO_DIAG, E_SINGULAR_COARSE = -1, -2, -3, -4
+E_COARSE_TOO_LARGE, E_OOM, E_NO_DEVICE, E_CUDA = -5, -6, -7, -10
+
+OP_SPMV_A, OP_SPMV_P, OP_SPMV_R, OP_RESIDUAL, OP_RELAX, OP_COARSE, OP_VCYCLE = range(7)
+PROF_CLASSES = ("A0 pass", "A coarse", "transfer", "vector", "coarse solve")
+
+
+class AmgParams(C.Structure):
+    _fields_ = [
+        ("struct_size", C.c_uint32),
+        ("coarsening", C.c_int32),
+        ("eps_strong", C.c_double),
+        ("eps_decay", C.c_double),
+        ("p_omega", C.c_double),
+        ("relax", C.c_int32),
+        ("jacobi_omega", C.c_double),
+        ("cheb_degree", C.c_int32),
+        ("cheb_lower", C.c_double),
+        ("cheb_scaled", C.c_int32),
+        ("npre", C.c_int32),
+        ("npost", C.c_int32),
+        ("coarse_enough", C.c_int64),
+        ("max_levels", C.c_int32),
+        ("dense_max", C.c_int64),
+        ("solver", C.c_int32),
+        ("device", C.c_int32),
+        ("use_graph", C.c_int32),
+    ]
+
+
+class LevelInfo(C.Structure):
+    _fields_ = [
+        ("rows", C.c_int64), ("nnz_A", C.c_int64), ("nnz_P", C.c_int64), ("cols_P", C.c_int64),
+        ("aggregates", C.c_int64), ("is_coarsest", C.c_int32), ("reserved", C.c_int32),
+        ("dev_bytes", C.c_int64), ("padded_nnz_A", C.c_int64), ("alg_bytes_vcycle", C.c_double),
+    ]
+
+
+class LevelExport(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in (
+        "A_ptr", "A_col", "A_val", "P_ptr", "P_col", "P_val", "R_ptr", "R_col", "R_val",
+        "aggregates", "smoother", "coarse_inverse")]
+
+
+class SolveStats(C.Structure):
+    _fields_ = [
+        ("iters", C.c_int32), ("vcycles", C.c_int32), ("status", C.c_int32), ("reserved", C.c_int32),
+        ("kernel_launches", C.c_int64), ("solve_ms", C.c_double), ("rel_resid", C.c_double),
+        ("alg_bytes", C.c_double), ("prof_ms", C.c_double * 8), ("prof_bytes", C.c_double * 8),
+        ("prof_launches", C.c_int64 * 8),
+    ]
+
+
+_V = C.c_void_p
+_lib.amg_params_default.argtypes = [C.POINTER(AmgParams)]
+_lib.amg_setup.argtypes = [C.c_int64, _V, _V, _V, C.POINTER(AmgParams), C.POINTER(_V)]
+_lib.amg_solve.argtypes = [_V, _V, _V, C.c_double, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_double)]
+_lib.amg_solve_host.argtypes = _lib.amg_solve.argtypes
+_lib.amg_precond_apply.argtypes = [_V, _V, _V]
+_lib.amg_set_stream.argtypes = [_V, _V]
+_lib.amg_set_profile.argtypes = [_V, C.c_int32]
+_lib.amg_level_count.argtypes = [_V, C.POINTER(C.c_int32)]
+_lib.amg_level_info_get.argtypes = [_V, C.c_int32, C.POINTER(LevelInfo)]
+_lib.amg_export_level.argtypes = [_V, C.c_int32, C.POINTER(LevelExport)]
+_lib.amg_solve_stats_get.argtypes = [_V, C.POINTER(SolveStats)]
+_lib.amg_level_op.argtypes = [_V, C.c_int32, C.c_int32, _V, _V, _V]
+_lib.amg_destroy.argtypes = [_V]
+_lib.amg_last_error.restype = C.c_char_p
+_lib.amg_version.restype = C.c_char_p
+for _name in ("amg_setup", "amg_solve", "amg_solve_host", "amg_precond_apply", "amg_set_stream",
+              "amg_set_profile", "amg_level_count", "amg_level_info_get", "amg_export_level",
+              "amg_solve_stats_get", "amg_level_op"):
+    getattr(_lib, _name).restype = C.c_int
+
+# Exported C symbols (tests check them against include/amgb.h).
+SYMBOLS = ("amg_params_default", "amg_setup", "amg_solve", "amg_solve_host", "amg_precond_apply",
+           "amg_set_stream", "amg_set_profile", "amg_level_count", "amg_level_info_get",
+           "amg_export_level", "amg_solve_stats_get", "amg_level_op", "amg_destroy",
+           "amg_last_error", "amg_version")
+
+RELAX = {"spai0": 0, "damped_jacobi": 1, "chebyshev": 2}
+COARSENING = {"smoothed_aggregation": 0, "aggregation": 1}
+SOLVER = {"cg": 0, "bicgstab": 1}
+
+# dotted keys (Listing 2 style) -> amg_params field
+PARAM_KEYS = {
+    "precond.coarsening.type": "coarsening",
+    "precond.coarsening.aggr.eps_strong": "eps_strong",
+    "precond.coarsening.aggr.eps_decay": "eps_decay",
+    "precond.coarsening.p_omega": "p_omega",
+    "precond.relax.type": "relax",
+    "precond.relax.damping": "jacobi_omega",
+    "precond.relax.degree": "cheb_degree",
+    "precond.relax.lower": "cheb_lower",
+    "precond.relax.scaled": "cheb_scaled",
+    "precond.npre": "npre",
+    "precond.npost": "npost",
+    "precond.coarse_enough": "coarse_enough",
+    "precond.max_levels": "max_levels",
+    "precond.dense_max": "dense_max",
+    "solver.type": "solver",
+    "device": "device",
+    "use_graph": "use_graph",
+}
+_ENUMS = {"relax": RELAX, "coarsening": COARSENING, "solver": SOLVER}
+
+
+class AmgError(RuntimeError):
+    def __init__(self, code, where):
+        msg = _lib.amg_last_error().decode()
+        super().__init__(f"{where} failed ({code}): {msg}")
+        self.code = code
+
+
+def _check(rc, where):
+    if rc < 0:
+        raise AmgError(rc, where)
+    return rc
+
+
+def make_params(params: dict | None = None, **kw) -> AmgParams:
+    p = AmgParams()
+    _lib.amg_params_default(C.byref(p))
+    items = dict(params or {})
+    items.update(kw)
+    for k, v in items.items():
+        field = PARAM_KEYS.get(k, k)
+        if field not in dict(AmgParams._fields_):
+            raise KeyError(f"unknown parameter {k!r}")
+        if field in _ENUMS and isinstance(v, str):
+            v = _ENUMS[field][v]
+        setattr(p, field, v)
+    return p
+
+
+def version() -> str:
+    return _lib.amg_version().decode()
+
+
+def _ptr(a):
+    """Address of a numpy array or torch tensor (contiguous)."""
+    if isinstance(a, np.ndarray):
+        assert a.flags.c_contiguous
+        return a.ctypes.data
+    assert a.is_contiguous()
+    return a.data_ptr()
+
+
+class Hierarchy:
+    """amg_setup handle: AMG hierarchy of A, resident on the GPU (device >= 0) or
+    host-only (device = -1, for setup/export only)."""
+
+    def __init__(self, ptr, col, val, params: dict | None = None, **kw):
+        self._ptr = np.ascontiguousarray(ptr, np.int64)
+        col = np.ascontiguousarray(col, np.int32)
+        val = np.ascontiguousarray(val, np.float64)
+        self.n = len(self._ptr) - 1
+        self.prm = make_params(params, **kw)
+        h = C.c_void_p()
+        _check(_lib.amg_setup(self.n, self._ptr.ctypes.data, col.ctypes.data, val.ctypes.data,
+                              C.byref(self.prm), C.byref(h)), "amg_setup")
+        self._h = h
+        self.on_device = self.prm.device >= 0
+        if self.on_device:
+            import torch
+            self.device = torch.device("cuda", self.prm.device)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.amg_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    # ---- info / export -------------------------------------------------
+    @property
+    def nlevels(self) -> int:
+        n = C.c_int32()
+        _check(_lib.amg_level_count(self._h, C.byref(n)), "amg_level_count")
+        return n.value
+
+    def level_info(self, l: int) -> dict:
+        li = LevelInfo()
+        _check(_lib.amg_level_info_get(self._h, l, C.byref(li)), "amg_level_info_get")
+        return {k: getattr(li, k) for k, _ in LevelInfo._fields_ if k != "reserved"}
+
+    def complexities(self):
+        inf = [self.level_info(l) for l in range(self.nlevels)]
+        return (sum(i["nnz_A"] for i in inf) / inf[0]["nnz_A"],
+                sum(i["rows"] for i in inf) / inf[0]["rows"])
+
+    def export_level(self, l: int) -> dict:
+        """Host copies of level l: A, P, R (CSR triples), aggregates, smoother data
+        and (coarsest level) the dense inverse."""
+        inf = self.level_info(l)
+        n, nnz, np_, nc = inf["rows"], inf["nnz_A"], inf["nnz_P"], inf["cols_P"]
+        out = {"A": (np.zeros(n + 1, np.int64), np.zeros(nnz, np.int32), np.zeros(nnz))}
+        ex = LevelExport()
+        ex.A_ptr, ex.A_col, ex.A_val = (a.ctypes.data for a in out["A"])
+        if not inf["is_coarsest"]:
+            out["P"] = (np.zeros(n + 1, np.int64), np.zeros(np_, np.int32), np.zeros(np_))
+            out["R"] = (np.zeros(nc + 1, np.int64), np.zeros(np_, np.int32), np.zeros(np_))
+            out["aggregates"] = np.zeros(n, np.int32)
+            out["smoother"] = np.zeros(4 if self.prm.relax == 2 else n)
+            ex.P_ptr, ex.P_col, ex.P_val = (a.ctypes.data for a in out["P"])
+            ex.R_ptr, ex.R_col, ex.R_val = (a.ctypes.data for a in out["R"])
+            ex.aggregates = out["aggregates"].ctypes.data
+            ex.smoother = out["smoother"].ctypes.data
+        else:
+            out["coarse_inverse"] = np.zeros((n, n))
+            ex.coarse_inverse = out["coarse_inverse"].ctypes.data
+        _check(_lib.amg_export_level(self._h, l, C.byref(ex)), "amg_export_level")
+        return out
+
+    # ---- device operations ---------------------------------------------
+    def _sync_stream(self):
+        if not self.on_device:
+            return  # the library reports AMG_E_NO_DEVICE
+        import torch
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        _check(_lib.amg_set_stream(self._h, s), "amg_set_stream")
+
+    def solve(self, f, x=None, tol=1e-8, maxiter=100):
+        """Solve A x = f on the GPU; f, x are CUDA float64 tensors (x: initial
+        guess, overwritten).  Returns (x, iters, rel_resid, status)."""
+        import torch
+        if x is None:
+            x = torch.zeros_like(f)
+        self._sync_stream()
+        it, rel = C.c_int32(), C.c_double()
+        st = _check(_lib.amg_solve(self._h, _ptr(f), _ptr(x), tol, maxiter, C.byref(it), C.byref(rel)),
+                    "amg_solve")
+        return x, it.value, rel.value, st
+
+    def solve_host(self, f: np.ndarray, x: np.ndarray | None = None, tol=1e-8, maxiter=100):
+        """End-to-end solve with HOST arrays (copies inside the library call)."""
+        f = np.ascontiguousarray(f, np.float64)
+        x = np.zeros_like(f) if x is None else np.ascontiguousarray(x, np.float64)
+        self._sync_stream()
+        it, rel = C.c_int32(), C.c_double()
+        st = _check(_lib.amg_solve_host(self._h, _ptr(f), _ptr(x), tol, maxiter, C.byref(it),
+                                        C.byref(rel)), "amg_solve_host")
+        return x, it.value, rel.value, st
+
+    def precond(self, r, z=None):
+        """z = M r: one V-cycle from zero (asynchronous on the current stream)."""
+        import torch
+        if z is None:
+            z = torch.empty_like(r)
+        self._sync_stream()
+        _check(_lib.amg_precond_apply(self._h, _ptr(r), _ptr(z)), "amg_precond_apply")
+        return z
+
+    def level_op(self, l: int, op: int, x=None, f=None, y=None, ny=None):
+        """Test hook (amg_level_op); y is allocated if not given."""
+        import torch
+        if y is None:
+            y = torch.empty(ny, dtype=torch.float64, device=self.device)
+        self._sync_stream()
+        _check(_lib.amg_level_op(self._h, l, op, _ptr(x) if x is not None else None,
+                                 _ptr(f) if f is not None else None, _ptr(y)), "amg_level_op")
+        return y
+
+    def set_profile(self, on: bool):
+        _check(_lib.amg_set_profile(self._h, 1 if on else 0), "amg_set_profile")
+
+    def stats(self) -> dict:
+        s = SolveStats()
+        _check(_lib.amg_solve_stats_get(self._h, C.byref(s)), "amg_solve_stats_get")
+        d = {k: getattr(s, k) for k, _ in SolveStats._fields_ if k != "reserved"}
+        for k in ("prof_ms", "prof_bytes", "prof_launches"):
+            d[k] = list(d[k])[:len(PROF_CLASSES)]
+        return d
+
+
+def setup(ptr, col, val, params: dict | None = None, **kw) -> Hierarchy:
+    """amg_setup: build (host) and upload (GPU) the AMG hierarchy of A."""
+    return Hierarchy(ptr, col, val, params, **kw)
