@@ -1,0 +1,383 @@
+#!/usr/bin/env python
+"""bench.py -- AMG-preconditioned CG solve phase on B200 (arXiv 1811.05704).
+
+Headline (BASELINE.json metric): solve time and V-cycles/s of CG + smoothed-
+aggregation AMG (SPAI-0) on the 3D Poisson problem 256^3 (16,777,216 unknowns,
+117,047,296 nonzeros; Eq. (2)), tolerance 1e-8, with the
+HBM-roofline fraction of the dominant kernel class.
+
+One "step" = one full solve from x = 0 to rel. residual 1e-8 (all of §8(a):
+V-cycle kernels, Krylov updates, dots, convergence tests), inputs resident in
+HBM.  value = V-cycles per second over the K timed steps (whole job).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl amgb|reference]
+                  [--problem poisson|poisson_perm|varcoef|convdiff] [--n 256]
+
+--impl reference times the oracle (plain fp64 C, oracle/) on the host cores:
+one step = one oracle CG iteration (one V-cycle) on the same system.
+
+Multi-GPU (torchrun, N > 1): each rank solves its own copy of the problem
+(replicas, no halo exchange yet), value = sum over ranks,
+time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="amgb", choices=["amgb", "reference"])
+    ap.add_argument("--problem", default="poisson")
+    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--relax", default=None)
+    ap.add_argument("--solver", default=None)
+    ap.add_argument("--tol", type=float, default=1e-8)
+    ap.add_argument("--maxiter", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--json-out", default=None)
+    return ap.parse_args()
+
+
+PROBLEM_DEFAULTS = {  # BASELINE.json configs -> solver settings
+    "poisson": dict(relax="spai0", solver="cg", maxiter=100),
+    "poisson_perm": dict(relax="spai0", solver="cg", maxiter=100),
+    "varcoef": dict(relax="chebyshev", solver="cg", maxiter=200),
+    "convdiff": dict(relax="damped_jacobi", solver="bicgstab", maxiter=200),
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy bandwidth)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def problem_arrays(name, n):
+    ptr, col, val, f = synth.problem(name, n)
+    return ptr, col, val, f
+
+
+def workload_name(args, cfg):
+    return f"{args.problem}{args.n}^3_{cfg['solver']}_sa_{cfg['relax']}"
+
+
+def cpu_baseline_full_solve(ptr, col, val, f, cfg, tol, maxiter):
+    """The oracle as it stands on the host cores: untimed setup, then one full
+    solve of the same system (timed).  Also returns its iterations/solution for
+    the full-size parity check."""
+    import oracle
+    A = oracle.Csr(ptr, col, val)
+    t0 = time.perf_counter()
+    hier = oracle.Hierarchy(A, relax=cfg["relax"])
+    t_setup = time.perf_counter() - t0
+    fn = oracle.bicgstab if cfg["solver"] == "bicgstab" else oracle.cg
+    t0 = time.perf_counter()
+    res = fn(A, f, tol=tol, maxiter=maxiter, hier=hier)
+    t_solve = time.perf_counter() - t0
+    vcyc = res.get("vcycles", res["iters"])
+    return dict(setup_s=t_setup, solve_s=t_solve, iters=res["iters"], vcycles=vcyc, x=res["x"],
+                rel=res["rel_resid"])
+
+
+def run_reference(args, cfg):
+    """--impl reference: the oracle timed on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    ptr, col, val, f = problem_arrays(args.problem, args.n)
+    A = oracle.Csr(ptr, col, val)
+    t0 = time.perf_counter()
+    hier = oracle.Hierarchy(A, relax=cfg["relax"])
+    t_setup = time.perf_counter() - t0
+    fn = oracle.bicgstab if cfg["solver"] == "bicgstab" else oracle.cg
+    x = np.zeros(len(f))
+    # one step = one Krylov iteration (maxiter = 1, restarted from the current x)
+    for _ in range(args.warmup):
+        x = fn(A, f, x0=x, tol=0.0, maxiter=1, hier=hier)["x"]
+    vc = 0
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r = fn(A, f, x0=x, tol=0.0, maxiter=1, hier=hier)
+        x = r["x"]
+        vc += r.get("vcycles", r["iters"])
+    dt = time.perf_counter() - t0
+    cores = os.cpu_count()
+    value = vc / dt
+    line = {
+        "impl": "reference", "metric": "AMG-CG V-cycles/s (3D Poisson 256^3)", "value": value,
+        "unit": "V-cycles/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, synth/)",
+        "config": {"workload": workload_name(args, cfg), "step": "one oracle Krylov iteration "
+                   "(1 V-cycle + outer work, restarted from the current x)",
+                   "oracle_setup_s": t_setup},
+        "cpu_baseline": {"value": value, "unit": "V-cycles/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{args.steps} oracle CG iterations of the {args.n}^3 system"},
+        "e2e": {"value": value, "unit": "V-cycles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    cfg = dict(PROBLEM_DEFAULTS[args.problem])
+    if args.relax:
+        cfg["relax"] = args.relax
+    if args.solver:
+        cfg["solver"] = args.solver
+    if args.maxiter:
+        cfg["maxiter"] = args.maxiter
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1811_05704_b200 as amgb
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    ptr, col, val, f = problem_arrays(args.problem, args.n)
+    n, nnz = len(f), int(ptr[-1])
+    t0 = time.perf_counter()
+    h = amgb.setup(ptr, col, val, {"precond.relax.type": cfg["relax"], "solver.type": cfg["solver"]},
+                   device=local, use_graph=0 if args.no_graph else 1)
+    setup_s = time.perf_counter() - t0
+    infos = [h.level_info(l) for l in range(h.nlevels)]
+
+    stream = torch.cuda.Stream()
+    fd = torch.from_numpy(f).cuda()
+    x = torch.zeros_like(fd)
+    tol, maxiter = args.tol, cfg["maxiter"]
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            x.zero_()
+            h.solve(fd, x, tol=tol, maxiter=maxiter)
+        # profile only the dominant class (level-0 A passes): 2 event nodes per launch
+        h.set_profile(1 << 0)
+        x.zero_()
+        h.solve(fd, x, tol=tol, maxiter=maxiter)  # re-capture the graph with event nodes
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        iters_all, vc_total, launches, prof_ms, prof_bytes, prof_launch, alg_bytes = [], 0, 0, 0.0, 0.0, 0, 0.0
+        statuses, rels = [], []
+        with ClockSampler(local) as clk:
+            ev0.record(stream)
+            for _ in range(args.steps):
+                x.zero_()
+                _, it, rel, st = h.solve(fd, x, tol=tol, maxiter=maxiter)
+                s = h.stats()
+                iters_all.append(it)
+                vc_total += s["vcycles"]
+                launches += s["kernel_launches"]
+                prof_ms += s["prof_ms"][0]
+                prof_bytes += s["prof_bytes"][0]
+                prof_launch += s["prof_launches"][0]
+                alg_bytes += s["alg_bytes"]
+                statuses.append(st)
+                rels.append(rel)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+        elapsed_ms = ev0.elapsed_time(ev1)
+        barrier()
+        h.set_profile(0)
+    t_local = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
+    vc_local = torch.tensor([float(vc_total)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+        dist.all_reduce(vc_local, op=dist.ReduceOp.SUM)
+    t_max_ms = float(t_local.item())
+    vc_all = float(vc_local.item())
+    value = vc_all / (t_max_ms / 1e3)
+
+    # ---- end-to-end through the public API with HOST buffers (amg_solve_host)
+    e2e = None
+    if not args.no_e2e:
+        fh = torch.from_numpy(f).pin_memory().numpy()
+        xh = torch.zeros(n, dtype=torch.float64).pin_memory().numpy()
+        with torch.cuda.stream(stream):
+            for _ in range(max(1, args.warmup // 2)):
+                xh[:] = 0.0
+                h.solve_host(fh, xh, tol=tol, maxiter=maxiter)
+            barrier()
+            torch.cuda.synchronize()
+            vc_e = 0
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                xh[:] = 0.0
+                h.solve_host(fh, xh, tol=tol, maxiter=maxiter)
+                vc_e += h.stats()["vcycles"]
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+        te = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        ve = torch.tensor([float(vc_e)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            dist.all_reduce(ve, op=dist.ReduceOp.SUM)
+        e2e = {"value": float(ve.item()) / float(te.item()), "unit": "V-cycles/s",
+               "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 8 * n,
+               "ms_per_step": 1e3 * float(te.item()) / args.steps,
+               "timing": "host wall clock around amg_solve_host (H2D f,x + solve + D2H x), max over ranks"}
+
+    peak, peak_src = peaks()
+    achieved = (prof_bytes / (prof_ms / 1e3)) / 1e9 if prof_ms > 0 else None
+    solve_gbs = (alg_bytes / (elapsed_ms / 1e3)) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh_:
+            tj = json.load(fh_)
+            if tj.get("workload") == workload_name(args, cfg):
+                traffic = tj.get("a0_pass_bytes_per_launch")
+    except Exception:
+        pass
+
+    # ---- CPU baseline: the oracle on this host (rank 0, N = 1 only)
+    cpu = None
+    parity = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_baseline_full_solve(ptr, col, val, f, cfg, tol, maxiter)
+        cpu = {"value": cb["vcycles"] / cb["solve_s"], "unit": "V-cycles/s", "cores": os.cpu_count(),
+               "kind": "oracle",
+               "sample": f"one full oracle solve of the same {args.n}^3 system ({cb['iters']} iterations, "
+                         f"{cb['solve_s']:.1f} s; oracle setup {cb['setup_s']:.1f} s untimed)"}
+        xg = x.cpu().numpy()
+        parity = {"oracle_iters": cb["iters"], "gpu_iters": iters_all[-1],
+                  "x_rel_diff": float(np.linalg.norm(xg - cb["x"]) / np.linalg.norm(cb["x"])),
+                  "oracle_rel_resid": cb["rel"]}
+
+    if rank == 0:
+        line = {
+            "metric": "AMG-CG V-cycles/s, 3D Poisson 256^3 (solve time in config.solve_ms)",
+            "value": value, "unit": "V-cycles/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_max_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generators, synth/): 7-point FD Poisson, f = 1",
+            "config": {
+                "workload": workload_name(args, cfg), "n": n, "nnz": nnz, "tol": tol,
+                "solver": cfg["solver"], "relax": cfg["relax"], "coarsening": "smoothed_aggregation",
+                "parallelism": "1 GPU" if world == 1 else f"{world} replicas (no halo exchange yet)",
+                "levels": len(infos), "rows_per_level": [i["rows"] for i in infos],
+                "nnz_per_level": [i["nnz_A"] for i in infos],
+                "iters_per_solve": iters_all[-1], "rel_resid": rels[-1], "status": statuses[-1],
+                "solve_ms": t_max_ms / args.steps, "setup_s": setup_s,
+                "l2": "inputs larger than L2 (level-0 matrix %.2f GB + hierarchy vs 126 MB L2); no flush"
+                      % (12e-9 * nnz),
+                "solve_alg_GBps": solve_gbs, "solve_roofline_frac": solve_gbs / peak,
+            },
+            "roofline": {
+                "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "kernel": "level-0 A-pass kernels (sell_rows on A0: res0 / relax+dot / cg-dir+dot / r0)",
+                "launches_timed": prof_launch, "bytes_per_launch": prof_bytes / max(prof_launch, 1),
+                "ms_per_launch": prof_ms / max(prof_launch, 1), "peak_source": peak_src,
+            },
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "parity_full_size": parity,
+        }
+        out = json.dumps(line)
+        print(out, flush=True)
+        if args.json_out:
+            with open(args.json_out, "w") as fh_:
+                fh_.write(out + "\n")
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -23,8 +23,8 @@
  *   - "device" pointers are CUDA global-memory fp64 arrays on the handle's
  *     device, 16-byte aligned, length n, not aliased with each other; "host"
  *     pointers are ordinary (pageable or pinned) host memory.
- *   - Work is issued on the handle's stream (amg_set_stream; default: the legacy
- *     default stream).  Calls that return results (amg_solve*) synchronise that
+ *   - Work is issued on the handle's stream (amg_set_stream; default: a stream
+ *     the handle creates, which is ordered with the legacy default stream).  Calls that return results (amg_solve*) synchronise that
  *     stream before returning; amg_precond_apply and amg_level_op are
  *     asynchronous.
  *   - A handle is not re-entrant; distinct handles may be used concurrently.
@@ -108,7 +108,7 @@ typedef struct {
     int64_t kernel_launches;/* kernels this library launched during the solve */
     double solve_ms;        /* device time of the solve (events on the handle stream) */
     double rel_resid;       /* true |f - A x| / |f| */
-    double alg_bytes;       /* algorithmic HBM bytes of the whole solve */
+    double alg_bytes;       /* algorithmic HBM bytes of the kernels that ran */
     double prof_ms[8];      /* profile mode: device ms per kernel class (see AMG_PROF_*) */
     double prof_bytes[8];   /* profile mode: algorithmic bytes per kernel class */
     int64_t prof_launches[8];
@@ -156,9 +156,11 @@ amg_status amg_precond_apply(amg_handle h, const double *r, double *z);
 /* Issue subsequent work on `stream` (a cudaStream_t of the handle's device). */
 amg_status amg_set_stream(amg_handle h, void *stream);
 
-/* Profile mode: 1 = time kernel classes with CUDA events during amg_solve*
- * (results in amg_solve_stats.prof_*), 0 = off [default]. */
-amg_status amg_set_profile(amg_handle h, int32_t on);
+/* Profile mode: time the kernel classes in `mask` (bit c = class AMG_PROF_c;
+ * 0 = off [default]) with CUDA events during amg_solve* -- event-record nodes
+ * inside the iteration graph, so the timed solve is the production path.
+ * Results: amg_solve_stats.prof_ms / prof_bytes / prof_launches. */
+amg_status amg_set_profile(amg_handle h, int32_t mask);
 
 amg_status amg_level_count(amg_handle h, int32_t *nlevels);
 amg_status amg_level_info_get(amg_handle h, int32_t level, amg_level_info *out);

@@ -294,8 +294,9 @@ class Hierarchy:
                                  _ptr(f) if f is not None else None, _ptr(y)), "amg_level_op")
         return y
 
-    def set_profile(self, on: bool):
-        _check(_lib.amg_set_profile(self._h, 1 if on else 0), "amg_set_profile")
+    def set_profile(self, mask: int):
+        """Time kernel classes (bit c = PROF_CLASSES[c]) with CUDA events; 0 = off."""
+        _check(_lib.amg_set_profile(self._h, int(mask)), "amg_set_profile")
 
     def stats(self) -> dict:
         s = SolveStats()

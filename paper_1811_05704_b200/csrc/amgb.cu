@@ -184,7 +184,8 @@ struct FinBiX {  // after x, r update: rho_next = (rhat, r), res = |r|
 
 // ---- vector ops ----------------------------------------------------------
 
-struct VNorm2 {  // (a, a)
+struct VNorm2 {
+    static constexpr int STREAMS = 1;  // n-vectors moved; (a, a)
     static constexpr int NDOT = 1;
     const double* a;
     FinNorm fin;
@@ -193,7 +194,8 @@ struct VNorm2 {  // (a, a)
 };
 
 template <class Fin>
-struct VDot {  // (a, b)
+struct VDot {
+    static constexpr int STREAMS = 2;  // n-vectors moved; (a, b)
     static constexpr int NDOT = 1;
     const double* a;
     const double* b;
@@ -202,7 +204,8 @@ struct VDot {  // (a, b)
     __device__ void elem(int64_t i, double* d) const { d[0] += a[i] * b[i]; }
 };
 
-struct VMulDiag {  // x = m o f  (first SPAI-0/Jacobi sweep from zero)
+struct VMulDiag {
+    static constexpr int STREAMS = 3;  // n-vectors moved; x = m o f  (first SPAI-0/Jacobi sweep from zero)
     static constexpr int NDOT = 0;
     const double* m;
     const double* f;
@@ -212,7 +215,8 @@ struct VMulDiag {  // x = m o f  (first SPAI-0/Jacobi sweep from zero)
     __device__ void elem(int64_t i, double*) const { x[i] = m[i] * f[i]; }
 };
 
-struct VCheb0 {  // first Chebyshev step from x = 0: p = alpha (f / a_ii); x = p
+struct VCheb0 {
+    static constexpr int STREAMS = 4;  // n-vectors moved; first Chebyshev step from x = 0: p = alpha (f / a_ii); x = p
     static constexpr int NDOT = 0;
     const double* f;
     const double* diag;
@@ -231,7 +235,8 @@ struct VCheb0 {  // first Chebyshev step from x = 0: p = alpha (f / a_ii); x = p
     }
 };
 
-struct VCgUpdate {  // x += alpha p; r -= alpha q; (r, r)
+struct VCgUpdate {
+    static constexpr int STREAMS = 6;  // n-vectors moved; x += alpha p; r -= alpha q; (r, r)
     static constexpr int NDOT = 1;
     double* x;
     double* r;
@@ -249,7 +254,8 @@ struct VCgUpdate {  // x += alpha p; r -= alpha q; (r, r)
     }
 };
 
-struct VBiP {  // p = r (k = 0) or r + beta (p - omega v)
+struct VBiP {
+    static constexpr int STREAMS = 3;  // n-vectors moved; p = r (k = 0) or r + beta (p - omega v)
     static constexpr int NDOT = 0;
     const double* r;
     const double* v;
@@ -268,7 +274,8 @@ struct VBiP {  // p = r (k = 0) or r + beta (p - omega v)
     }
 };
 
-struct VBiS {  // s = r - alpha v; (s, s)
+struct VBiS {
+    static constexpr int STREAMS = 3;  // n-vectors moved; s = r - alpha v; (s, s)
     static constexpr int NDOT = 1;
     const double* r;
     const double* v;
@@ -284,7 +291,8 @@ struct VBiS {  // s = r - alpha v; (s, s)
     }
 };
 
-struct VBiX {  // half: x += alpha ph; else x += alpha ph + omega sh, r = s - omega t
+struct VBiX {
+    static constexpr int STREAMS = 9;  // n-vectors moved; half: x += alpha ph; else x += alpha ph + omega sh, r = s - omega t
     static constexpr int NDOT = 2;
     double* x;
     double* r;
@@ -417,12 +425,12 @@ struct Handle {
     // CUDA graph of two Krylov iterations, keyed by the x pointer
     cudaGraphExec_t graph = nullptr;
     const double* graph_x = nullptr;
+    int graph_prof_mask = 0;
     int64_t graph_kernels = 0;
     // accounting
     int64_t launches = 0;
     bool count_only = false;  // while capturing: count kernels into graph_kernels
     amg_solve_stats stats{};
-    bool profile = false;
     bool sync_debug = false;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
@@ -442,6 +450,7 @@ struct Handle {
     }
     ~Handle() {
         if (graph) cudaGraphExecDestroy(graph);
+        for (cudaEvent_t e : ev_all) cudaEventDestroy(e);
         for (void* p : allocs) cudaFree(p);
         if (ks_host) cudaFreeHost(ks_host);
         if (ev0) cudaEventDestroy(ev0);
@@ -454,23 +463,112 @@ struct Handle {
         return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)num_sms * 8));
     }
 
-    void post_launch(const char* what) {
+    // ------------------------------------------------------------ accounting
+    // Every launch carries a kernel class (AMG_PROF_*), its algorithmic bytes
+    // and the Krylov iteration (0/1 inside a two-iteration
+    // group, -1 outside) it belongs to.  Bytes of iterations that actually ran
+    // are summed into the solve statistics; in profile mode the classes in
+    // prof_mask are bracketed with CUDA events (event-record nodes when the
+    // launches are being captured into the iteration graph).
+    struct Rec {
+        cudaEvent_t a = nullptr, b = nullptr;
+        int cls = 0, iter = -1;
+        double bytes = 0;
+    };
+    int prof_mask = 0;
+    bool capturing = false;
+    int cur_iter = -1;
+    std::vector<Rec> rec_direct, rec_graph;  // launches since the last sync / in the graph
+    std::vector<cudaEvent_t> ev_pool, ev_all;
+    double acc_ms[8] = {}, acc_bytes[8] = {}, alg_bytes = 0;
+    int64_t acc_launches[8] = {};
+
+    cudaEvent_t get_event() {
+        if (ev_pool.empty()) {
+            cudaEvent_t e;
+            ck(cudaEventCreate(&e), "cudaEventCreate");
+            ev_all.push_back(e);
+            return e;
+        }
+        cudaEvent_t e = ev_pool.back();
+        ev_pool.pop_back();
+        return e;
+    }
+    void record(cudaEvent_t e) {
+        if (capturing)
+            ck(cudaEventRecordWithFlags(e, stream, cudaEventRecordExternal), "event record node");
+        else
+            ck(cudaEventRecord(e, stream), "cudaEventRecord");
+    }
+    template <class F>
+    void launch(int cls, double bytes, const char* what, F&& fn) {
+        Rec rc;
+        rc.cls = cls;
+        rc.iter = cur_iter;
+        rc.bytes = bytes;
+        const bool timed = (prof_mask >> cls) & 1;
+        if (timed) {
+            rc.a = get_event();
+            rc.b = get_event();
+            record(rc.a);
+        }
+        fn();
+        if (timed) record(rc.b);
+        (capturing ? rec_graph : rec_direct).push_back(rc);
         ++launches;
         if (sync_debug) {
             ck(cudaGetLastError(), what);
             ck(cudaStreamSynchronize(stream), what);
         }
     }
+    // After a stream sync: account launches of iterations < ran (and all
+    // launches outside iterations); recycle direct-launch events.
+    void collect(std::vector<Rec>& v, int ran, bool recycle) {
+        for (Rec& rc : v) {
+            if (rc.iter >= 0 && rc.iter >= ran) continue;
+            alg_bytes += rc.bytes;
+            if (rc.a) {
+                float ms = 0.f;
+                ck(cudaEventElapsedTime(&ms, rc.a, rc.b), "cudaEventElapsedTime");
+                acc_ms[rc.cls] += ms;
+                acc_bytes[rc.cls] += rc.bytes;
+                acc_launches[rc.cls] += 1;
+            }
+        }
+        if (recycle) {
+            for (Rec& rc : v)
+                if (rc.a) {
+                    ev_pool.push_back(rc.a);
+                    ev_pool.push_back(rc.b);
+                }
+            v.clear();
+        }
+    }
+    void drop_graph() {
+        if (graph) cudaGraphExecDestroy(graph);
+        graph = nullptr;
+        for (Rec& rc : rec_graph)
+            if (rc.a) {
+                ev_pool.push_back(rc.a);
+                ev_pool.push_back(rc.b);
+            }
+        rec_graph.clear();
+    }
 
     // ---------------------------------------------------------------- launches
+    int mat_class(const Sell& M) const {
+        if (M.val == lv[0].A.val) return AMG_PROF_A0_PASS;
+        for (const auto& L : lv)
+            if (M.val == L.A.val) return AMG_PROF_A_COARSE;
+        return AMG_PROF_TRANSFER;
+    }
     template <int U, class Op>
-    void rows(const Sell& M, const Op& op, const int32_t* gate, bool stream_loads, const char* what) {
+    void rows(const Sell& M, const Op& op, const int32_t* gate, bool stream_loads) {
         const int g = grid_for(M.nrows);
         if (stream_loads)
             sell_rows<U, true, Op><<<g, kBlock, 0, stream>>>(M, op, gate, red);
         else
             sell_rows<U, false, Op><<<g, kBlock, 0, stream>>>(M, op, gate, red);
-        post_launch(what);
     }
     template <class Op>
     void rows_auto(const Sell& M, int64_t nnz, const Op& op, const int32_t* gate, const char* what) {
@@ -478,15 +576,18 @@ struct Handle {
         // it cached so coarse levels stay L2-resident across cycles
         const bool big = nnz * 12 > (int64_t)48 << 20;
         const double avg = M.nrows ? (double)nnz / (double)M.nrows : 0.0;
-        if (avg <= 8.5)
-            rows<8>(M, op, gate, big, what);
-        else
-            rows<4>(M, op, gate, big, what);
+        const double bytes = 12.0 * nnz + 4.0 * M.nrows + 8.0 * M.ncols * Op::GATHER + 8.0 * M.nrows * Op::ROWV;
+        launch(mat_class(M), bytes, what, [&] {
+            if (avg <= 8.5)
+                rows<8>(M, op, gate, big);
+            else
+                rows<4>(M, op, gate, big);
+        });
     }
     template <class Op>
     void vec(int64_t n, const Op& op, const int32_t* gate, const char* what) {
-        vec_kernel<Op><<<grid_for(n), kBlock, 0, stream>>>(n, op, gate, red);
-        post_launch(what);
+        launch(AMG_PROF_VECTOR, 8.0 * n * Op::STREAMS, what,
+               [&] { vec_kernel<Op><<<grid_for(n), kBlock, 0, stream>>>(n, op, gate, red); });
     }
 
     // ---------------------------------------------------------------- V-cycle
@@ -511,8 +612,8 @@ bool Handle::vcycle(int l, const double* f, double* out, const int32_t* gate, co
     if (l == nlev - 1) {  // coarsest: out = A_L^-1 f
         const int64_t warps = std::min<int64_t>(L.n, (int64_t)num_sms * 64);
         const int g = (int)std::max<int64_t>(1, (warps * 32 + kBlock - 1) / kBlock);
-        dense_gemv<<<g, kBlock, 0, stream>>>(L.n, coarse_inv, f, out, gate);
-        post_launch("coarse gemv");
+        launch(AMG_PROF_COARSE_SOLVE, 8.0 * L.n * L.n + 16.0 * L.n, "coarse gemv",
+               [&] { dense_gemv<<<g, kBlock, 0, stream>>>(L.n, coarse_inv, f, out, gate); });
         return false;
     }
     DevLevel& C = lv[l + 1];
@@ -643,6 +744,16 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
     const int64_t n = L0.n;
     const bool bicg = prm.solver == 1;
     const int64_t launches0 = launches;
+    std::fill(acc_ms, acc_ms + 8, 0.0);
+    std::fill(acc_bytes, acc_bytes + 8, 0.0);
+    std::fill(acc_launches, acc_launches + 8, 0);
+    alg_bytes = 0;
+    collect(rec_direct, 0, true);  // discard launches issued outside a solve
+    alg_bytes = 0;
+    std::fill(acc_ms, acc_ms + 8, 0.0);
+    std::fill(acc_bytes, acc_bytes + 8, 0.0);
+    std::fill(acc_launches, acc_launches + 8, 0);
+    cur_iter = -1;
     ck(cudaEventRecord(ev0, stream), "event");
     // scalars: maxiter in, everything else computed on the device
     std::memset(ks_host, 0, sizeof(KState));
@@ -658,6 +769,7 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
     }
     ck(cudaMemcpyAsync(ks_host, ks, sizeof(KState), cudaMemcpyDeviceToHost, stream), "ks read");
     ck(cudaStreamSynchronize(stream), "sync");
+    collect(rec_direct, 0, true);
     if (ks_host->nf == 0.0) {  // zero right-hand side: x = 0
         ck(cudaMemsetAsync(x, 0, n * sizeof(double), stream), "memset");
         ck(cudaStreamSynchronize(stream), "sync");
@@ -665,55 +777,64 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
         *rel = 0.0;
         stats = amg_solve_stats{};
         stats.kernel_launches = launches - launches0;
+        stats.alg_bytes = alg_bytes;
         return AMG_OK;
     }
 
     // Krylov loop: two iterations per host round trip, replayed from a CUDA
     // graph; kernels of iterations past convergence exit at their gate.
     const bool use_graph = prm.use_graph && !sync_debug;
+    auto two_iterations = [&] {
+        for (int k = 0; k < 2; ++k) {
+            cur_iter = k;
+            if (bicg)
+                bicgstab_iteration(x);
+            else
+                cg_iteration(x, k);
+        }
+        cur_iter = -1;
+    };
     while (!ks_host->done) {
+        const int iter_before = ks_host->iter;
         if (use_graph) {
-            if (!graph || graph_x != x) {
-                if (graph) {
-                    cudaGraphExecDestroy(graph);
-                    graph = nullptr;
-                }
+            if (!graph || graph_x != x || graph_prof_mask != prof_mask) {
+                drop_graph();
                 cudaGraph_t g;
                 const int64_t before = launches;
                 ck(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "capture");
-                if (bicg) {
-                    bicgstab_iteration(x);
-                    bicgstab_iteration(x);
-                } else {
-                    cg_iteration(x, 0);
-                    cg_iteration(x, 1);
+                capturing = true;
+                try {
+                    two_iterations();
+                } catch (...) {
+                    capturing = false;
+                    cudaStreamEndCapture(stream, &g);
+                    throw;
                 }
+                capturing = false;
                 ck(cudaStreamEndCapture(stream, &g), "end capture");
                 graph_kernels = launches - before;
                 launches = before;
                 ck(cudaGraphInstantiate(&graph, g, 0), "instantiate");
                 cudaGraphDestroy(g);
                 graph_x = x;
+                graph_prof_mask = prof_mask;
             }
             ck(cudaGraphLaunch(graph, stream), "graph launch");
             launches += graph_kernels;
         } else {
-            if (bicg) {
-                bicgstab_iteration(x);
-                bicgstab_iteration(x);
-            } else {
-                cg_iteration(x, 0);
-                cg_iteration(x, 1);
-            }
+            two_iterations();
         }
         ck(cudaMemcpyAsync(ks_host, ks, sizeof(KState), cudaMemcpyDeviceToHost, stream), "ks read");
         ck(cudaStreamSynchronize(stream), "sync");
+        const int ran = ks_host->iter - iter_before + (ks_host->done && ks_host->status ? 1 : 0);
+        collect(use_graph ? rec_graph : rec_direct, ran, !use_graph);
     }
     // true residual |f - A x| / |f|
     rows_auto(L0.A, L0.nnzA, OpResidual<1, FinTrueRes>{x, f, r, FinTrueRes{ks}}, nullptr, "true res");
     ck(cudaEventRecord(ev1, stream), "event");
     ck(cudaMemcpyAsync(ks_host, ks, sizeof(KState), cudaMemcpyDeviceToHost, stream), "ks read");
     ck(cudaStreamSynchronize(stream), "sync");
+    collect(rec_direct, 0, true);
     *iters = ks_host->iter;
     *rel = ks_host->true_res / ks_host->nf;
     float ms = 0;
@@ -725,6 +846,12 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
     stats.kernel_launches = launches - launches0;
     stats.solve_ms = ms;
     stats.rel_resid = *rel;
+    stats.alg_bytes = alg_bytes;
+    for (int c = 0; c < 8; ++c) {
+        stats.prof_ms[c] = acc_ms[c];
+        stats.prof_bytes[c] = acc_bytes[c];
+        stats.prof_launches[c] = acc_launches[c];
+    }
     if (ks_host->status == AMG_BREAKDOWN) {
         g_err = bicg ? "BiCGStab breakdown" : "CG breakdown: (r, Mr) <= 0 or (p, Ap) <= 0";
         stats.status = AMG_BREAKDOWN;
@@ -1066,17 +1193,14 @@ amg_status amg_set_stream(amg_handle h, void* stream) {
     // the legacy default stream cannot be captured into a graph: keep the
     // handle's own blocking stream, which is ordered with it implicitly
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : h->h->own_stream;
-    if (h->h->stream != s && h->h->graph) {
-        cudaGraphExecDestroy(h->h->graph);
-        h->h->graph = nullptr;
-    }
+    if (h->h->stream != s) h->h->drop_graph();
     h->h->stream = s;
     return AMG_OK;
 }
 
-amg_status amg_set_profile(amg_handle h, int32_t on) {
+amg_status amg_set_profile(amg_handle h, int32_t mask) {
     if (!h || !h->h) return set_error(AMG_E_INVALID_ARG, "NULL handle");
-    h->h->profile = on != 0;
+    h->h->prof_mask = mask & 0xff;
     return AMG_OK;
 }
 
@@ -1141,19 +1265,7 @@ amg_status amg_export_level(amg_handle h, int32_t l, const amg_level_export* out
 
 amg_status amg_solve_stats_get(amg_handle h, amg_solve_stats* out) {
     if (!h || !h->h || !out) return set_error(AMG_E_INVALID_ARG, "NULL argument");
-    const Handle& H = *h->h;
-    *out = H.stats;
-    // algorithmic bytes of the solve: per iteration V-cycle(s) + outer updates
-    double vc = 0;
-    for (const auto& L : H.lv) vc += L.alg_bytes;
-    const double n = (double)H.lv[0].n, z = (double)H.lv[0].nnzA;
-    const double outer_cg = (12 * z + 4 * n + 32 * n) + 48 * n;  // a7 + a8
-    const double outer_bi = 2 * (12 * z + 4 * n + 24 * n) + 24 * n + 24 * n + 72 * n;
-    const double init = 8 * n + 2 * (12 * z + 4 * n + 24 * n);  // |f|, r0, true residual
-    if (H.prm.solver == 1)
-        out->alg_bytes = init + out->vcycles * vc + out->iters * outer_bi;
-    else
-        out->alg_bytes = init + out->iters * (vc + outer_cg);
+    *out = h->h->stats;
     return AMG_OK;
 }
 

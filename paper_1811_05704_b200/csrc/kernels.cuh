@@ -198,8 +198,13 @@ __global__ void __launch_bounds__(kBlock) dense_gemv(int64_t n, const double* __
                                                      const int32_t* gate);
 
 // ----------------------------------------------------------------- epilogue ops
+// Each op declares its algorithmic traffic: a pass over M (rows x
+// cols, nnz) moves 12 nnz + 4 rows (CSR-equivalent matrix bytes) + 8 cols per
+// gathered vector (each read once, ideal reuse) + 8 rows per row-indexed vector
+// read or written.
 // y = A x
 struct OpSpmv {
+    static constexpr int GATHER = 1, ROWV = 1;  // vectors gathered / row-indexed (bytes model)
     static constexpr int NDOT = 0;
     static constexpr bool NEED_DIAG = false;
     const double* x;
@@ -213,6 +218,7 @@ struct OpSpmv {
 // y = f - A x  [+ (y, y)]
 template <int ND, class Fin>
 struct OpResidual {
+    static constexpr int GATHER = 1, ROWV = 2;  // vectors gathered / row-indexed (bytes model)
     static constexpr int NDOT = ND;
     static constexpr bool NEED_DIAG = false;
     const double* x;
@@ -231,6 +237,7 @@ struct OpResidual {
 // Zero-start smoother + residual (a1): with x = m o f (the first SPAI-0/Jacobi
 // sweep from x = 0), t = f - A x, computing x_j = m_j f_j inside the gather.
 struct OpRes0 {
+    static constexpr int GATHER = 2, ROWV = 1;  // vectors gathered / row-indexed (bytes model)
     static constexpr int NDOT = 0;
     static constexpr bool NEED_DIAG = false;
     const double* m;
@@ -245,6 +252,7 @@ struct OpRes0 {
 // Damped-Jacobi / SPAI-0 sweep (a6): xo = x + m o (f - A x), optional (f, xo).
 template <int ND, class Fin>
 struct OpRelax {
+    static constexpr int GATHER = 1, ROWV = 3;  // vectors gathered / row-indexed (bytes model)
     static constexpr int NDOT = ND;
     static constexpr bool NEED_DIAG = false;
     const double* x;
@@ -264,6 +272,7 @@ struct OpRelax {
 
 // Prolongation-correction after a zero-start sweep (a5): x = m o f + P e.
 struct OpProl0 {
+    static constexpr int GATHER = 1, ROWV = 3;  // vectors gathered / row-indexed (bytes model)
     static constexpr int NDOT = 0;
     static constexpr bool NEED_DIAG = false;
     const double* e;
@@ -278,6 +287,7 @@ struct OpProl0 {
 
 // General prolongation-correction: x = x + P e (x updated in place, row-local).
 struct OpProlAdd {
+    static constexpr int GATHER = 1, ROWV = 2;  // vectors gathered / row-indexed (bytes model)
     static constexpr int NDOT = 0;
     static constexpr bool NEED_DIAG = false;
     const double* e;
@@ -292,6 +302,7 @@ struct OpProlAdd {
 // the row itself); p = alpha r + beta p (first step: p = alpha r); xo = x + p.
 template <int ND, class Fin>
 struct OpCheb {
+    static constexpr int GATHER = 1, ROWV = 4;  // vectors gathered / row-indexed (bytes model)
     static constexpr int NDOT = ND;
     static constexpr bool NEED_DIAG = true;
     const double* x;
@@ -318,6 +329,7 @@ struct OpCheb {
 // sigma = (p', q).
 template <class Fin>
 struct OpCgDir {
+    static constexpr int GATHER = 2, ROWV = 2;  // vectors gathered / row-indexed (bytes model)
     static constexpr int NDOT = 1;
     static constexpr bool NEED_DIAG = false;
     const double* z;
@@ -340,6 +352,7 @@ struct OpCgDir {
 // y = A x with dots: ND = 1: (w, y); ND = 2: (y, y), (y, w).
 template <int ND, class Fin>
 struct OpSpmvDot {
+    static constexpr int GATHER = 1, ROWV = 2;  // vectors gathered / row-indexed (bytes model)
     static constexpr int NDOT = ND;
     static constexpr bool NEED_DIAG = false;
     const double* x;
