@@ -199,9 +199,9 @@ class Hierarchy:
             self.device = torch.device("cuda", self.prm.device)
 
     def close(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.amg_destroy(self._h)
-            self._h = None
+        self._h = None
 
     __del__ = close
 
