@@ -344,49 +344,63 @@ struct HostSell {
     std::vector<double> val;
 };
 
-// CSR -> SELL-32 (see kernels.cuh).
-HostSell to_sell(const Csr& A) {
+// CSR -> SELL-C, slice height C (see kernels.cuh): entry k of row s*C + r at
+// sptr[s] + k*C + r.
+HostSell to_sell(const Csr& A, int C = 32) {
     HostSell S;
     S.nrows = A.nrows;
     S.ncols = A.ncols;
-    S.nslices = (A.nrows + 31) / 32;
+    S.nslices = (A.nrows + C - 1) / C;
     S.sptr.assign(S.nslices + 1, 0);
     for (int64_t s = 0; s < S.nslices; ++s) {
         int64_t w = 0;
-        for (int64_t r = s * 32; r < std::min<int64_t>(A.nrows, s * 32 + 32); ++r)
+        for (int64_t r = s * C; r < std::min<int64_t>(A.nrows, s * C + C); ++r)
             w = std::max<int64_t>(w, A.ptr[r + 1] - A.ptr[r]);
-        S.sptr[s + 1] = S.sptr[s] + 32 * w;
+        S.sptr[s + 1] = S.sptr[s] + C * w;
     }
     S.col.assign(S.sptr[S.nslices], 0);
     S.val.assign(S.sptr[S.nslices], 0.0);
 #pragma omp parallel for schedule(static)
     for (int64_t s = 0; s < S.nslices; ++s) {
-        const int64_t w = (S.sptr[s + 1] - S.sptr[s]) / 32;
-        for (int lane = 0; lane < 32; ++lane) {
-            const int64_t r = s * 32 + lane;
+        const int64_t w = (S.sptr[s + 1] - S.sptr[s]) / C;
+        for (int lane = 0; lane < C; ++lane) {
+            const int64_t r = s * C + lane;
             int64_t len = 0;
             int32_t last = 0;
             if (r < A.nrows) {
                 len = A.ptr[r + 1] - A.ptr[r];
                 for (int64_t k = 0; k < len; ++k) {
-                    S.col[S.sptr[s] + 32 * k + lane] = A.col[A.ptr[r] + k];
-                    S.val[S.sptr[s] + 32 * k + lane] = A.val[A.ptr[r] + k];
+                    S.col[S.sptr[s] + C * k + lane] = A.col[A.ptr[r] + k];
+                    S.val[S.sptr[s] + C * k + lane] = A.val[A.ptr[r] + k];
                 }
                 if (len > 0) last = A.col[A.ptr[r] + len - 1];
             }
             for (int64_t k = len; k < w; ++k) {
-                S.col[S.sptr[s] + 32 * k + lane] = last;
-                S.val[S.sptr[s] + 32 * k + lane] = 0.0;
+                S.col[S.sptr[s] + C * k + lane] = last;
+                S.val[S.sptr[s] + C * k + lane] = 0.0;
             }
         }
     }
     return S;
 }
 
+// A device matrix in the format chosen for it.
+enum class Fmt { CSR, SELL, TMA };
+
+struct DMat {
+    Fmt fmt = Fmt::CSR;
+    bool is_csr = true;
+    Sell sell;
+    SellTma tma;
+    int64_t sell_wmax = 0;  // widest slice
+    CsrDev csr;
+    int64_t nrows = 0, ncols = 0, nnz = 0, stored = 0;
+};
+
 struct DevLevel {
     int64_t n = 0, nc = 0;
     int64_t nnzA = 0, nnzP = 0, padA = 0;
-    Sell A, P, R;
+    DMat A, P, R;
     double* m = nullptr;     // SPAI-0 / Jacobi diagonal
     double* diag = nullptr;  // a_ii (Chebyshev)
     double* f = nullptr;     // right-hand side (levels >= 1)
@@ -556,32 +570,75 @@ struct Handle {
     }
 
     // ---------------------------------------------------------------- launches
-    int mat_class(const Sell& M) const {
-        if (M.val == lv[0].A.val) return AMG_PROF_A0_PASS;
+    int mat_class(const DMat& M) const {
+        if (&M == &lv[0].A) return AMG_PROF_A0_PASS;
         for (const auto& L : lv)
-            if (M.val == L.A.val) return AMG_PROF_A_COARSE;
+            if (&M == &L.A) return AMG_PROF_A_COARSE;
         return AMG_PROF_TRANSFER;
     }
-    template <int U, class Op>
-    void rows(const Sell& M, const Op& op, const int32_t* gate, bool stream_loads) {
-        const int g = grid_for(M.nrows);
+    template <int U, bool PIPE, class Op>
+    void rows_sell(const Sell& M, const Op& op, const int32_t* gate, bool stream_loads) {
+        const int g = (int)std::max<int64_t>(
+            1, std::min<int64_t>((M.nrows + kBlock - 1) / kBlock, (int64_t)num_sms * (PIPE ? 4 : 6)));
         if (stream_loads)
-            sell_rows<U, true, Op><<<g, kBlock, 0, stream>>>(M, op, gate, red);
+            sell_rows<U, true, PIPE, Op><<<g, kBlock, 0, stream>>>(M, op, gate, red);
         else
-            sell_rows<U, false, Op><<<g, kBlock, 0, stream>>>(M, op, gate, red);
+            sell_rows<U, false, PIPE, Op><<<g, kBlock, 0, stream>>>(M, op, gate, red);
+    }
+    template <int G, class Op>
+    void rows_csr(const CsrDev& M, const Op& op, const int32_t* gate, bool stream_loads) {
+        const int g = (int)std::max<int64_t>(1, std::min<int64_t>(M.nblocks, (int64_t)num_sms * 8));
+        if (stream_loads)
+            csr_rows<G, true, Op><<<g, kBlock, 0, stream>>>(M, op, gate, red);
+        else
+            csr_rows<G, false, Op><<<g, kBlock, 0, stream>>>(M, op, gate, red);
+    }
+    template <int T, bool STREAM, class Op>
+    void rows_tma_impl(const SellTma& M, const Op& op, const int32_t* gate) {
+        auto kern = sell_tma<T, STREAM, Op>;
+        const size_t smem = (size_t)kTmaStages * M.tile_ent * 12 + 2 * kTmaStages * 8;
+        static size_t configured = 0;  // per instantiation
+        if (smem > configured) {
+            ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+            configured = smem;
+        }
+        const int g = (int)std::max<int64_t>(1, std::min<int64_t>(M.ntiles, (int64_t)num_sms * kTmaBlocksPerSM));
+        kern<<<g, kTmaThreads, smem, stream>>>(M, op, gate, red);
+    }
+    template <int T, class Op>
+    void rows_tma(const SellTma& M, const Op& op, const int32_t* gate, bool stream_loads) {
+        if (stream_loads)
+            rows_tma_impl<T, true>(M, op, gate);
+        else
+            rows_tma_impl<T, false>(M, op, gate);
     }
     template <class Op>
-    void rows_auto(const Sell& M, int64_t nnz, const Op& op, const int32_t* gate, const char* what) {
-        // levels too big for L2 stream their matrix (evict-first); the rest keep
-        // it cached so coarse levels stay L2-resident across cycles
-        const bool big = nnz * 12 > (int64_t)48 << 20;
-        const double avg = M.nrows ? (double)nnz / (double)M.nrows : 0.0;
-        const double bytes = 12.0 * nnz + 4.0 * M.nrows + 8.0 * M.ncols * Op::GATHER + 8.0 * M.nrows * Op::ROWV;
+    void rows_auto(const DMat& M, const Op& op, const int32_t* gate, const char* what) {
+        // matrices too big for L2 stream their entries (evict-first); the rest
+        // keep them cached so coarse levels stay L2-resident across cycles
+        const bool big = M.nnz * 12 > (int64_t)48 << 20;
+        const double bytes = 12.0 * M.nnz + 4.0 * M.nrows + 8.0 * M.ncols * Op::GATHER + 8.0 * M.nrows * Op::ROWV;
         launch(mat_class(M), bytes, what, [&] {
-            if (avg <= 8.5)
-                rows<8>(M, op, gate, big);
-            else
-                rows<4>(M, op, gate, big);
+            if (M.fmt == Fmt::TMA) {
+                switch (M.tma.T) {
+                    case 1: rows_tma<1>(M.tma, op, gate, big); break;
+                    case 2: rows_tma<2>(M.tma, op, gate, big); break;
+                    case 4: rows_tma<4>(M.tma, op, gate, big); break;
+                    default: rows_tma<8>(M.tma, op, gate, big); break;
+                }
+            } else if (M.is_csr) {
+                switch (M.csr.G) {
+                    case 1: rows_csr<1>(M.csr, op, gate, big); break;
+                    case 2: rows_csr<2>(M.csr, op, gate, big); break;
+                    case 4: rows_csr<4>(M.csr, op, gate, big); break;
+                    case 8: rows_csr<8>(M.csr, op, gate, big); break;
+                    default: rows_csr<16>(M.csr, op, gate, big); break;
+                }
+            } else if (M.sell_wmax <= 8) {
+                rows_sell<8, false>(M.sell, op, gate, big);
+            } else {
+                rows_sell<8, true>(M.sell, op, gate, big);
+            }
         });
     }
     template <class Op>
@@ -628,17 +685,17 @@ bool Handle::vcycle(int l, const double* f, double* out, const int32_t* gate, co
     if (!cheb) {
         if (npre == 0) {
             ck(cudaMemsetAsync(x, 0, L.n * sizeof(double), stream), "memset");
-            rows_auto(L.A, L.nnzA, OpResidual<0, NoFin>{x, f, L.t, {}}, gate, "residual");
+            rows_auto(L.A, OpResidual<0, NoFin>{x, f, L.t, {}}, gate, "residual");
         } else if (npre == 1) {
             x_is_mf = true;  // fused: t = f - A (m o f)
-            rows_auto(L.A, L.nnzA, OpRes0{L.m, f, L.t, {}}, gate, "res0");
+            rows_auto(L.A, OpRes0{L.m, f, L.t, {}}, gate, "res0");
         } else {
             vec(L.n, VMulDiag{L.m, f, x, {}}, gate, "x=mf");
             for (int s = 1; s < npre; ++s) {
-                rows_auto(L.A, L.nnzA, OpRelax<0, NoFin>{x, L.m, f, y, {}}, gate, "relax");
+                rows_auto(L.A, OpRelax<0, NoFin>{x, L.m, f, y, {}}, gate, "relax");
                 std::swap(x, y);
             }
-            rows_auto(L.A, L.nnzA, OpResidual<0, NoFin>{x, f, L.t, {}}, gate, "residual");
+            rows_auto(L.A, OpResidual<0, NoFin>{x, f, L.t, {}}, gate, "residual");
         }
     } else {
         if (npre == 0) {
@@ -650,8 +707,8 @@ bool Handle::vcycle(int l, const double* f, double* out, const int32_t* gate, co
                         vec(L.n, VCheb0{f, L.diag, L.p, x, L.cheb_alpha[0], prm.cheb_scaled, {}}, gate,
                             "cheb0");
                     } else {
-                        rows_auto(L.A, L.nnzA,
-                                  OpCheb<0, NoFin>{x, f, L.p, y, L.cheb_alpha[k], L.cheb_beta[k],
+                        rows_auto(L.A,
+                                  OpCheb<0, NoFin>{x, f, L.diag, L.p, y, L.cheb_alpha[k], L.cheb_beta[k],
                                                    prm.cheb_scaled, k == 0, {}},
                                   gate, "cheb");
                         std::swap(x, y);
@@ -659,16 +716,16 @@ bool Handle::vcycle(int l, const double* f, double* out, const int32_t* gate, co
                 }
             }
         }
-        rows_auto(L.A, L.nnzA, OpResidual<0, NoFin>{x, f, L.t, {}}, gate, "residual");
+        rows_auto(L.A, OpResidual<0, NoFin>{x, f, L.t, {}}, gate, "residual");
     }
 
     // ---- restriction f_c = R t, coarse solve, prolongation x += P x_c
-    rows_auto(L.R, L.nnzP, OpSpmv{L.t, C.f}, gate, "restrict");
+    rows_auto(L.R, OpSpmv{L.t, C.f}, gate, "restrict");
     vcycle_plain(l + 1, C.f, C.o, gate);
     if (x_is_mf)
-        rows_auto(L.P, L.nnzP, OpProl0{C.o, L.m, f, x, {}}, gate, "prolong0");
+        rows_auto(L.P, OpProl0{C.o, L.m, f, x, {}}, gate, "prolong0");
     else
-        rows_auto(L.P, L.nnzP, OpProlAdd{C.o, x, {}}, gate, "prolong");
+        rows_auto(L.P, OpProlAdd{C.o, x, {}}, gate, "prolong");
 
     // ---- post-smoothing; the last sweep writes `out`
     if (!cheb) {
@@ -679,9 +736,9 @@ bool Handle::vcycle(int l, const double* f, double* out, const int32_t* gate, co
         for (int s = 0; s < npost; ++s) {
             double* dst = (s == npost - 1) ? out : y;
             if (s == npost - 1 && rho_fin)
-                rows_auto(L.A, L.nnzA, OpRelax<1, FinT>{x, L.m, f, dst, *rho_fin}, gate, "relax+dot");
+                rows_auto(L.A, OpRelax<1, FinT>{x, L.m, f, dst, *rho_fin}, gate, "relax+dot");
             else
-                rows_auto(L.A, L.nnzA, OpRelax<0, NoFin>{x, L.m, f, dst, {}}, gate, "relax");
+                rows_auto(L.A, OpRelax<0, NoFin>{x, L.m, f, dst, {}}, gate, "relax");
             if (dst == y) std::swap(x, y);
         }
         return rho_fin != nullptr;
@@ -695,13 +752,13 @@ bool Handle::vcycle(int l, const double* f, double* out, const int32_t* gate, co
             const bool lastk = (s == npost - 1) && (k == K - 1);
             double* dst = lastk ? out : y;
             if (lastk && rho_fin)
-                rows_auto(L.A, L.nnzA,
-                          OpCheb<1, FinT>{x, f, L.p, dst, L.cheb_alpha[k], L.cheb_beta[k], prm.cheb_scaled,
+                rows_auto(L.A,
+                          OpCheb<1, FinT>{x, f, L.diag, L.p, dst, L.cheb_alpha[k], L.cheb_beta[k], prm.cheb_scaled,
                                           k == 0, *rho_fin},
                           gate, "cheb+dot");
             else
-                rows_auto(L.A, L.nnzA,
-                          OpCheb<0, NoFin>{x, f, L.p, dst, L.cheb_alpha[k], L.cheb_beta[k], prm.cheb_scaled,
+                rows_auto(L.A,
+                          OpCheb<0, NoFin>{x, f, L.diag, L.p, dst, L.cheb_alpha[k], L.cheb_beta[k], prm.cheb_scaled,
                                            k == 0, {}},
                           gate, "cheb");
             if (!lastk) std::swap(x, y);
@@ -720,7 +777,7 @@ void Handle::cg_iteration(double* x, int parity) {
     DevLevel& L0 = lv[0];
     FinRho frho{ks};
     if (!vcycle<FinRho>(0, r, z, gate, &frho)) vec(L0.n, VDot<FinRho>{r, z, frho}, gate, "dot(r,z)");
-    rows_auto(L0.A, L0.nnzA, OpCgDir<FinSigma>{z, pold, pnew, q, ks, 0.0, FinSigma{ks}}, gate, "cg dir");
+    rows_auto(L0.A, OpCgDir<FinSigma>{z, pold, pnew, q, ks, 0.0, FinSigma{ks}}, gate, "cg dir");
     vec(L0.n, VCgUpdate{x, r, pnew, q, ks, 0.0, FinCgUpdate{ks}}, gate, "cg update");
 }
 
@@ -731,10 +788,10 @@ void Handle::bicgstab_iteration(double* x) {
     DevLevel& L0 = lv[0];
     vec(L0.n, VBiP{r, v, pa, ks, 0, 0, 0, {}}, gate, "bicg p");
     vcycle_plain(0, pa, ph, gate);
-    rows_auto(L0.A, L0.nnzA, OpSpmvDot<1, FinBiAlpha>{ph, rhat, v, FinBiAlpha{ks}}, gate, "v=A ph");
+    rows_auto(L0.A, OpSpmvDot<1, FinBiAlpha>{ph, rhat, v, FinBiAlpha{ks}}, gate, "v=A ph");
     vec(L0.n, VBiS{r, v, s, ks, 0.0, FinBiS{ks}}, gate, "bicg s");
     vcycle_plain(0, s, sh, gate2);
-    rows_auto(L0.A, L0.nnzA, OpSpmvDot<2, FinBiOmega>{sh, s, tv, FinBiOmega{ks}}, gate2, "t=A sh");
+    rows_auto(L0.A, OpSpmvDot<2, FinBiOmega>{sh, s, tv, FinBiOmega{ks}}, gate2, "t=A sh");
     vec(L0.n, VBiX{x, r, ph, sh, s, tv, rhat, ks, 0, 0, 0, FinBiX{ks}}, gate, "bicg x");
 }
 
@@ -760,7 +817,7 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
     ks_host->maxiter = maxiter;
     ck(cudaMemcpyAsync(ks, ks_host, sizeof(KState), cudaMemcpyHostToDevice, stream), "ks init");
     vec(n, VNorm2{f, FinNorm{ks, tol}}, nullptr, "norm f");
-    rows_auto(L0.A, L0.nnzA, OpResidual<1, FinInitRes>{x, f, r, FinInitRes{ks}}, nullptr, "r0");
+    rows_auto(L0.A, OpResidual<1, FinInitRes>{x, f, r, FinInitRes{ks}}, nullptr, "r0");
     ck(cudaMemsetAsync(pa, 0, n * sizeof(double), stream), "memset");
     ck(cudaMemsetAsync(pb, 0, n * sizeof(double), stream), "memset");
     if (bicg) {
@@ -830,7 +887,7 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
         collect(use_graph ? rec_graph : rec_direct, ran, !use_graph);
     }
     // true residual |f - A x| / |f|
-    rows_auto(L0.A, L0.nnzA, OpResidual<1, FinTrueRes>{x, f, r, FinTrueRes{ks}}, nullptr, "true res");
+    rows_auto(L0.A, OpResidual<1, FinTrueRes>{x, f, r, FinTrueRes{ks}}, nullptr, "true res");
     ck(cudaEventRecord(ev1, stream), "event");
     ck(cudaMemcpyAsync(ks_host, ks, sizeof(KState), cudaMemcpyDeviceToHost, stream), "ks read");
     ck(cudaStreamSynchronize(stream), "sync");
@@ -866,17 +923,110 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
 
 namespace {
 
-Sell upload_sell(Handle& H, const Csr& A, int64_t* bytes, int64_t* padded) {
-    HostSell S = to_sell(A);
-    Sell d;
-    d.nrows = S.nrows;
-    d.ncols = S.ncols;
-    d.nslices = S.nslices;
-    d.sptr = H.upload(S.sptr);
-    d.col = H.upload(S.col);
-    d.val = H.upload(S.val);
-    *bytes += (int64_t)(S.sptr.size() * 8 + S.col.size() * 12);
-    if (padded) *padded = (int64_t)S.col.size();
+// Matrix format policy: AMGB_FORMAT = auto (default) | csr | sell | tma.
+// auto: row-block CSR for matrices with < 65536 rows (coarse levels: few, long
+// rows); otherwise TMA-staged SELL-32 for narrow rows, SELL-32 for wide ones.
+Fmt pick_format(const Csr& A) {
+    const char* e = std::getenv("AMGB_FORMAT");
+    const std::string f = e ? e : "auto";
+    if (f == "csr") return Fmt::CSR;
+    if (f == "sell") return Fmt::SELL;
+    if (f == "tma") return Fmt::TMA;
+    if (A.nrows < 65536) return Fmt::CSR;
+    int64_t lmax = 0;
+    for (int64_t r = 0; r < A.nrows; ++r) lmax = std::max<int64_t>(lmax, A.ptr[r + 1] - A.ptr[r]);
+    // narrow rows (level-0 A, P): TMA-staged SELL-32, one thread per row.  Wide
+    // rows (coarse A, R): their gathers are L2-bound and one thread per row of a
+    // register-pipelined SELL-32 measured faster than T > 1 lanes per row.
+    return lmax <= 12 ? Fmt::TMA : Fmt::SELL;
+}
+
+// Row blocks of the CSR kernel: at most kEnt entries and a row cap chosen from
+// the mean row length; a row longer than kEnt forms a block of its own.
+std::vector<int32_t> row_blocks(const Csr& A, int G) {
+    const double avg = A.nrows ? (double)A.nnz() / (double)A.nrows : 0.0;
+    const int64_t cap = G > 1 ? kRowsMax : (avg < 4.0 ? 512 : 256);
+    std::vector<int32_t> b{0};
+    int64_t r = 0;
+    while (r < A.nrows) {
+        int64_t ents = 0, rows = 0;
+        if (A.ptr[r + 1] - A.ptr[r] > kEnt) {
+            ++r;
+        } else {
+            while (r < A.nrows && rows < cap && ents + (A.ptr[r + 1] - A.ptr[r]) <= kEnt) {
+                ents += A.ptr[r + 1] - A.ptr[r];
+                ++rows;
+                ++r;
+            }
+        }
+        b.push_back((int32_t)r);
+    }
+    return b;
+}
+
+DMat upload_mat(Handle& H, const Csr& A, int64_t* bytes) {
+    DMat d;
+    d.nrows = A.nrows;
+    d.ncols = A.ncols;
+    d.nnz = A.nnz();
+    if (d.nnz >= INT32_MAX) throw CudaError{"level has >= 2^31 nonzeros"};
+    d.fmt = pick_format(A);
+    d.is_csr = d.fmt == Fmt::CSR;
+    if (d.is_csr) {
+        const double avg = A.nrows ? (double)A.nnz() / (double)A.nrows : 0.0;
+        int G = 1;
+        if (avg >= 96) G = 16;
+        else if (avg >= 48) G = 8;
+        else if (avg >= 20) G = 4;
+        else if (avg >= 12) G = 2;
+        std::vector<int32_t> ptr32(A.ptr.begin(), A.ptr.end());
+        std::vector<int32_t> blocks = row_blocks(A, G);
+        d.csr.nrows = A.nrows;
+        d.csr.ncols = A.ncols;
+        d.csr.nnz = A.nnz();
+        d.csr.nblocks = (int64_t)blocks.size() - 1;
+        d.csr.G = G;
+        d.csr.ptr = H.upload(ptr32);
+        d.csr.col = H.upload(A.col);
+        d.csr.val = H.upload(A.val);
+        d.csr.brow = H.upload(blocks);
+        d.stored = d.nnz;
+        *bytes += (int64_t)(ptr32.size() * 4 + A.col.size() * 12 + blocks.size() * 4);
+    } else if (d.fmt == Fmt::SELL) {
+        HostSell S = to_sell(A, 32);
+        d.sell.nrows = S.nrows;
+        d.sell.ncols = S.ncols;
+        d.sell.nslices = S.nslices;
+        d.sell.sptr = H.upload(S.sptr);
+        d.sell.col = H.upload(S.col);
+        d.sell.val = H.upload(S.val);
+        d.stored = (int64_t)S.col.size();
+        for (int64_t q = 0; q < S.nslices; ++q) d.sell_wmax = std::max(d.sell_wmax, (S.sptr[q + 1] - S.sptr[q]) / 32);
+        *bytes += (int64_t)(S.sptr.size() * 8 + S.col.size() * 12);
+    } else {  // TMA-staged SELL-C: lanes per row T from the longest row, C = 32 / T
+        int64_t lmax = 0;
+        for (int64_t r = 0; r < A.nrows; ++r) lmax = std::max<int64_t>(lmax, A.ptr[r + 1] - A.ptr[r]);
+        const char* te_env = std::getenv("AMGB_TMA_T");
+        int T = lmax <= 12 ? 1 : lmax <= 24 ? 2 : lmax <= 48 ? 4 : 8;
+        if (te_env) T = std::atoi(te_env);
+        const int C = 32 / T;
+        HostSell S = to_sell(A, C);
+        SellTma& t = d.tma;
+        t.nrows = S.nrows;
+        t.ncols = S.ncols;
+        t.nslices = S.nslices;
+        t.T = T;
+        t.ntiles = (S.nslices + 7) / 8;
+        int64_t te = 0;
+        for (int64_t q = 0; q < t.ntiles; ++q)
+            te = std::max(te, S.sptr[std::min<int64_t>((q + 1) * 8, S.nslices)] - S.sptr[q * 8]);
+        t.tile_ent = (int32_t)(((std::max<int64_t>(te, 32) + 31) / 32) * 32);
+        t.sptr = H.upload(S.sptr);
+        t.col = H.upload(S.col);
+        t.val = H.upload(S.val);
+        d.stored = (int64_t)S.col.size();
+        *bytes += (int64_t)(S.sptr.size() * 8 + S.col.size() * 12);
+    }
     return d;
 }
 
@@ -1066,11 +1216,12 @@ amg_status amg_setup(int64_t n, const int64_t* ptr, const int32_t* col, const do
             DevLevel& L = H->lv[l];
             const bool coarsest = l == nlev - 1;
             if (!coarsest) {
-                L.A = upload_sell(*H, hl.A, &L.dev_bytes, &L.padA);
-                L.P = upload_sell(*H, hl.P, &L.dev_bytes, nullptr);
-                L.R = upload_sell(*H, hl.R, &L.dev_bytes, nullptr);
+                L.A = upload_mat(*H, hl.A, &L.dev_bytes);
+                L.P = upload_mat(*H, hl.P, &L.dev_bytes);
+                L.R = upload_mat(*H, hl.R, &L.dev_bytes);
+                L.padA = L.A.stored;
                 if (prm.relax != 2) L.m = H->upload(hl.m);
-                if (prm.relax == 2) L.diag = H->upload(hl.diag);
+                if (prm.relax == 2) L.diag = H->upload(hl.diag);  // Chebyshev D^-1 scaling
                 L.x = H->dalloc(L.n);
                 L.y = H->dalloc(L.n);
                 L.t = H->dalloc(L.n);
@@ -1089,7 +1240,8 @@ amg_status amg_setup(int64_t n, const int64_t* ptr, const int32_t* col, const do
         H->lv.back().dev_bytes += 8 * H->nL * H->nL;
         if (nlev == 1) {  // single level: the level-0 A is needed by the Krylov loop
             int64_t dummy = 0;
-            H->lv[0].A = upload_sell(*H, H->host.levels[0].A, &H->lv[0].dev_bytes, &H->lv[0].padA);
+            H->lv[0].A = upload_mat(*H, H->host.levels[0].A, &H->lv[0].dev_bytes);
+            H->lv[0].padA = H->lv[0].A.stored;
             (void)dummy;
         }
         const int64_t n = H->lv[0].n;
@@ -1282,19 +1434,19 @@ amg_status amg_level_op(amg_handle h, int32_t l, int32_t op, const double* x, co
         switch (op) {
             case AMG_OP_SPMV_A:
                 if (coarsest && nlev > 1) return set_error(AMG_E_INVALID_ARG, "coarsest A is stored dense");
-                H.rows_auto(L.A, L.nnzA, OpSpmv{x, y}, nullptr, "spmv A");
+                H.rows_auto(L.A, OpSpmv{x, y}, nullptr, "spmv A");
                 break;
             case AMG_OP_SPMV_P:
             case AMG_OP_SPMV_R:
                 if (coarsest) return set_error(AMG_E_INVALID_ARG, "no P/R on the coarsest level");
                 if (op == AMG_OP_SPMV_P)
-                    H.rows_auto(L.P, L.nnzP, OpSpmv{x, y}, nullptr, "spmv P");
+                    H.rows_auto(L.P, OpSpmv{x, y}, nullptr, "spmv P");
                 else
-                    H.rows_auto(L.R, L.nnzP, OpSpmv{x, y}, nullptr, "spmv R");
+                    H.rows_auto(L.R, OpSpmv{x, y}, nullptr, "spmv R");
                 break;
             case AMG_OP_RESIDUAL:
                 if (coarsest && nlev > 1) return set_error(AMG_E_INVALID_ARG, "coarsest A is stored dense");
-                H.rows_auto(L.A, L.nnzA, OpResidual<0, NoFin>{x, f, y, {}}, nullptr, "residual");
+                H.rows_auto(L.A, OpResidual<0, NoFin>{x, f, y, {}}, nullptr, "residual");
                 break;
             case AMG_OP_RELAX:
                 if (coarsest) return set_error(AMG_E_INVALID_ARG, "no smoother on the coarsest level");
@@ -1305,14 +1457,14 @@ amg_status amg_level_op(amg_handle h, int32_t l, int32_t op, const double* x, co
                     ck(cudaMemcpyAsync(a, x, L.n * sizeof(double), cudaMemcpyDeviceToDevice, H.stream), "copy");
                     for (int k = 0; k < H.prm.cheb_degree; ++k) {
                         double* dst = (k == H.prm.cheb_degree - 1) ? y : b;
-                        H.rows_auto(L.A, L.nnzA,
-                                    OpCheb<0, NoFin>{a, f, L.p, dst, L.cheb_alpha[k], L.cheb_beta[k],
+                        H.rows_auto(L.A,
+                                    OpCheb<0, NoFin>{a, f, L.diag, L.p, dst, L.cheb_alpha[k], L.cheb_beta[k],
                                                      H.prm.cheb_scaled, k == 0, {}},
                                     nullptr, "cheb");
                         std::swap(a, b);
                     }
                 } else {
-                    H.rows_auto(L.A, L.nnzA, OpRelax<0, NoFin>{x, L.m, f, y, {}}, nullptr, "relax");
+                    H.rows_auto(L.A, OpRelax<0, NoFin>{x, L.m, f, y, {}}, nullptr, "relax");
                 }
                 break;
             case AMG_OP_COARSE:

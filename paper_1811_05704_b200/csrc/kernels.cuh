@@ -66,7 +66,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 // reproducible run to run.
 template <int NV, class Fin>
 __device__ __forceinline__ void grid_reduce(double (&v)[NV], const Red& red, const Fin& fin) {
-    __shared__ double sh[NV][kBlock / kWarp];
+    __shared__ double sh[NV][32];
     __shared__ bool last;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int nw = blockDim.x >> 5;
@@ -129,50 +129,319 @@ __device__ __forceinline__ bool gated(const int32_t* gate) {
 
 // ----------------------------------------------------------------- SELL row kernel
 // One thread per row; U entries of the row are loaded before their gathers are
-// issued (bytes in flight), then accumulated in ascending column order.
-// Op supplies: NDOT (number of fused dot products), NEED_DIAG, prepare(),
-// gather(col) -> value of the input vector at col (may fuse a vector op, e.g.
-// m_j f_j or z_j + beta p_j), row(i, sum, diag, dots) -> epilogue, fin.
-template <int U, bool STREAM, class Op>
-__global__ void __launch_bounds__(kBlock) sell_rows(Sell A, Op op, const int32_t* gate, Red red) {
+// issued (bytes in flight), the next U entries are requested before this
+// chunk's products are accumulated (software pipelining), and the sum runs in
+// ascending column order.
+// Op supplies: NDOT (number of fused dot products), prepare(), load(i) -> the
+// row-local operands of the epilogue (Row), gather(col) -> value of the input
+// vector at col (may fuse a vector op, e.g. m_j f_j or z_j + beta p_j),
+// row(i, sum, Row, dots) -> epilogue, fin.
+// PIPE = false: all U entries of the (narrow, w <= U) row in one chunk, no
+// prefetch registers; launch bounds ask for >= 6 resident blocks (48 warps) so
+// enough loads are in flight per SM.
+template <int U, bool STREAM, bool PIPE, class Op>
+__global__ void __launch_bounds__(kBlock, PIPE ? 4 : 6) sell_rows(Sell A, Op op, const int32_t* gate, Red red) {
     if (gated(gate)) return;
     op.prepare();
-    double dots[Op::NDOT > 0 ? Op::NDOT : 1];
+    constexpr int ND = Op::NDOT > 0 ? Op::NDOT : 1;
+    double dots[ND];
 #pragma unroll
-    for (int k = 0; k < (Op::NDOT > 0 ? Op::NDOT : 1); ++k) dots[k] = 0.0;
+    for (int k = 0; k < ND; ++k) dots[k] = 0.0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < A.nrows; row += stride) {
+        // row-local epilogue operands are requested first, so their latency
+        // overlaps the matrix stream
+        const typename Op::Row rr = op.load(row);
         const int64_t s = row >> 5;
         const int lane = (int)(row & 31);
         const int64_t beg = A.sptr[s];
         const int w = (int)((A.sptr[s + 1] - beg) >> 5);
         const int32_t* cp = A.col + beg + lane;
         const double* vp = A.val + beg + lane;
-        double sum = 0.0, dg = 0.0;
-        for (int k0 = 0; k0 < w; k0 += U) {
-            int32_t c[U];
-            double v[U], xv[U];
+        double sum = 0.0;
+        int32_t c[U];
+        double v[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                if (k0 + u < w) {
-                    c[u] = ld_mat<STREAM>(cp + 32 * (k0 + u));
-                    v[u] = ld_mat<STREAM>(vp + 32 * (k0 + u));
-                } else {
-                    c[u] = 0;
-                    v[u] = 0.0;
-                }
-            }
+        for (int u = 0; u < U; ++u) {
+            c[u] = u < w ? ld_mat<STREAM>(cp + 32 * u) : 0;
+            v[u] = u < w ? ld_mat<STREAM>(vp + 32 * u) : 0.0;
+        }
+        if constexpr (!PIPE) {
+            double xv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) xv[u] = u < w ? op.gather(c[u]) : 0.0;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (u < w) sum = fma(v[u], xv[u], sum);
+        }
+        for (int k0 = 0; PIPE && k0 < w; k0 += U) {
+            double xv[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) xv[u] = (k0 + u < w) ? op.gather(c[u]) : 0.0;
+            // software pipelining: the next chunk's entries are in flight while
+            // this chunk's gathers complete
+            int32_t cn[U];
+            double vn[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                if (k0 + u < w) {
-                    sum = fma(v[u], xv[u], sum);
-                    if (Op::NEED_DIAG && c[u] == row && dg == 0.0) dg = v[u];
-                }
+                const int k = k0 + U + u;
+                cn[u] = k < w ? ld_mat<STREAM>(cp + 32 * k) : 0;
+                vn[u] = k < w ? ld_mat<STREAM>(vp + 32 * k) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (k0 + u < w) sum = fma(v[u], xv[u], sum);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                c[u] = cn[u];
+                v[u] = vn[u];
             }
         }
-        op.row(row, sum, dg, dots);
+        op.row(row, sum, rr, dots);
+    }
+    if constexpr (Op::NDOT > 0) grid_reduce<Op::NDOT>(dots, red, op.fin);
+}
+
+// ----------------------------------------------------------------- TMA-staged SELL-C kernel
+// The matrix stream is decoupled from the register file: a producer warp moves
+// whole tiles (8 consecutive slices; their col and val ranges are contiguous)
+// into a kTmaStages-deep shared-memory ring with cp.async.bulk (TMA bulk
+// copies, completion counted in bytes on an mbarrier), while 8 consumer warps
+// read entries from shared memory, issue the gathers and run the fused
+// epilogue.  Matrices are stored as SELL-C with slice height C = 32/T: warp w
+// owns slice w of the tile, lane l works on row l % C, entries k = l / C + T j
+// (T lanes per row).  Entry k of row r sits at slice_off + k C + r, so the 32
+// lanes of a warp read 32 consecutive words (conflict-free) and the T partial
+// sums of a row are combined with xor-shuffles in a fixed order.
+constexpr int kTmaStages = 2;
+constexpr int kTmaBlocksPerSM = 4;
+constexpr int kTmaThreads = kBlock + 32;  // 8 consumer warps + 1 producer warp
+
+struct SellTma {
+    int64_t nrows = 0, ncols = 0, nslices = 0, ntiles = 0;
+    const int64_t* sptr = nullptr;  // nslices + 1 element offsets (multiples of C)
+    const int32_t* col = nullptr;
+    const double* val = nullptr;
+    int32_t T = 1;          // lanes per row; slice height C = 32 / T
+    int32_t tile_ent = 0;   // capacity of one stage in entries (max over tiles)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+template <bool STREAM>
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar,
+                                         uint64_t policy) {
+    if constexpr (STREAM)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+            " [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+            "l"(src), "r"(bytes), "r"(mbar), "l"(policy)
+            : "memory");
+    else
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+            "l"(src), "r"(bytes), "r"(mbar)
+            : "memory");
+}
+
+template <int T, bool STREAM, class Op>
+__global__ void __launch_bounds__(kTmaThreads, kTmaBlocksPerSM) sell_tma(SellTma A, Op op, const int32_t* gate,
+                                                                         Red red) {
+    if (gated(gate)) return;
+    op.prepare();
+    constexpr int C = 32 / T;  // slice height
+    constexpr int NS = 8;      // slices per tile (one per consumer warp)
+    extern __shared__ __align__(128) unsigned char smem[];
+    // layout: kTmaStages x { val[tile_ent] (8 B), col[tile_ent] (4 B) } | barriers
+    const int te = A.tile_ent;
+    const size_t stage_bytes = (size_t)te * 12;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTmaStages * stage_bytes);  // full[S], empty[S]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kTmaStages; ++s) {
+            mbar_init(smem_u32(bars + s), 1);
+            mbar_init(smem_u32(bars + kTmaStages + s), kBlock / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    constexpr int ND = Op::NDOT > 0 ? Op::NDOT : 1;
+    double dots[ND];
+#pragma unroll
+    for (int k = 0; k < ND; ++k) dots[k] = 0.0;
+
+    if (warp == kBlock / 32) {  // ---------------- producer warp
+        if (lane == 0) {
+            uint64_t policy = 0;
+            if constexpr (STREAM) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+            int i = 0;
+            for (int64_t t = blockIdx.x; t < A.ntiles; t += gridDim.x, ++i) {
+                const int s = i % kTmaStages;
+                if (i >= kTmaStages) mbar_wait(smem_u32(bars + kTmaStages + s), ((i / kTmaStages) & 1) ^ 1);
+                const int64_t s0 = t * NS;
+                const int64_t s1 = s0 + NS < A.nslices ? s0 + NS : A.nslices;
+                const int64_t e0 = A.sptr[s0], e1 = A.sptr[s1];
+                const uint32_t n = (uint32_t)(e1 - e0);
+                const uint32_t full = smem_u32(bars + s);
+                unsigned char* st = smem + (size_t)s * stage_bytes;
+                mbar_expect_tx(full, n * 12u);
+                bulk_g2s<STREAM>(smem_u32(st), A.val + e0, n * 8u, full, policy);
+                bulk_g2s<STREAM>(smem_u32(st + (size_t)te * 8), A.col + e0, n * 4u, full, policy);
+            }
+        }
+    } else {  // ------------------------------------ consumer warps
+        const int r = lane % C;  // row within the slice
+        const int pt = lane / C; // part of the row
+        int i = 0;
+        for (int64_t t = blockIdx.x; t < A.ntiles; t += gridDim.x, ++i) {
+            const int s = i % kTmaStages;
+            const int64_t slice = t * NS + warp;
+            const int64_t row = slice * C + r;
+            const bool has_row = slice < A.nslices && row < A.nrows;
+            typename Op::Row rr{};
+            if (pt == 0 && has_row) rr = op.load(row);  // in flight during the wait
+            int off = 0, w = 0;
+            if (slice < A.nslices) {
+                const int64_t e0 = A.sptr[slice];
+                off = (int)(e0 - A.sptr[t * NS]);
+                w = (int)((A.sptr[slice + 1] - e0) / C);
+            }
+            mbar_wait(smem_u32(bars + s), (i / kTmaStages) & 1);
+            const double* sv = reinterpret_cast<const double*>(smem + (size_t)s * stage_bytes) + off + r;
+            const int32_t* sc =
+                reinterpret_cast<const int32_t*>(smem + (size_t)s * stage_bytes + (size_t)te * 8) + off + r;
+            double sum = 0.0;
+            for (int k0 = pt; k0 < w; k0 += 8 * T) {
+                double xv[8];
+                int32_t c[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int k = k0 + u * T;
+                    c[u] = k < w ? sc[C * k] : 0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) xv[u] = (k0 + u * T < w) ? op.gather(c[u]) : 0.0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int k = k0 + u * T;
+                    if (k < w) sum = fma(sv[C * k], xv[u], sum);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(bars + kTmaStages + s));  // stage free
+            if constexpr (T > 1) {
+#pragma unroll
+                for (int o = C; o < 32; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            }
+            if (pt == 0 && has_row) op.row(row, sum, rr, dots);
+        }
+    }
+    if constexpr (Op::NDOT > 0) grid_reduce<Op::NDOT>(dots, red, op.fin);
+}
+
+// ----------------------------------------------------------------- row-block CSR kernel
+// Padding-free alternative to SELL for any row-length mix ("CSR-stream").  The
+// rows are cut on the host into blocks of at most kEnt entries (and kRowsMax
+// rows).  Per block: (1) the block's contiguous [ptr[rb], ptr[re]) slice of col /
+// val is read with fully coalesced loads, kEnt/kBlock entries per thread, all
+// issued before their gathers, and the products a_ij * x_j go to shared memory;
+// (2) G threads per row sum the row's products (G = 1: one thread, ascending
+// order -- the same arithmetic as a plain CSR row loop) and run the epilogue.
+// A row longer than kEnt gets a block of its own and is reduced block-wide.
+// Persistent grid (grid-stride over row blocks) so fused dot products reduce
+// over a bounded number of partials.
+constexpr int kEnt = 2048;
+constexpr int kRowsMax = 512;
+
+struct CsrDev {
+    int64_t nrows = 0, ncols = 0, nnz = 0, nblocks = 0;
+    const int32_t* ptr = nullptr;   // nrows + 1 (nnz < 2^31 per level)
+    const int32_t* col = nullptr;
+    const double* val = nullptr;
+    const int32_t* brow = nullptr;  // nblocks + 1 first rows of the row blocks
+    int32_t G = 1;                  // threads per row in the summation phase
+};
+
+template <int G, bool STREAM, class Op>
+__global__ void __launch_bounds__(kBlock) csr_rows(CsrDev A, Op op, const int32_t* gate, Red red) {
+    if (gated(gate)) return;
+    op.prepare();
+    __shared__ double prod[kEnt];
+    constexpr int ND = Op::NDOT > 0 ? Op::NDOT : 1;
+    double dots[ND];
+#pragma unroll
+    for (int k = 0; k < ND; ++k) dots[k] = 0.0;
+    const int tid = threadIdx.x;
+    const int lig = tid & (G - 1);
+    const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << ((tid & 31) & ~(G - 1)));
+    for (int64_t b = blockIdx.x; b < A.nblocks; b += gridDim.x) {
+        const int rb = A.brow[b], re = A.brow[b + 1];
+        const int eb = A.ptr[rb], ne = A.ptr[re] - eb;
+        if (ne <= kEnt) {
+            constexpr int PER = kEnt / kBlock;
+            int32_t c[PER];
+            double v[PER];
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const int e = tid + k * kBlock;
+                if (e < ne) {
+                    c[k] = ld_mat<STREAM>(A.col + eb + e);
+                    v[k] = ld_mat<STREAM>(A.val + eb + e);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const int e = tid + k * kBlock;
+                if (e < ne) prod[e] = v[k] * op.gather(c[k]);
+            }
+            __syncthreads();
+            for (int r = rb + tid / G; r < re; r += kBlock / G) {
+                const typename Op::Row rr = op.load(r);
+                const int s0 = A.ptr[r] - eb, s1 = A.ptr[r + 1] - eb;
+                double s = 0.0;
+                for (int k = s0 + lig; k < s1; k += G) s += prod[k];
+                if constexpr (G > 1) {
+#pragma unroll
+                    for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(gmask, s, o);
+                }
+                if (lig == 0) op.row(r, s, rr, dots);
+            }
+            __syncthreads();
+        } else {  // one long row
+            double s = 0.0;
+            for (int e = tid; e < ne; e += kBlock)
+                s += ld_mat<STREAM>(A.val + eb + e) * op.gather(ld_mat<STREAM>(A.col + eb + e));
+            s = warp_sum(s);
+            if ((tid & 31) == 0) prod[tid >> 5] = s;
+            __syncthreads();
+            if (tid == 0) {
+                double t = 0.0;
+                for (int w = 0; w < kBlock / 32; ++w) t += prod[w];
+                op.row(rb, t, op.load(rb), dots);
+            }
+            __syncthreads();
+        }
     }
     if constexpr (Op::NDOT > 0) grid_reduce<Op::NDOT>(dots, red, op.fin);
 }
@@ -206,13 +475,14 @@ __global__ void __launch_bounds__(kBlock) dense_gemv(int64_t n, const double* __
 struct OpSpmv {
     static constexpr int GATHER = 1, ROWV = 1;  // vectors gathered / row-indexed (bytes model)
     static constexpr int NDOT = 0;
-    static constexpr bool NEED_DIAG = false;
     const double* x;
     double* y;
     NoFin fin;
+    struct Row {};
     __device__ void prepare() {}
+    __device__ Row load(int64_t) const { return {}; }
     __device__ double gather(int32_t c) const { return __ldg(x + c); }
-    __device__ void row(int64_t i, double s, double, double*) const { y[i] = s; }
+    __device__ void row(int64_t i, double s, const Row&, double*) const { y[i] = s; }
 };
 
 // y = f - A x  [+ (y, y)]
@@ -220,15 +490,18 @@ template <int ND, class Fin>
 struct OpResidual {
     static constexpr int GATHER = 1, ROWV = 2;  // vectors gathered / row-indexed (bytes model)
     static constexpr int NDOT = ND;
-    static constexpr bool NEED_DIAG = false;
     const double* x;
     const double* f;
     double* y;
     Fin fin;
+    struct Row {
+        double f;
+    };
     __device__ void prepare() {}
+    __device__ Row load(int64_t i) const { return {f[i]}; }
     __device__ double gather(int32_t c) const { return __ldg(x + c); }
-    __device__ void row(int64_t i, double s, double, double* d) const {
-        double r = f[i] - s;
+    __device__ void row(int64_t i, double s, const Row& rr, double* d) const {
+        double r = rr.f - s;
         y[i] = r;
         if constexpr (ND > 0) d[0] += r * r;
     }
@@ -239,14 +512,17 @@ struct OpResidual {
 struct OpRes0 {
     static constexpr int GATHER = 2, ROWV = 1;  // vectors gathered / row-indexed (bytes model)
     static constexpr int NDOT = 0;
-    static constexpr bool NEED_DIAG = false;
     const double* m;
     const double* f;
     double* t;
     NoFin fin;
+    struct Row {
+        double f;
+    };
     __device__ void prepare() {}
+    __device__ Row load(int64_t i) const { return {f[i]}; }
     __device__ double gather(int32_t c) const { return __ldg(m + c) * __ldg(f + c); }
-    __device__ void row(int64_t i, double s, double, double*) const { t[i] = f[i] - s; }
+    __device__ void row(int64_t i, double s, const Row& rr, double*) const { t[i] = rr.f - s; }
 };
 
 // Damped-Jacobi / SPAI-0 sweep (a6): xo = x + m o (f - A x), optional (f, xo).
@@ -254,17 +530,20 @@ template <int ND, class Fin>
 struct OpRelax {
     static constexpr int GATHER = 1, ROWV = 3;  // vectors gathered / row-indexed (bytes model)
     static constexpr int NDOT = ND;
-    static constexpr bool NEED_DIAG = false;
     const double* x;
     const double* m;
     const double* f;
     double* xo;
     Fin fin;
+    struct Row {
+        double x, m, f;
+    };
     __device__ void prepare() {}
+    __device__ Row load(int64_t i) const { return {x[i], m[i], f[i]}; }
     __device__ double gather(int32_t c) const { return __ldg(x + c); }
-    __device__ void row(int64_t i, double s, double, double* d) const {
-        const double fi = f[i];
-        const double xn = x[i] + m[i] * (fi - s);
+    __device__ void row(int64_t i, double s, const Row& rr, double* d) const {
+        const double fi = rr.f;
+        const double xn = rr.x + rr.m * (fi - s);
         xo[i] = xn;
         if constexpr (ND > 0) d[0] += fi * xn;
     }
@@ -274,54 +553,64 @@ struct OpRelax {
 struct OpProl0 {
     static constexpr int GATHER = 1, ROWV = 3;  // vectors gathered / row-indexed (bytes model)
     static constexpr int NDOT = 0;
-    static constexpr bool NEED_DIAG = false;
     const double* e;
     const double* m;
     const double* f;
     double* x;
     NoFin fin;
+    struct Row {
+        double m, f;
+    };
     __device__ void prepare() {}
+    __device__ Row load(int64_t i) const { return {m[i], f[i]}; }
     __device__ double gather(int32_t c) const { return __ldg(e + c); }
-    __device__ void row(int64_t i, double s, double, double*) const { x[i] = m[i] * f[i] + s; }
+    __device__ void row(int64_t i, double s, const Row& rr, double*) const { x[i] = rr.m * rr.f + s; }
 };
 
 // General prolongation-correction: x = x + P e (x updated in place, row-local).
 struct OpProlAdd {
     static constexpr int GATHER = 1, ROWV = 2;  // vectors gathered / row-indexed (bytes model)
     static constexpr int NDOT = 0;
-    static constexpr bool NEED_DIAG = false;
     const double* e;
     double* x;
     NoFin fin;
+    struct Row {
+        double x;
+    };
     __device__ void prepare() {}
+    __device__ Row load(int64_t i) const { return {x[i]}; }
     __device__ double gather(int32_t c) const { return __ldg(e + c); }
-    __device__ void row(int64_t i, double s, double, double*) const { x[i] = x[i] + s; }
+    __device__ void row(int64_t i, double s, const Row& rr, double*) const { x[i] = rr.x + s; }
 };
 
 // One Chebyshev step (§8c c-1): r = f - A x; scaled: r = r / a_ii (a_ii read from
 // the row itself); p = alpha r + beta p (first step: p = alpha r); xo = x + p.
 template <int ND, class Fin>
 struct OpCheb {
-    static constexpr int GATHER = 1, ROWV = 4;  // vectors gathered / row-indexed (bytes model)
+    static constexpr int GATHER = 1, ROWV = 5;  // vectors gathered / row-indexed (bytes model)
     static constexpr int NDOT = ND;
-    static constexpr bool NEED_DIAG = true;
     const double* x;
     const double* f;
+    const double* diag;
     double* p;
     double* xo;
     double alpha, beta;
     int32_t scaled, first;
     Fin fin;
+    struct Row {
+        double f, dg, p, x;
+    };
     __device__ void prepare() {}
+    __device__ Row load(int64_t i) const { return {f[i], diag[i], first ? 0.0 : p[i], x[i]}; }
     __device__ double gather(int32_t c) const { return __ldg(x + c); }
-    __device__ void row(int64_t i, double s, double dg, double* d) const {
-        double r = f[i] - s;
-        if (scaled) r = r / dg;
-        const double pn = first ? alpha * r : alpha * r + beta * p[i];
+    __device__ void row(int64_t i, double s, const Row& rr, double* d) const {
+        double r = rr.f - s;
+        if (scaled) r = r / rr.dg;
+        const double pn = first ? alpha * r : alpha * r + beta * rr.p;
         p[i] = pn;
-        const double xn = x[i] + pn;
+        const double xn = rr.x + pn;
         xo[i] = xn;
-        if constexpr (ND > 0) d[0] += f[i] * xn;
+        if constexpr (ND > 0) d[0] += rr.f * xn;
     }
 };
 
@@ -331,7 +620,6 @@ template <class Fin>
 struct OpCgDir {
     static constexpr int GATHER = 2, ROWV = 2;  // vectors gathered / row-indexed (bytes model)
     static constexpr int NDOT = 1;
-    static constexpr bool NEED_DIAG = false;
     const double* z;
     const double* p;
     double* pn;
@@ -339,10 +627,14 @@ struct OpCgDir {
     const KState* ks;
     double beta;
     Fin fin;
+    struct Row {
+        double z, p;
+    };
     __device__ void prepare() { beta = ks->beta; }
+    __device__ Row load(int64_t i) const { return {z[i], p[i]}; }
     __device__ double gather(int32_t c) const { return fma(beta, __ldg(p + c), __ldg(z + c)); }
-    __device__ void row(int64_t i, double s, double, double* d) {
-        const double pi = fma(beta, p[i], z[i]);
+    __device__ void row(int64_t i, double s, const Row& rr, double* d) const {
+        const double pi = fma(beta, rr.p, rr.z);
         pn[i] = pi;
         q[i] = s;
         d[0] += pi * s;
@@ -354,20 +646,23 @@ template <int ND, class Fin>
 struct OpSpmvDot {
     static constexpr int GATHER = 1, ROWV = 2;  // vectors gathered / row-indexed (bytes model)
     static constexpr int NDOT = ND;
-    static constexpr bool NEED_DIAG = false;
     const double* x;
     const double* w;
     double* y;
     Fin fin;
+    struct Row {
+        double w;
+    };
     __device__ void prepare() {}
+    __device__ Row load(int64_t i) const { return {w[i]}; }
     __device__ double gather(int32_t c) const { return __ldg(x + c); }
-    __device__ void row(int64_t i, double s, double, double* d) const {
+    __device__ void row(int64_t i, double s, const Row& rr, double* d) const {
         y[i] = s;
         if constexpr (ND == 1) {
-            d[0] += w[i] * s;
+            d[0] += rr.w * s;
         } else {
             d[0] += s * s;
-            d[1] += s * w[i];
+            d[1] += s * rr.w;
         }
     }
 };
