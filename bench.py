@@ -16,9 +16,9 @@ HBM.  value = V-cycles per second over the K timed steps (whole job).
 --impl reference times the oracle (plain fp64 C, oracle/) on the host cores:
 one step = one oracle CG iteration (one V-cycle) on the same system.
 
-Multi-GPU (torchrun, N > 1): each rank solves its own copy of the problem
-(replicas, no halo exchange yet), value = sum over ranks,
-time = max over ranks.
+Multi-GPU (torchrun, N > 1): strong scaling -- the same global system is
+row-partitioned over the N GPUs (halo exchange, all-reduce and coarse-level
+all-gather over NCCL); time = max over ranks.
 """
 from __future__ import annotations
 
@@ -39,6 +39,7 @@ import numpy as np  # noqa: E402
 import synth  # noqa: E402
 
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+METRIC = "AMG-CG V-cycles/s, 3D Poisson 256^3 (solve time in config.solve_ms)"
 
 
 def parse():
@@ -186,9 +187,9 @@ def run_reference(args, cfg):
     cores = os.cpu_count()
     value = vc / dt
     line = {
-        "impl": "reference", "metric": "AMG-CG V-cycles/s (3D Poisson 256^3)", "value": value,
+        "impl": "reference", "metric": METRIC, "value": value,
         "unit": "V-cycles/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, synth/)",
         "config": {"workload": workload_name(args, cfg), "step": "one oracle Krylov iteration "
                    "(1 V-cycle + outer work, restarted from the current x)",
@@ -211,13 +212,15 @@ def main():
         cfg["maxiter"] = args.maxiter
     if args.impl == "reference":
         return run_reference(args, cfg)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    # host setup threads: share the host cores between the ranks of this node
+    os.environ.setdefault("OMP_NUM_THREADS", str(max(1, (os.cpu_count() or 1) // world)))
 
     import torch
     import torch.distributed as dist
 
     import paper_1811_05704_b200 as amgb
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -230,14 +233,28 @@ def main():
 
     ptr, col, val, f = problem_arrays(args.problem, args.n)
     n, nnz = len(f), int(ptr[-1])
+    prm = {"precond.relax.type": cfg["relax"], "solver.type": cfg["solver"]}
     t0 = time.perf_counter()
-    h = amgb.setup(ptr, col, val, {"precond.relax.type": cfg["relax"], "solver.type": cfg["solver"]},
-                   device=local, use_graph=0 if args.no_graph else 1)
+    if world == 1:
+        h = amgb.setup(ptr, col, val, prm, device=local, use_graph=0 if args.no_graph else 1)
+        r0, r1 = 0, n
+    else:
+        # strong scaling: the global system row-partitioned over the ranks, halo
+        # exchange / all-reduce / coarse all-gather over NCCL
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.tensor(list(amgb.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        h = amgb.setup_dist(ptr, col, val, nranks=world, rank=rank, nccl_id=bytes(uid.cpu().tolist()),
+                            params=prm, device=local, use_graph=0 if args.no_graph else 1)
+        st = h.dist_info()["row_starts"]
+        r0, r1 = int(st[rank]), int(st[rank + 1])
     setup_s = time.perf_counter() - t0
     infos = [h.level_info(l) for l in range(h.nlevels)]
+    nl = r1 - r0
 
     stream = torch.cuda.Stream()
-    fd = torch.from_numpy(f).cuda()
+    fd = torch.from_numpy(np.ascontiguousarray(f[r0:r1])).cuda()
     x = torch.zeros_like(fd)
     tol, maxiter = args.tol, cfg["maxiter"]
     with torch.cuda.stream(stream):
@@ -275,19 +292,17 @@ def main():
         barrier()
         h.set_profile(0)
     t_local = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
-    vc_local = torch.tensor([float(vc_total)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
-        dist.all_reduce(vc_local, op=dist.ReduceOp.SUM)
     t_max_ms = float(t_local.item())
-    vc_all = float(vc_local.item())
-    value = vc_all / (t_max_ms / 1e3)
+    # one global solve per step: the job's V-cycles are those of the solve
+    value = float(vc_total) / (t_max_ms / 1e3)
 
     # ---- end-to-end through the public API with HOST buffers (amg_solve_host)
     e2e = None
     if not args.no_e2e:
-        fh = torch.from_numpy(f).pin_memory().numpy()
-        xh = torch.zeros(n, dtype=torch.float64).pin_memory().numpy()
+        fh = torch.from_numpy(np.ascontiguousarray(f[r0:r1])).pin_memory().numpy()
+        xh = torch.zeros(nl, dtype=torch.float64).pin_memory().numpy()
         with torch.cuda.stream(stream):
             for _ in range(max(1, args.warmup // 2)):
                 xh[:] = 0.0
@@ -303,11 +318,9 @@ def main():
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
         te = torch.tensor([dt], dtype=torch.float64, device="cuda")
-        ve = torch.tensor([float(vc_e)], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-            dist.all_reduce(ve, op=dist.ReduceOp.SUM)
-        e2e = {"value": float(ve.item()) / float(te.item()), "unit": "V-cycles/s",
+        e2e = {"value": float(vc_e) / float(te.item()), "unit": "V-cycles/s",
                "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 8 * n,
                "ms_per_step": 1e3 * float(te.item()) / args.steps,
                "timing": "host wall clock around amg_solve_host (H2D f,x + solve + D2H x), max over ranks"}
@@ -333,22 +346,24 @@ def main():
                "kind": "oracle",
                "sample": f"one full oracle solve of the same {args.n}^3 system ({cb['iters']} iterations, "
                          f"{cb['solve_s']:.1f} s; oracle setup {cb['setup_s']:.1f} s untimed)"}
-        xg = x.cpu().numpy()
+        xg = x.cpu().numpy()  # N = 1: the full solution
         parity = {"oracle_iters": cb["iters"], "gpu_iters": iters_all[-1],
                   "x_rel_diff": float(np.linalg.norm(xg - cb["x"]) / np.linalg.norm(cb["x"])),
                   "oracle_rel_resid": cb["rel"]}
 
     if rank == 0:
         line = {
-            "metric": "AMG-CG V-cycles/s, 3D Poisson 256^3 (solve time in config.solve_ms)",
+            "metric": METRIC,
             "value": value, "unit": "V-cycles/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generators, synth/): 7-point FD Poisson, f = 1",
             "config": {
                 "workload": workload_name(args, cfg), "n": n, "nnz": nnz, "tol": tol,
                 "solver": cfg["solver"], "relax": cfg["relax"], "coarsening": "smoothed_aggregation",
-                "parallelism": "1 GPU" if world == 1 else f"{world} replicas (no halo exchange yet)",
+                "parallelism": "1 GPU" if world == 1 else
+                f"row partition over {world} GPUs (NCCL halo exchange + all-reduce; levels < "
+                f"{h.dist_info()['first_replicated']} distributed, coarser replicated)",
                 "levels": len(infos), "rows_per_level": [i["rows"] for i in infos],
                 "nnz_per_level": [i["nnz_A"] for i in infos],
                 "iters_per_solve": iters_all[-1], "rel_resid": rels[-1], "status": statuses[-1],

@@ -177,6 +177,54 @@ enum { AMG_OP_SPMV_A = 0, AMG_OP_SPMV_P = 1, AMG_OP_SPMV_R = 2, AMG_OP_RESIDUAL 
 amg_status amg_level_op(amg_handle h, int32_t level, int32_t op, const double *x, const double *f,
                         double *y);
 
+/* ---------------------------------------------------------------- multi-GPU
+ * Row partition of the hierarchy over `nranks` ranks (the paper
+ * runs the method over MPI processes).  Every rank passes the
+ * SAME global matrix; the host setup is global and deterministic, each rank
+ * keeps its contiguous row slice of every level (coarse rows follow their
+ * aggregate roots) with ghost columns renumbered after the local ones, and
+ * levels with fewer than gather_below rows are replicated on every rank.
+ *   rank >= 0: one process per GPU; halo exchange / all-reduce / all-gather run
+ *              over NCCL (loaded with dlopen) created from nccl_id, which rank 0
+ *              obtains with amg_nccl_unique_id and broadcasts.  amg_solve then
+ *              takes this rank's slice of f and x (rows row_starts[rank] ..
+ *              row_starts[rank+1]-1, see amg_dist_info).
+ *   rank == -1: every rank lives in this process on one GPU ("virtual ranks":
+ *              transport = device copies).  amg_solve / amg_precond_apply take
+ *              the GLOBAL f and x.  Used to test the partitioned path on one GPU.
+ * Results equal the single-GPU solve up to the order of the dot-product sums
+ * (row sums keep the global column order). */
+typedef struct {
+    int32_t nranks;
+    int32_t rank;           /* >= 0: NCCL rank of this process; -1: all ranks here */
+    int64_t gather_below;   /* replicate levels with fewer rows [0 -> 131072] */
+    uint8_t nccl_id[128];   /* ncclUniqueId from amg_nccl_unique_id (rank >= 0) */
+} amg_dist;
+
+/* Test/export hook of one rank's level (host buffers sized by amg_dist_level_info). */
+typedef struct {
+    int64_t *A_ptr; int32_t *A_col; double *A_val;   /* local rows, local|ghost columns */
+    int64_t *P_ptr; int32_t *P_col; double *P_val;   /* local fine rows */
+    int64_t *R_ptr; int32_t *R_col; double *R_val;   /* local coarse rows */
+    int64_t *ghost_global;                           /* global index of each ghost */
+    int32_t *recv_peer; int64_t *recv_off, *recv_cnt;/* ghost-region segments by owner */
+    int32_t *send_peer; int64_t *send_off, *send_cnt;/* packed send-buffer segments */
+    int32_t *send_idx;                               /* local indices to send, by peer */
+} amg_dist_level_export;
+
+/* Write a fresh NCCL unique id (call on rank 0 only).  AMG_E_CUDA if NCCL is unavailable. */
+amg_status amg_nccl_unique_id(uint8_t id[128]);
+/* Distributed setup (see above); same errors as amg_setup, plus AMG_E_INVALID_ARG
+ * for a hierarchy that cannot be distributed (a single level). */
+amg_status amg_setup_dist(int64_t n, const int64_t *ptr, const int32_t *col, const double *val,
+                          const amg_params *prm, const amg_dist *dist, amg_handle *out);
+/* nranks, first replicated level and the level-0 row starts (nranks+1 entries, may be NULL). */
+amg_status amg_dist_info(amg_handle h, int32_t *nranks, int32_t *first_replicated, int64_t *row_starts);
+/* out[0..11] = row0, row1, ghosts, nnz(A), nnz(P), nnz(R), crow0, crow1, replicated,
+ *              send entries, recv peers, send peers of (rank, level). */
+amg_status amg_dist_level_info(amg_handle h, int32_t rank, int32_t level, int64_t out[12]);
+amg_status amg_dist_export(amg_handle h, int32_t rank, int32_t level, const amg_dist_level_export *out);
+
 void amg_destroy(amg_handle h);
 const char *amg_last_error(void);
 /* Library build identification string (compile flags, arch). */

@@ -75,6 +75,18 @@ class LevelExport(C.Structure):
         "aggregates", "smoother", "coarse_inverse")]
 
 
+class AmgDist(C.Structure):
+    _fields_ = [("nranks", C.c_int32), ("rank", C.c_int32), ("gather_below", C.c_int64),
+                ("nccl_id", C.c_uint8 * 128)]
+
+
+class DistLevelExport(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in (
+        "A_ptr", "A_col", "A_val", "P_ptr", "P_col", "P_val", "R_ptr", "R_col", "R_val",
+        "ghost_global", "recv_peer", "recv_off", "recv_cnt", "send_peer", "send_off", "send_cnt",
+        "send_idx")]
+
+
 class SolveStats(C.Structure):
     _fields_ = [
         ("iters", C.c_int32), ("vcycles", C.c_int32), ("status", C.c_int32), ("reserved", C.c_int32),
@@ -98,18 +110,26 @@ _lib.amg_export_level.argtypes = [_V, C.c_int32, C.POINTER(LevelExport)]
 _lib.amg_solve_stats_get.argtypes = [_V, C.POINTER(SolveStats)]
 _lib.amg_level_op.argtypes = [_V, C.c_int32, C.c_int32, _V, _V, _V]
 _lib.amg_destroy.argtypes = [_V]
+_lib.amg_nccl_unique_id.argtypes = [_V]
+_lib.amg_setup_dist.argtypes = [C.c_int64, _V, _V, _V, C.POINTER(AmgParams), C.POINTER(AmgDist),
+                                C.POINTER(_V)]
+_lib.amg_dist_info.argtypes = [_V, C.POINTER(C.c_int32), C.POINTER(C.c_int32), _V]
+_lib.amg_dist_level_info.argtypes = [_V, C.c_int32, C.c_int32, _V]
+_lib.amg_dist_export.argtypes = [_V, C.c_int32, C.c_int32, C.POINTER(DistLevelExport)]
 _lib.amg_last_error.restype = C.c_char_p
 _lib.amg_version.restype = C.c_char_p
 for _name in ("amg_setup", "amg_solve", "amg_solve_host", "amg_precond_apply", "amg_set_stream",
               "amg_set_profile", "amg_level_count", "amg_level_info_get", "amg_export_level",
-              "amg_solve_stats_get", "amg_level_op"):
+              "amg_solve_stats_get", "amg_level_op", "amg_nccl_unique_id", "amg_setup_dist",
+              "amg_dist_info", "amg_dist_level_info", "amg_dist_export"):
     getattr(_lib, _name).restype = C.c_int
 
 # Exported C symbols (tests check them against include/amgb.h).
 SYMBOLS = ("amg_params_default", "amg_setup", "amg_solve", "amg_solve_host", "amg_precond_apply",
            "amg_set_stream", "amg_set_profile", "amg_level_count", "amg_level_info_get",
            "amg_export_level", "amg_solve_stats_get", "amg_level_op", "amg_destroy",
-           "amg_last_error", "amg_version")
+           "amg_last_error", "amg_version", "amg_nccl_unique_id", "amg_setup_dist", "amg_dist_info",
+           "amg_dist_level_info", "amg_dist_export")
 
 RELAX = {"spai0": 0, "damped_jacobi": 1, "chebyshev": 2}
 COARSENING = {"smoothed_aggregation": 0, "aggregation": 1}
@@ -183,15 +203,21 @@ class Hierarchy:
     """amg_setup handle: AMG hierarchy of A, resident on the GPU (device >= 0) or
     host-only (device = -1, for setup/export only)."""
 
-    def __init__(self, ptr, col, val, params: dict | None = None, **kw):
+    def __init__(self, ptr, col, val, params: dict | None = None, dist: AmgDist | None = None, **kw):
         self._ptr = np.ascontiguousarray(ptr, np.int64)
         col = np.ascontiguousarray(col, np.int32)
         val = np.ascontiguousarray(val, np.float64)
         self.n = len(self._ptr) - 1
         self.prm = make_params(params, **kw)
+        self.dist = dist
         h = C.c_void_p()
-        _check(_lib.amg_setup(self.n, self._ptr.ctypes.data, col.ctypes.data, val.ctypes.data,
-                              C.byref(self.prm), C.byref(h)), "amg_setup")
+        if dist is None:
+            _check(_lib.amg_setup(self.n, self._ptr.ctypes.data, col.ctypes.data, val.ctypes.data,
+                                  C.byref(self.prm), C.byref(h)), "amg_setup")
+        else:
+            _check(_lib.amg_setup_dist(self.n, self._ptr.ctypes.data, col.ctypes.data,
+                                       val.ctypes.data, C.byref(self.prm), C.byref(dist),
+                                       C.byref(h)), "amg_setup_dist")
         self._h = h
         self.on_device = self.prm.device >= 0
         if self.on_device:
@@ -243,6 +269,55 @@ class Hierarchy:
             out["coarse_inverse"] = np.zeros((n, n))
             ex.coarse_inverse = out["coarse_inverse"].ctypes.data
         _check(_lib.amg_export_level(self._h, l, C.byref(ex)), "amg_export_level")
+        return out
+
+    # ---- partition (multi-GPU) -----------------------------------------
+    def dist_info(self) -> dict:
+        nr, lg = C.c_int32(), C.c_int32()
+        _check(_lib.amg_dist_info(self._h, C.byref(nr), C.byref(lg), None), "amg_dist_info")
+        starts = np.zeros(nr.value + 1, np.int64)
+        _check(_lib.amg_dist_info(self._h, C.byref(nr), C.byref(lg), starts.ctypes.data),
+               "amg_dist_info")
+        return {"nranks": nr.value, "first_replicated": lg.value, "row_starts": starts}
+
+    def dist_level_info(self, rank: int, l: int) -> dict:
+        out = np.zeros(12, np.int64)
+        _check(_lib.amg_dist_level_info(self._h, rank, l, out.ctypes.data), "amg_dist_level_info")
+        keys = ("row0", "row1", "ghosts", "nnz_A", "nnz_P", "nnz_R", "crow0", "crow1", "replicated",
+                "send_total", "recv_peers", "send_peers")
+        return dict(zip(keys, (int(v) for v in out)))
+
+    def dist_export(self, rank: int, l: int) -> dict:
+        """Local matrices (local|ghost columns) and halo plan of (rank, level)."""
+        inf = self.dist_level_info(rank, l)
+        nloc = inf["row1"] - inf["row0"]
+        ncr = inf["crow1"] - inf["crow0"]
+        out = {"info": inf}
+        ex = DistLevelExport()
+
+        def csr(name, nr, nnz):
+            a = (np.zeros(nr + 1, np.int64), np.zeros(nnz, np.int32), np.zeros(nnz))
+            out[name] = a
+            setattr(ex, name + "_ptr", a[0].ctypes.data)
+            setattr(ex, name + "_col", a[1].ctypes.data)
+            setattr(ex, name + "_val", a[2].ctypes.data)
+
+        csr("A", nloc, inf["nnz_A"])
+        if inf["nnz_P"] or inf["nnz_R"] or ncr:
+            csr("P", nloc, inf["nnz_P"])
+            csr("R", ncr, inf["nnz_R"])
+        arrs = {"ghost_global": np.zeros(inf["ghosts"], np.int64),
+                "recv_peer": np.zeros(inf["recv_peers"], np.int32),
+                "recv_off": np.zeros(inf["recv_peers"], np.int64),
+                "recv_cnt": np.zeros(inf["recv_peers"], np.int64),
+                "send_peer": np.zeros(inf["send_peers"], np.int32),
+                "send_off": np.zeros(inf["send_peers"], np.int64),
+                "send_cnt": np.zeros(inf["send_peers"], np.int64),
+                "send_idx": np.zeros(inf["send_total"], np.int32)}
+        for k, a in arrs.items():
+            setattr(ex, k, a.ctypes.data if a.size else None)
+            out[k] = a
+        _check(_lib.amg_dist_export(self._h, rank, l, C.byref(ex)), "amg_dist_export")
         return out
 
     # ---- device operations ---------------------------------------------
@@ -310,3 +385,22 @@ class Hierarchy:
 def setup(ptr, col, val, params: dict | None = None, **kw) -> Hierarchy:
     """amg_setup: build (host) and upload (GPU) the AMG hierarchy of A."""
     return Hierarchy(ptr, col, val, params, **kw)
+
+
+def nccl_unique_id() -> bytes:
+    """amg_nccl_unique_id (rank 0 of a multi-GPU run)."""
+    buf = (C.c_uint8 * 128)()
+    _check(_lib.amg_nccl_unique_id(C.cast(buf, C.c_void_p)), "amg_nccl_unique_id")
+    return bytes(buf)
+
+
+def setup_dist(ptr, col, val, nranks: int, rank: int = -1, gather_below: int = 1 << 17,
+               nccl_id: bytes | None = None, params: dict | None = None, **kw) -> Hierarchy:
+    """amg_setup_dist: row-partitioned hierarchy (rank = -1: every rank in this
+    process on one GPU; rank >= 0: one NCCL rank per process)."""
+    d = AmgDist()
+    d.nranks, d.rank, d.gather_below = nranks, rank, gather_below
+    if nccl_id is not None:
+        for i, b in enumerate(nccl_id[:128]):
+            d.nccl_id[i] = b
+    return Hierarchy(ptr, col, val, params, dist=d, **kw)

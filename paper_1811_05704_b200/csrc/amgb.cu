@@ -4,9 +4,16 @@
 // Solve phase of arXiv 1811.05704 (AMGCL): Algorithm 2 as the
 // preconditioner of CG / BiCGStab.  The
 // hierarchy comes from setup.cpp (Algorithm 1, on the host)
-// and is uploaded once into sliced-ELL device matrices (kernels.cuh).  Every
-// step of the solve runs in this file's kernels; the host only sequences
-// launches and reads one small state struct per pair of Krylov iterations.
+// and is uploaded once.  Every step of the solve runs in the
+// kernels of kernels.cuh / ops.cuh; the host only sequences launches and reads
+// one small state struct per pair of Krylov iterations.
+//
+// Multi-GPU: a handle holds one or more "parts" (row slices of
+// the hierarchy, dist.hpp).  With NCCL there is one part per process; in
+// virtual mode one process holds every part on one GPU and the transport is
+// device-to-device copies (used to test the partitioned path on one GPU).  The
+// executor issues every step for every part, with halo exchanges before each
+// distributed matrix pass and an all-reduce after each fused dot.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -14,314 +21,54 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
 
 #include "../../include/amgb.h"
+#include "comm.hpp"
+#include "dist.hpp"
 #include "kernels.cuh"
+#include "ops.cuh"
 #include "setup.hpp"
 
 namespace amgb {
 
-// ============================================================ device code
+// ============================================================ multi-part kernels
 
-__global__ void __launch_bounds__(kBlock) dense_gemv(int64_t n, const double* __restrict__ M,
-                                                     const double* __restrict__ x, double* __restrict__ y,
-                                                     const int32_t* gate) {
-    if (gated(gate)) return;
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t r = warp; r < n; r += nwarps) {
-        const double* row = M + r * n;
-        double s = 0.0;
-        for (int64_t j = lane; j < n; j += 32) s = fma(__ldg(row + j), __ldg(x + j), s);
-        s = warp_sum(s);
-        if (lane == 0) y[r] = s;
-    }
+// sendbuf[k] = v[idx[k]] (halo pack)
+__global__ void __launch_bounds__(kBlock) pack_kernel(const int32_t* __restrict__ idx, const double* __restrict__ v,
+                                                      double* __restrict__ out, int64_t n) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        out[k] = v[idx[k]];
 }
 
-// ---- finalizers (run once, by the last block of a reducing kernel) ----------
-
-struct FinNorm {  // |f| -> nf, tol |f|
-    KState* ks;
-    double tol;
-    __device__ void operator()(const double* t) const {
-        ks->nf = sqrt(t[0]);
-        ks->tolnf = tol * ks->nf;
-    }
-};
-
-struct FinInitRes {  // r0 = f - A x0: res, done; BiCGStab also rho = (r,r), |rhat|
-    KState* ks;
-    __device__ void operator()(const double* t) const {
-        const double res = sqrt(t[0]);
-        ks->res = res;
-        ks->rho = t[0];
-        ks->rhat_norm = res;
-        ks->iter = 0;
-        ks->half = 0;
-        ks->status = 0;
-        ks->done = !(0 < ks->maxiter && res > ks->tolnf);
-        ks->skip2 = ks->done;
-    }
-};
-
-struct FinTrueRes {
-    KState* ks;
-    __device__ void operator()(const double* t) const { ks->true_res = sqrt(t[0]); }
-};
-
-struct FinRho {  // CG: rho = (r, z); beta = rho / rho_prev (0 on the first iteration)
-    KState* ks;
-    __device__ void operator()(const double* t) const {
-        const double rho = t[0];
-        if (!(rho > 0.0)) {
-            ks->status = AMG_BREAKDOWN;
-            ks->done = 1;
-            return;
-        }
-        ks->rho = rho;
-        ks->beta = ks->iter == 0 ? 0.0 : rho / ks->rho_prev;
-    }
-};
-
-struct FinSigma {  // CG: sigma = (p, q); alpha = rho / sigma
-    KState* ks;
-    __device__ void operator()(const double* t) const {
-        const double sigma = t[0];
-        if (!(sigma > 0.0)) {
-            ks->status = AMG_BREAKDOWN;
-            ks->done = 1;
-            return;
-        }
-        ks->sigma = sigma;
-        ks->alpha = ks->rho / sigma;
-    }
-};
-
-struct FinCgUpdate {  // CG: res = |r|; k += 1; loop test of §8c c-1
-    KState* ks;
-    __device__ void operator()(const double* t) const {
-        ks->res = sqrt(t[0]);
-        ks->iter += 1;
-        ks->rho_prev = ks->rho;
-        ks->done = !(ks->iter < ks->maxiter && ks->res > ks->tolnf);
-    }
-};
-
-// BiCGStab finalizers (§8c c-1, right-preconditioned van der Vorst)
-struct FinBiAlpha {  // alpha = rho / (rhat, v)
-    KState* ks;
-    __device__ void operator()(const double* t) const {
-        if (t[0] == 0.0) {
-            ks->status = AMG_BREAKDOWN;
-            ks->done = 1;
-            ks->skip2 = 1;
-            return;
-        }
-        ks->alpha = ks->rho / t[0];
-    }
-};
-
-struct FinBiS {  // |s| <= tol |f| -> half-step exit
-    KState* ks;
-    __device__ void operator()(const double* t) const {
-        ks->ss = sqrt(t[0]);
-        if (ks->ss <= ks->tolnf) {
-            ks->half = 1;
-            ks->skip2 = 1;
-        }
-    }
-};
-
-struct FinBiOmega {  // omega = (t, s) / (t, t)
-    KState* ks;
-    __device__ void operator()(const double* t) const {
-        if (t[0] == 0.0) {
-            ks->status = AMG_BREAKDOWN;
-            ks->done = 1;
-            ks->skip2 = 1;
-            return;
-        }
-        const double om = t[1] / t[0];
-        if (fabs(om) < 1e-30) {
-            ks->status = AMG_BREAKDOWN;
-            ks->done = 1;
-            ks->skip2 = 1;
-            return;
-        }
-        ks->omega = om;
-    }
-};
-
-struct FinBiX {  // after x, r update: rho_next = (rhat, r), res = |r|
-    KState* ks;
-    __device__ void operator()(const double* t) const {
-        ks->iter += 1;
-        if (ks->half) {
-            ks->res = ks->ss;
-            ks->done = 1;
-            ks->skip2 = 1;
-            return;
-        }
-        const double rho_next = t[0];
-        ks->res = sqrt(t[1]);
-        ks->done = !(ks->iter < ks->maxiter && ks->res > ks->tolnf);
-        if (!ks->done && fabs(rho_next) < 1e-30 * ks->rhat_norm * ks->res) {
-            ks->status = AMG_BREAKDOWN;
-            ks->done = 1;
-        }
-        if (!ks->done) {
-            ks->beta = (rho_next / ks->rho) * (ks->alpha / ks->omega);
-            ks->rho_prev = ks->rho;
-            ks->rho = rho_next;
-        }
-        ks->skip2 = ks->done;
-    }
-};
-
-// ---- vector ops ----------------------------------------------------------
-
-struct VNorm2 {
-    static constexpr int STREAMS = 1;  // n-vectors moved; (a, a)
-    static constexpr int NDOT = 1;
-    const double* a;
-    FinNorm fin;
-    __device__ void prepare() {}
-    __device__ void elem(int64_t i, double* d) const { d[0] += a[i] * a[i]; }
-};
-
+// deferred finalize after the cross-rank all-reduce of a fused dot
 template <class Fin>
-struct VDot {
-    static constexpr int STREAMS = 2;  // n-vectors moved; (a, b)
-    static constexpr int NDOT = 1;
-    const double* a;
-    const double* b;
-    Fin fin;
-    __device__ void prepare() {}
-    __device__ void elem(int64_t i, double* d) const { d[0] += a[i] * b[i]; }
-};
+__global__ void fin_kernel(Fin fin, const double* tot, const int32_t* gate) {
+    if (gated(gate)) return;
+    fin(tot);
+}
 
-struct VMulDiag {
-    static constexpr int STREAMS = 3;  // n-vectors moved; x = m o f  (first SPAI-0/Jacobi sweep from zero)
-    static constexpr int NDOT = 0;
-    const double* m;
-    const double* f;
-    double* x;
-    NoFin fin;
-    __device__ void prepare() {}
-    __device__ void elem(int64_t i, double*) const { x[i] = m[i] * f[i]; }
-};
+// virtual-mode all-reduce: every part's totals <- sum over parts in rank order
+__global__ void sum_parts_kernel(double* const* parts, int nparts, int nv) {
+    const int k = threadIdx.x;
+    if (k >= nv) return;
+    double s = 0.0;
+    for (int p = 0; p < nparts; ++p) s += parts[p][k];
+    for (int p = 0; p < nparts; ++p) parts[p][k] = s;
+}
 
-struct VCheb0 {
-    static constexpr int STREAMS = 4;  // n-vectors moved; first Chebyshev step from x = 0: p = alpha (f / a_ii); x = p
-    static constexpr int NDOT = 0;
-    const double* f;
-    const double* diag;
-    double* p;
-    double* x;
-    double alpha;
-    int32_t scaled;
-    NoFin fin;
-    __device__ void prepare() {}
-    __device__ void elem(int64_t i, double*) const {
-        double r = f[i];
-        if (scaled) r = r / diag[i];
-        const double pn = alpha * r;
-        p[i] = pn;
-        x[i] = pn;
-    }
-};
-
-struct VCgUpdate {
-    static constexpr int STREAMS = 6;  // n-vectors moved; x += alpha p; r -= alpha q; (r, r)
-    static constexpr int NDOT = 1;
-    double* x;
-    double* r;
-    const double* p;
-    const double* q;
-    const KState* ks;
-    double alpha;
-    FinCgUpdate fin;
-    __device__ void prepare() { alpha = ks->alpha; }
-    __device__ void elem(int64_t i, double* d) const {
-        x[i] = fma(alpha, p[i], x[i]);
-        const double rn = fma(-alpha, q[i], r[i]);
-        r[i] = rn;
-        d[0] += rn * rn;
-    }
-};
-
-struct VBiP {
-    static constexpr int STREAMS = 3;  // n-vectors moved; p = r (k = 0) or r + beta (p - omega v)
-    static constexpr int NDOT = 0;
-    const double* r;
-    const double* v;
-    double* p;
-    const KState* ks;
-    double beta, omega;
-    int32_t first;
-    NoFin fin;
-    __device__ void prepare() {
-        beta = ks->beta;
-        omega = ks->omega;
-        first = ks->iter == 0;
-    }
-    __device__ void elem(int64_t i, double*) const {
-        p[i] = first ? r[i] : fma(beta, p[i] - omega * v[i], r[i]);
-    }
-};
-
-struct VBiS {
-    static constexpr int STREAMS = 3;  // n-vectors moved; s = r - alpha v; (s, s)
-    static constexpr int NDOT = 1;
-    const double* r;
-    const double* v;
-    double* s;
-    const KState* ks;
-    double alpha;
-    FinBiS fin;
-    __device__ void prepare() { alpha = ks->alpha; }
-    __device__ void elem(int64_t i, double* d) const {
-        const double si = fma(-alpha, v[i], r[i]);
-        s[i] = si;
-        d[0] += si * si;
-    }
-};
-
-struct VBiX {
-    static constexpr int STREAMS = 9;  // n-vectors moved; half: x += alpha ph; else x += alpha ph + omega sh, r = s - omega t
-    static constexpr int NDOT = 2;
-    double* x;
-    double* r;
-    const double* ph;
-    const double* sh;
-    const double* s;
-    const double* t;
-    const double* rhat;
-    const KState* ks;
-    double alpha, omega;
-    int32_t half;
-    FinBiX fin;
-    __device__ void prepare() {
-        alpha = ks->alpha;
-        omega = ks->omega;
-        half = ks->half;
-    }
-    __device__ void elem(int64_t i, double* d) const {
-        if (half) {
-            x[i] = fma(alpha, ph[i], x[i]);
-            return;
-        }
-        x[i] = fma(omega, sh[i], fma(alpha, ph[i], x[i]));
-        const double rn = fma(-omega, t[i], s[i]);
-        r[i] = rn;
-        d[0] += rhat[i] * rn;
-        d[1] += rn * rn;
-    }
-};
+// CG ghost update: pn[g] = z[g] + beta p[g] on the ghost region (the local
+// rows of pn are written by the CG direction kernel)
+__global__ void __launch_bounds__(kBlock) ghost_dir_kernel(const double* z, const double* p, double* pn, int64_t n,
+                                                           const KState* ks, const int32_t* gate) {
+    if (gated(gate)) return;
+    const double beta = ks->beta;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        pn[i] = fma(beta, p[i], z[i]);
+}
 
 // ============================================================ host side
 
@@ -337,6 +84,14 @@ inline void ck(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw CudaError{std::string(what) + ": " + cudaGetErrorString(e)};
 }
 
+inline void ckn(int r, const char* what) {
+    if (r != 0) {
+        Nccl& n = Nccl::get();
+        throw CudaError{std::string(what) + ": NCCL error " + std::to_string(r) +
+                        (n.getErrorString ? std::string(" ") + n.getErrorString(r) : std::string())};
+    }
+}
+
 struct HostSell {
     int64_t nrows = 0, ncols = 0, nslices = 0;
     std::vector<int64_t> sptr;
@@ -345,7 +100,7 @@ struct HostSell {
 };
 
 // CSR -> SELL-C, slice height C (see kernels.cuh): entry k of row s*C + r at
-// sptr[s] + k*C + r.
+// sptr[s] + k*C + r.  Padding repeats the row's last column with value 0.
 HostSell to_sell(const Csr& A, int C = 32) {
     HostSell S;
     S.nrows = A.nrows;
@@ -389,19 +144,23 @@ enum class Fmt { CSR, SELL, TMA };
 
 struct DMat {
     Fmt fmt = Fmt::CSR;
-    bool is_csr = true;
     Sell sell;
     SellTma tma;
-    int64_t sell_wmax = 0;  // widest slice
     CsrDev csr;
     int64_t nrows = 0, ncols = 0, nnz = 0, stored = 0;
 };
 
+// One level of one part.  Vectors that are gathered by a matrix pass have a
+// ghost region after the n local entries.
 struct DevLevel {
-    int64_t n = 0, nc = 0;
-    int64_t nnzA = 0, nnzP = 0, padA = 0;
+    bool replicated = true, next_replicated = true;
+    int64_t n = 0;                 // local rows
+    int64_t ng = 0;                // ghost entries
+    int64_t nc = 0;                // columns of P (coarse local + ghost, or the full coarse size)
+    int64_t crow0 = 0, crow1 = 0;  // local rows of R (slice of level l+1)
+    int64_t nnzA = 0, nnzP = 0, nnzR = 0, padA = 0;
     DMat A, P, R;
-    double* m = nullptr;     // SPAI-0 / Jacobi diagonal
+    double* m = nullptr;     // SPAI-0 / Jacobi diagonal (local + ghost)
     double* diag = nullptr;  // a_ii (Chebyshev)
     double* f = nullptr;     // right-hand side (levels >= 1)
     double* x = nullptr;     // work
@@ -412,7 +171,29 @@ struct DevLevel {
     std::vector<double> cheb_alpha, cheb_beta;
     double alg_bytes = 0;
     int64_t dev_bytes = 0;
+    // halo (distributed levels)
+    HaloPlan plan;
+    int32_t* send_idx = nullptr;
+    double* sendbuf = nullptr;
+    int64_t nsend = 0;
 };
+
+struct Part {
+    int rank = 0;
+    int64_t row0 = 0, row1 = 0;  // level-0 rows
+    std::vector<DevLevel> lv;
+    double* coarse_inv = nullptr;
+    int64_t nL = 0;
+    KState* ks = nullptr;
+    Red red;
+    // Krylov vectors (level-0 local length + ghosts where gathered)
+    double *r = nullptr, *z = nullptr, *pa = nullptr, *pb = nullptr, *q = nullptr, *xw = nullptr;
+    double *rhat = nullptr, *v = nullptr, *s = nullptr, *sh = nullptr, *ph = nullptr, *tv = nullptr;
+    const double* fcur = nullptr;  // right-hand side of the current solve (local slice)
+    double* xcur = nullptr;        // solution vector of the current solve (with ghosts if needed)
+};
+
+double level_alg_bytes(int64_t n_, int64_t z_, int64_t p_, int64_t c_, const amg_params& p, bool coarsest);
 
 }  // namespace
 
@@ -424,17 +205,17 @@ struct Handle {
     int num_sms = 148;
     cudaStream_t stream = nullptr;      // work stream (own_stream unless set by the caller)
     cudaStream_t own_stream = nullptr;  // blocking stream: ordered with the legacy default stream
-    std::vector<DevLevel> lv;
-    double* coarse_inv = nullptr;
-    int64_t nL = 0;
-    KState* ks = nullptr;
-    KState* ks_host = nullptr;  // pinned
-    Red red;
-    int32_t* zero_gate = nullptr;
-    // Krylov vectors (level-0 length)
-    double *r = nullptr, *z = nullptr, *pa = nullptr, *pb = nullptr, *q = nullptr;
-    double *rhat = nullptr, *v = nullptr, *s = nullptr, *sh = nullptr, *ph = nullptr, *tv = nullptr;
-    double *hf = nullptr, *hx = nullptr;  // device copies for amg_solve_host
+    // partition
+    int nranks = 1;        // total ranks of the partition
+    bool virt = false;     // every part lives in this process (one GPU)
+    int lg = 1;            // first replicated level
+    void* nccl = nullptr;  // ncclComm_t (NCCL mode)
+    std::vector<std::vector<int64_t>> starts;  // level_starts
+    std::vector<RankPart> host_parts;          // host copies (export / upload)
+    std::vector<Part> parts;
+    double** d_defer_ptrs = nullptr;       // virtual all-reduce: device array of part->defer
+    KState* ks_host = nullptr;             // pinned (part 0)
+    double *hf = nullptr, *hx = nullptr;   // device copies for amg_solve_host
     std::vector<void*> allocs;
     // CUDA graph of two Krylov iterations, keyed by the x pointer
     cudaGraphExec_t graph = nullptr;
@@ -443,14 +224,16 @@ struct Handle {
     int64_t graph_kernels = 0;
     // accounting
     int64_t launches = 0;
-    bool count_only = false;  // while capturing: count kernels into graph_kernels
     amg_solve_stats stats{};
     bool sync_debug = false;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
+    bool distributed() const { return nranks > 1; }
+
     double* dalloc(int64_t n) {
         void* p = nullptr;
         ck(cudaMalloc(&p, std::max<int64_t>(n, 1) * sizeof(double)), "cudaMalloc");
+        ck(cudaMemset(p, 0, std::max<int64_t>(n, 1) * sizeof(double)), "cudaMemset");
         allocs.push_back(p);
         return static_cast<double*>(p);
     }
@@ -470,6 +253,7 @@ struct Handle {
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         if (own_stream) cudaStreamDestroy(own_stream);
+        if (nccl && Nccl::get().commDestroy) Nccl::get().commDestroy(nccl);
     }
 
     int grid_for(int64_t n) const {
@@ -570,14 +354,14 @@ struct Handle {
     }
 
     // ---------------------------------------------------------------- launches
-    int mat_class(const DMat& M) const {
-        if (&M == &lv[0].A) return AMG_PROF_A0_PASS;
-        for (const auto& L : lv)
+    int mat_class(const Part& p, const DMat& M) const {
+        if (&M == &p.lv[0].A) return AMG_PROF_A0_PASS;
+        for (const auto& L : p.lv)
             if (&M == &L.A) return AMG_PROF_A_COARSE;
         return AMG_PROF_TRANSFER;
     }
     template <int U, bool PIPE, class Op>
-    void rows_sell(const Sell& M, const Op& op, const int32_t* gate, bool stream_loads) {
+    void rows_sell(const Sell& M, const Op& op, const int32_t* gate, const Red& red, bool stream_loads) {
         const int g = (int)std::max<int64_t>(
             1, std::min<int64_t>((M.nrows + kBlock - 1) / kBlock, (int64_t)num_sms * (PIPE ? 4 : 6)));
         if (stream_loads)
@@ -586,7 +370,7 @@ struct Handle {
             sell_rows<U, false, PIPE, Op><<<g, kBlock, 0, stream>>>(M, op, gate, red);
     }
     template <int G, class Op>
-    void rows_csr(const CsrDev& M, const Op& op, const int32_t* gate, bool stream_loads) {
+    void rows_csr(const CsrDev& M, const Op& op, const int32_t* gate, const Red& red, bool stream_loads) {
         const int g = (int)std::max<int64_t>(1, std::min<int64_t>(M.nblocks, (int64_t)num_sms * 8));
         if (stream_loads)
             csr_rows<G, true, Op><<<g, kBlock, 0, stream>>>(M, op, gate, red);
@@ -594,7 +378,7 @@ struct Handle {
             csr_rows<G, false, Op><<<g, kBlock, 0, stream>>>(M, op, gate, red);
     }
     template <int T, bool STREAM, class Op>
-    void rows_tma_impl(const SellTma& M, const Op& op, const int32_t* gate) {
+    void rows_tma_impl(const SellTma& M, const Op& op, const int32_t* gate, const Red& red) {
         auto kern = sell_tma<T, STREAM, Op>;
         const size_t smem = (size_t)kTmaStages * M.tile_ent * 12 + 2 * kTmaStages * 8;
         static size_t configured = 0;  // per instantiation
@@ -606,229 +390,429 @@ struct Handle {
         kern<<<g, kTmaThreads, smem, stream>>>(M, op, gate, red);
     }
     template <int T, class Op>
-    void rows_tma(const SellTma& M, const Op& op, const int32_t* gate, bool stream_loads) {
+    void rows_tma(const SellTma& M, const Op& op, const int32_t* gate, const Red& red, bool stream_loads) {
         if (stream_loads)
-            rows_tma_impl<T, true>(M, op, gate);
+            rows_tma_impl<T, true>(M, op, gate, red);
         else
-            rows_tma_impl<T, false>(M, op, gate);
+            rows_tma_impl<T, false>(M, op, gate, red);
     }
+    // a part with no rows contributes zeros to an all-reduce
+    void zero_defer(Part& p) {
+        if (p.red.defer) ck(cudaMemsetAsync(p.red.defer, 0, 4 * sizeof(double), stream), "memset");
+    }
+    // One pass over matrix M of part p with the fused epilogue op.
     template <class Op>
-    void rows_auto(const DMat& M, const Op& op, const int32_t* gate, const char* what) {
+    void rows(Part& p, const DMat& M, const Op& op, const int32_t* gate, const char* what) {
+        if (M.nrows == 0) {
+            if constexpr (Op::NDOT > 0) zero_defer(p);
+            return;
+        }
         // matrices too big for L2 stream their entries (evict-first); the rest
         // keep them cached so coarse levels stay L2-resident across cycles
         const bool big = M.nnz * 12 > (int64_t)48 << 20;
         const double bytes = 12.0 * M.nnz + 4.0 * M.nrows + 8.0 * M.ncols * Op::GATHER + 8.0 * M.nrows * Op::ROWV;
-        launch(mat_class(M), bytes, what, [&] {
+        const Red& red = p.red;
+        launch(mat_class(p, M), bytes, what, [&] {
             if (M.fmt == Fmt::TMA) {
                 switch (M.tma.T) {
-                    case 1: rows_tma<1>(M.tma, op, gate, big); break;
-                    case 2: rows_tma<2>(M.tma, op, gate, big); break;
-                    case 4: rows_tma<4>(M.tma, op, gate, big); break;
-                    default: rows_tma<8>(M.tma, op, gate, big); break;
+                    case 1: rows_tma<1>(M.tma, op, gate, red, big); break;
+                    case 2: rows_tma<2>(M.tma, op, gate, red, big); break;
+                    case 4: rows_tma<4>(M.tma, op, gate, red, big); break;
+                    default: rows_tma<8>(M.tma, op, gate, red, big); break;
                 }
-            } else if (M.is_csr) {
+            } else if (M.fmt == Fmt::CSR) {
                 switch (M.csr.G) {
-                    case 1: rows_csr<1>(M.csr, op, gate, big); break;
-                    case 2: rows_csr<2>(M.csr, op, gate, big); break;
-                    case 4: rows_csr<4>(M.csr, op, gate, big); break;
-                    case 8: rows_csr<8>(M.csr, op, gate, big); break;
-                    default: rows_csr<16>(M.csr, op, gate, big); break;
+                    case 1: rows_csr<1>(M.csr, op, gate, red, big); break;
+                    case 2: rows_csr<2>(M.csr, op, gate, red, big); break;
+                    case 4: rows_csr<4>(M.csr, op, gate, red, big); break;
+                    case 8: rows_csr<8>(M.csr, op, gate, red, big); break;
+                    default: rows_csr<16>(M.csr, op, gate, red, big); break;
                 }
-            } else if (M.sell_wmax <= 8) {
-                rows_sell<8, false>(M.sell, op, gate, big);
             } else {
-                rows_sell<8, true>(M.sell, op, gate, big);
+                rows_sell<8, true>(M.sell, op, gate, red, big);
             }
         });
     }
     template <class Op>
-    void vec(int64_t n, const Op& op, const int32_t* gate, const char* what) {
+    void vec(Part& p, int64_t n, const Op& op, const int32_t* gate, const char* what) {
+        if (n == 0) {
+            if constexpr (Op::NDOT > 0) zero_defer(p);
+            return;
+        }
         launch(AMG_PROF_VECTOR, 8.0 * n * Op::STREAMS, what,
-               [&] { vec_kernel<Op><<<grid_for(n), kBlock, 0, stream>>>(n, op, gate, red); });
+               [&] { vec_kernel<Op><<<grid_for(n), kBlock, 0, stream>>>(n, op, gate, p.red); });
     }
 
-    // ---------------------------------------------------------------- V-cycle
-    // Algorithm 2 on level l: out = V(f) from x = 0.  If
-    // rho_fin is set, the last kernel also computes (f, out) and calls it.
-    // Returns true if the dot was fused.
-    template <class FinT>
-    bool vcycle(int l, const double* f, double* out, const int32_t* gate, const FinT* rho_fin);
-    bool vcycle_plain(int l, const double* f, double* out, const int32_t* gate) {
-        return vcycle<FinRho>(l, f, out, gate, nullptr);
+    // ------------------------------------------------------------ collectives
+    using Sel = std::function<double*(Part&)>;
+    using CSel = std::function<const double*(Part&)>;
+    using GSel = std::function<const int32_t*(Part&)>;
+
+    // Halo exchange of the level-l vector sel(part): pack, then NCCL
+    // send/recv (one part per process) or device copies between parts.
+    void exchange(int l, const Sel& sel) {
+        if (!distributed() || parts[0].lv[l].replicated) return;
+        for (Part& p : parts) {
+            DevLevel& L = p.lv[l];
+            if (L.nsend == 0) continue;
+            double* v = sel(p);
+            launch(AMG_PROF_VECTOR, 12.0 * L.nsend, "halo pack", [&] {
+                pack_kernel<<<grid_for(L.nsend), kBlock, 0, stream>>>(L.send_idx, v, L.sendbuf, L.nsend);
+            });
+        }
+        if (virt) {
+            for (Part& p : parts) {
+                DevLevel& L = p.lv[l];
+                double* dst = sel(p) + L.n;
+                for (size_t k = 0; k < L.plan.recv_peer.size(); ++k) {
+                    const int q = L.plan.recv_peer[k];
+                    const DevLevel& Q = parts[q].lv[l];
+                    int64_t soff = -1;
+                    for (size_t j = 0; j < Q.plan.send_peer.size(); ++j)
+                        if (Q.plan.send_peer[j] == p.rank) soff = Q.plan.send_off[j];
+                    if (soff < 0) throw CudaError{"halo plan mismatch"};
+                    ck(cudaMemcpyAsync(dst + L.plan.recv_off[k], Q.sendbuf + soff, L.plan.recv_cnt[k] * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, stream),
+                       "halo copy");
+                }
+            }
+        } else {
+            Nccl& nc = Nccl::get();
+            Part& p = parts[0];
+            DevLevel& L = p.lv[l];
+            double* dst = sel(p) + L.n;
+            ckn(nc.groupStart(), "ncclGroupStart");
+            for (size_t j = 0; j < L.plan.send_peer.size(); ++j)
+                ckn(nc.send(L.sendbuf + L.plan.send_off[j], L.plan.send_cnt[j], kNcclDouble, L.plan.send_peer[j], nccl,
+                            stream),
+                    "ncclSend");
+            for (size_t k = 0; k < L.plan.recv_peer.size(); ++k)
+                ckn(nc.recv(dst + L.plan.recv_off[k], L.plan.recv_cnt[k], kNcclDouble, L.plan.recv_peer[k], nccl,
+                            stream),
+                    "ncclRecv");
+            ckn(nc.groupEnd(), "ncclGroupEnd");
+        }
+    }
+    // After a fused dot on a distributed handle: all-reduce the deferred
+    // totals, then finalize on every part.
+    template <class MakeFin>
+    void allreduce_fin(int nv, const MakeFin& make_fin, const GSel& gate) {
+        if (!distributed()) return;
+        if (virt) {
+            launch(AMG_PROF_VECTOR, 0, "allreduce (virtual)",
+                   [&] { sum_parts_kernel<<<1, 32, 0, stream>>>(d_defer_ptrs, (int)parts.size(), nv); });
+        } else {
+            Part& p = parts[0];
+            ckn(Nccl::get().allReduce(p.red.defer, p.red.defer, nv, kNcclDouble, kNcclSum, nccl, stream),
+                "ncclAllReduce");
+        }
+        for (Part& p : parts) {
+            auto fin = make_fin(p);
+            const int32_t* g = gate(p);
+            launch(AMG_PROF_VECTOR, 0, "finalize", [&] { fin_kernel<<<1, 1, 0, stream>>>(fin, p.red.defer, g); });
+        }
+    }
+    // Level l_rep (first replicated level): every part wrote its slice of the
+    // full vector sel(part); gather the other ranks' slices.
+    void allgather_slices(int l_rep, const Sel& sel) {
+        if (!distributed()) return;
+        const std::vector<int64_t>& st = starts[l_rep];
+        if (virt) {
+            for (Part& p : parts)
+                for (Part& q : parts) {
+                    if (q.rank == p.rank) continue;
+                    const int64_t a = st[q.rank], b = st[q.rank + 1];
+                    if (b > a)
+                        ck(cudaMemcpyAsync(sel(p) + a, sel(q) + a, (b - a) * sizeof(double), cudaMemcpyDeviceToDevice,
+                                           stream),
+                           "allgather copy");
+                }
+        } else {
+            Nccl& nc = Nccl::get();
+            double* buf = sel(parts[0]);
+            ckn(nc.groupStart(), "ncclGroupStart");
+            for (int q = 0; q < nranks; ++q) {
+                const int64_t a = st[q], b = st[q + 1];
+                if (b > a) ckn(nc.broadcast(buf + a, buf + a, b - a, kNcclDouble, q, nccl, stream), "ncclBroadcast");
+            }
+            ckn(nc.groupEnd(), "ncclGroupEnd");
+        }
     }
 
-    void cg_iteration(double* x, int parity);
-    void bicgstab_iteration(double* x);
+    bool vcycle(int l, const CSel& f, const Sel& out, const GSel& gate, bool with_rho);
+    void cg_iteration(int parity);
+    void bicgstab_iteration();
     amg_status solve(const double* f, double* x, double tol, int32_t maxiter, int32_t* iters, double* rel);
+    void precond(const double* r, double* z);
 };
 
-template <class FinT>
-bool Handle::vcycle(int l, const double* f, double* out, const int32_t* gate, const FinT* rho_fin) {
-    DevLevel& L = lv[l];
-    const int nlev = (int)lv.size();
-    if (l == nlev - 1) {  // coarsest: out = A_L^-1 f
-        const int64_t warps = std::min<int64_t>(L.n, (int64_t)num_sms * 64);
-        const int g = (int)std::max<int64_t>(1, (warps * 32 + kBlock - 1) / kBlock);
-        launch(AMG_PROF_COARSE_SOLVE, 8.0 * L.n * L.n + 16.0 * L.n, "coarse gemv",
-               [&] { dense_gemv<<<g, kBlock, 0, stream>>>(L.n, coarse_inv, f, out, gate); });
+// Algorithm 2 on level l for every part: out = V(f) from
+// x = 0.  If with_rho, the last kernel also computes rho = (f, out) (CG,
+// FinRho).  Returns true if the dot was fused.
+bool Handle::vcycle(int l, const CSel& fsel, const Sel& osel, const GSel& gate, bool with_rho) {
+    const int nlev = (int)parts[0].lv.size();
+    if (l == nlev - 1) {  // coarsest: out = A_L^-1 f, replicated
+        for (Part& p : parts) {
+            DevLevel& L = p.lv[l];
+            const int64_t warps = std::min<int64_t>(L.n, (int64_t)num_sms * 64);
+            const int g = (int)std::max<int64_t>(1, (warps * 32 + kBlock - 1) / kBlock);
+            const double* f = fsel(p);
+            double* out = osel(p);
+            const int32_t* gt = gate(p);
+            launch(AMG_PROF_COARSE_SOLVE, 8.0 * L.n * L.n + 16.0 * L.n, "coarse gemv",
+                   [&] { dense_gemv<<<g, kBlock, 0, stream>>>(L.n, p.coarse_inv, f, out, gt); });
+        }
         return false;
     }
-    DevLevel& C = lv[l + 1];
     const int npre = prm.npre, npost = prm.npost;
     const bool cheb = prm.relax == 2;
     const int K = prm.cheb_degree;
+    const bool next_rep = parts[0].lv[l].next_replicated;
+    // ping-pong buffers per part
+    std::vector<double*> X(parts.size()), Y(parts.size());
+    for (size_t i = 0; i < parts.size(); ++i) {
+        X[i] = parts[i].lv[l].x;
+        Y[i] = parts[i].lv[l].y;
+    }
+    Sel xsel = [&](Part& p) { return X[&p - &parts[0]]; };
+    auto for_parts = [&](const std::function<void(Part&, size_t)>& fn) {
+        for (size_t i = 0; i < parts.size(); ++i) fn(parts[i], i);
+    };
+    auto swap_xy = [&] {
+        for (size_t i = 0; i < parts.size(); ++i) std::swap(X[i], Y[i]);
+    };
+
+    // the right-hand side of a distributed level is gathered by the first pass
+    exchange(l, [&](Part& p) { return const_cast<double*>(fsel(p)); });
 
     // ---- pre-smoothing from x = 0 and residual t = f - A x
-    double* x = L.x;
-    double* y = L.y;
     bool x_is_mf = false;  // x == m o f implicitly (not materialised)
     if (!cheb) {
-        if (npre == 0) {
-            ck(cudaMemsetAsync(x, 0, L.n * sizeof(double), stream), "memset");
-            rows_auto(L.A, OpResidual<0, NoFin>{x, f, L.t, {}}, gate, "residual");
-        } else if (npre == 1) {
+        if (npre == 1) {
             x_is_mf = true;  // fused: t = f - A (m o f)
-            rows_auto(L.A, OpRes0{L.m, f, L.t, {}}, gate, "res0");
+            for_parts([&](Part& p, size_t) {
+                DevLevel& L = p.lv[l];
+                rows(p, L.A, OpRes0{L.m, fsel(p), L.t, {}}, gate(p), "res0");
+            });
         } else {
-            vec(L.n, VMulDiag{L.m, f, x, {}}, gate, "x=mf");
+            for_parts([&](Part& p, size_t i) {
+                DevLevel& L = p.lv[l];
+                if (npre == 0)
+                    ck(cudaMemsetAsync(X[i], 0, (L.n + L.ng) * sizeof(double), stream), "memset");
+                else
+                    vec(p, L.n + L.ng, VMulDiag{L.m, fsel(p), X[i], {}}, gate(p), "x=mf");
+            });
             for (int s = 1; s < npre; ++s) {
-                rows_auto(L.A, OpRelax<0, NoFin>{x, L.m, f, y, {}}, gate, "relax");
-                std::swap(x, y);
+                exchange(l, xsel);
+                for_parts([&](Part& p, size_t i) {
+                    DevLevel& L = p.lv[l];
+                    rows(p, L.A, OpRelax<0, NoFin>{X[i], L.m, fsel(p), Y[i], {}}, gate(p), "relax");
+                });
+                swap_xy();
             }
-            rows_auto(L.A, OpResidual<0, NoFin>{x, f, L.t, {}}, gate, "residual");
+            exchange(l, xsel);
+            for_parts([&](Part& p, size_t i) {
+                DevLevel& L = p.lv[l];
+                rows(p, L.A, OpResidual<0, NoFin>{X[i], fsel(p), L.t, {}}, gate(p), "residual");
+            });
         }
     } else {
-        if (npre == 0) {
-            ck(cudaMemsetAsync(x, 0, L.n * sizeof(double), stream), "memset");
-        } else {
-            for (int s = 0; s < npre; ++s) {
-                for (int k = 0; k < K; ++k) {
-                    if (s == 0 && k == 0) {
-                        vec(L.n, VCheb0{f, L.diag, L.p, x, L.cheb_alpha[0], prm.cheb_scaled, {}}, gate,
-                            "cheb0");
-                    } else {
-                        rows_auto(L.A,
-                                  OpCheb<0, NoFin>{x, f, L.diag, L.p, y, L.cheb_alpha[k], L.cheb_beta[k],
-                                                   prm.cheb_scaled, k == 0, {}},
-                                  gate, "cheb");
-                        std::swap(x, y);
-                    }
+        for (int s = 0; s < npre; ++s) {
+            for (int k = 0; k < K; ++k) {
+                if (s == 0 && k == 0) {
+                    for_parts([&](Part& p, size_t i) {
+                        DevLevel& L = p.lv[l];
+                        vec(p, L.n + L.ng, VCheb0{fsel(p), L.diag, L.p, X[i], L.cheb_alpha[0], prm.cheb_scaled, {}},
+                            gate(p), "cheb0");
+                    });
+                } else {
+                    exchange(l, xsel);
+                    for_parts([&](Part& p, size_t i) {
+                        DevLevel& L = p.lv[l];
+                        rows(p, L.A,
+                             OpCheb<0, NoFin>{X[i], fsel(p), L.diag, L.p, Y[i], L.cheb_alpha[k], L.cheb_beta[k],
+                                              prm.cheb_scaled, k == 0, {}},
+                             gate(p), "cheb");
+                    });
+                    swap_xy();
                 }
             }
         }
-        rows_auto(L.A, OpResidual<0, NoFin>{x, f, L.t, {}}, gate, "residual");
+        if (npre == 0)
+            for_parts([&](Part& p, size_t i) {
+                ck(cudaMemsetAsync(X[i], 0, (p.lv[l].n + p.lv[l].ng) * sizeof(double), stream), "memset");
+            });
+        exchange(l, xsel);
+        for_parts([&](Part& p, size_t i) {
+            DevLevel& L = p.lv[l];
+            rows(p, L.A, OpResidual<0, NoFin>{X[i], fsel(p), L.t, {}}, gate(p), "residual");
+        });
     }
 
     // ---- restriction f_c = R t, coarse solve, prolongation x += P x_c
-    rows_auto(L.R, OpSpmv{L.t, C.f}, gate, "restrict");
-    vcycle_plain(l + 1, C.f, C.o, gate);
-    if (x_is_mf)
-        rows_auto(L.P, OpProl0{C.o, L.m, f, x, {}}, gate, "prolong0");
-    else
-        rows_auto(L.P, OpProlAdd{C.o, x, {}}, gate, "prolong");
+    exchange(l, [&](Part& p) { return p.lv[l].t; });
+    for_parts([&](Part& p, size_t) {
+        DevLevel& L = p.lv[l];
+        DevLevel& C = p.lv[l + 1];
+        // into the next level's vector; a replicated next level receives the
+        // slice [crow0, crow1) of the full vector
+        rows(p, L.R, OpSpmv{L.t, C.f + (next_rep ? L.crow0 : 0)}, gate(p), "restrict");
+    });
+    if (next_rep) allgather_slices(l + 1, [&](Part& p) { return p.lv[l + 1].f; });
+    vcycle(l + 1, [&](Part& p) { return (const double*)p.lv[l + 1].f; }, [&](Part& p) { return p.lv[l + 1].o; }, gate,
+           false);
+    exchange(l + 1, [&](Part& p) { return p.lv[l + 1].o; });
+    for_parts([&](Part& p, size_t i) {
+        DevLevel& L = p.lv[l];
+        DevLevel& C = p.lv[l + 1];
+        if (x_is_mf)
+            rows(p, L.P, OpProl0{C.o, L.m, fsel(p), X[i], {}}, gate(p), "prolong0");
+        else
+            rows(p, L.P, OpProlAdd{C.o, X[i], {}}, gate(p), "prolong");
+    });
 
     // ---- post-smoothing; the last sweep writes `out`
-    if (!cheb) {
-        if (npost == 0) {
-            ck(cudaMemcpyAsync(out, x, L.n * sizeof(double), cudaMemcpyDeviceToDevice, stream), "copy");
-            return false;
-        }
-        for (int s = 0; s < npost; ++s) {
-            double* dst = (s == npost - 1) ? out : y;
-            if (s == npost - 1 && rho_fin)
-                rows_auto(L.A, OpRelax<1, FinT>{x, L.m, f, dst, *rho_fin}, gate, "relax+dot");
-            else
-                rows_auto(L.A, OpRelax<0, NoFin>{x, L.m, f, dst, {}}, gate, "relax");
-            if (dst == y) std::swap(x, y);
-        }
-        return rho_fin != nullptr;
-    }
     if (npost == 0) {
-        ck(cudaMemcpyAsync(out, x, L.n * sizeof(double), cudaMemcpyDeviceToDevice, stream), "copy");
+        for_parts([&](Part& p, size_t i) {
+            ck(cudaMemcpyAsync(osel(p), X[i], p.lv[l].n * sizeof(double), cudaMemcpyDeviceToDevice, stream), "copy");
+        });
         return false;
     }
-    for (int s = 0; s < npost; ++s) {
-        for (int k = 0; k < K; ++k) {
-            const bool lastk = (s == npost - 1) && (k == K - 1);
-            double* dst = lastk ? out : y;
-            if (lastk && rho_fin)
-                rows_auto(L.A,
-                          OpCheb<1, FinT>{x, f, L.diag, L.p, dst, L.cheb_alpha[k], L.cheb_beta[k], prm.cheb_scaled,
-                                          k == 0, *rho_fin},
-                          gate, "cheb+dot");
-            else
-                rows_auto(L.A,
-                          OpCheb<0, NoFin>{x, f, L.diag, L.p, dst, L.cheb_alpha[k], L.cheb_beta[k], prm.cheb_scaled,
-                                           k == 0, {}},
-                          gate, "cheb");
-            if (!lastk) std::swap(x, y);
-        }
+    const int sweeps = cheb ? npost * K : npost;
+    for (int s = 0; s < sweeps; ++s) {
+        const bool last = s == sweeps - 1;
+        exchange(l, xsel);
+        for_parts([&](Part& p, size_t i) {
+            DevLevel& L = p.lv[l];
+            double* dst = last ? osel(p) : Y[i];
+            if (!cheb) {
+                if (last && with_rho)
+                    rows(p, L.A, OpRelax<1, FinRho>{X[i], L.m, fsel(p), dst, FinRho{p.ks}}, gate(p), "relax+dot");
+                else
+                    rows(p, L.A, OpRelax<0, NoFin>{X[i], L.m, fsel(p), dst, {}}, gate(p), "relax");
+            } else {
+                const int k = s % K;
+                if (last && with_rho)
+                    rows(p, L.A,
+                         OpCheb<1, FinRho>{X[i], fsel(p), L.diag, L.p, dst, L.cheb_alpha[k], L.cheb_beta[k],
+                                           prm.cheb_scaled, k == 0, FinRho{p.ks}},
+                         gate(p), "cheb+dot");
+                else
+                    rows(p, L.A,
+                         OpCheb<0, NoFin>{X[i], fsel(p), L.diag, L.p, dst, L.cheb_alpha[k], L.cheb_beta[k],
+                                          prm.cheb_scaled, k == 0, {}},
+                         gate(p), "cheb");
+            }
+        });
+        if (!last) swap_xy();
     }
-    return rho_fin != nullptr;
+    if (with_rho) allreduce_fin(1, [](Part& p) { return FinRho{p.ks}; }, gate);
+    return with_rho;
 }
 
 // One CG iteration (§8c c-1): z = M r, rho = (r, z) [fused in the last V-cycle
 // kernel]; p' = z + beta p, q = A p', sigma = (p', q) [one kernel];
 // x += alpha p', r -= alpha q, (r, r) [one kernel].
-void Handle::cg_iteration(double* x, int parity) {
-    const int32_t* gate = &ks->done;
-    double* pold = parity ? pb : pa;
-    double* pnew = parity ? pa : pb;
-    DevLevel& L0 = lv[0];
-    FinRho frho{ks};
-    if (!vcycle<FinRho>(0, r, z, gate, &frho)) vec(L0.n, VDot<FinRho>{r, z, frho}, gate, "dot(r,z)");
-    rows_auto(L0.A, OpCgDir<FinSigma>{z, pold, pnew, q, ks, 0.0, FinSigma{ks}}, gate, "cg dir");
-    vec(L0.n, VCgUpdate{x, r, pnew, q, ks, 0.0, FinCgUpdate{ks}}, gate, "cg update");
+void Handle::cg_iteration(int parity) {
+    GSel gate = [](Part& p) { return (const int32_t*)&p.ks->done; };
+    auto pold = [parity](Part& p) { return parity ? p.pb : p.pa; };
+    auto pnew = [parity](Part& p) { return parity ? p.pa : p.pb; };
+    if (!vcycle(0, [](Part& p) { return (const double*)p.r; }, [](Part& p) { return p.z; }, gate, true)) {
+        for (Part& p : parts) vec(p, p.lv[0].n, VDot<FinRho>{p.r, p.z, FinRho{p.ks}}, gate(p), "dot(r,z)");
+        allreduce_fin(1, [](Part& p) { return FinRho{p.ks}; }, gate);
+    }
+    exchange(0, [](Part& p) { return p.z; });
+    if (distributed())  // ghost entries of p' = z + beta p, formed redundantly
+        for (Part& p : parts) {
+            DevLevel& L = p.lv[0];
+            if (L.ng == 0) continue;
+            const int32_t* g = gate(p);
+            double *zg = p.z + L.n, *pog = pold(p) + L.n, *png = pnew(p) + L.n;
+            launch(AMG_PROF_VECTOR, 24.0 * L.ng, "ghost dir", [&] {
+                ghost_dir_kernel<<<grid_for(L.ng), kBlock, 0, stream>>>(zg, pog, png, L.ng, p.ks, g);
+            });
+        }
+    for (Part& p : parts)
+        rows(p, p.lv[0].A, OpCgDir<FinSigma>{p.z, pold(p), pnew(p), p.q, p.ks, 0.0, FinSigma{p.ks}}, gate(p), "cg dir");
+    allreduce_fin(1, [](Part& p) { return FinSigma{p.ks}; }, gate);
+    for (Part& p : parts)
+        vec(p, p.lv[0].n, VCgUpdate{p.xcur, p.r, pnew(p), p.q, p.ks, 0.0, FinCgUpdate{p.ks}}, gate(p), "cg update");
+    allreduce_fin(1, [](Part& p) { return FinCgUpdate{p.ks}; }, gate);
 }
 
 // One BiCGStab iteration (§8c c-1).
-void Handle::bicgstab_iteration(double* x) {
-    const int32_t* gate = &ks->done;
-    const int32_t* gate2 = &ks->skip2;
-    DevLevel& L0 = lv[0];
-    vec(L0.n, VBiP{r, v, pa, ks, 0, 0, 0, {}}, gate, "bicg p");
-    vcycle_plain(0, pa, ph, gate);
-    rows_auto(L0.A, OpSpmvDot<1, FinBiAlpha>{ph, rhat, v, FinBiAlpha{ks}}, gate, "v=A ph");
-    vec(L0.n, VBiS{r, v, s, ks, 0.0, FinBiS{ks}}, gate, "bicg s");
-    vcycle_plain(0, s, sh, gate2);
-    rows_auto(L0.A, OpSpmvDot<2, FinBiOmega>{sh, s, tv, FinBiOmega{ks}}, gate2, "t=A sh");
-    vec(L0.n, VBiX{x, r, ph, sh, s, tv, rhat, ks, 0, 0, 0, FinBiX{ks}}, gate, "bicg x");
+void Handle::bicgstab_iteration() {
+    GSel gate = [](Part& p) { return (const int32_t*)&p.ks->done; };
+    GSel gate2 = [](Part& p) { return (const int32_t*)&p.ks->skip2; };
+    for (Part& p : parts) vec(p, p.lv[0].n, VBiP{p.r, p.v, p.pa, p.ks, 0, 0, 0, {}}, gate(p), "bicg p");
+    vcycle(0, [](Part& p) { return (const double*)p.pa; }, [](Part& p) { return p.ph; }, gate, false);
+    exchange(0, [](Part& p) { return p.ph; });
+    for (Part& p : parts)
+        rows(p, p.lv[0].A, OpSpmvDot<1, FinBiAlpha>{p.ph, p.rhat, p.v, FinBiAlpha{p.ks}}, gate(p), "v=A ph");
+    allreduce_fin(1, [](Part& p) { return FinBiAlpha{p.ks}; }, gate);
+    for (Part& p : parts) vec(p, p.lv[0].n, VBiS{p.r, p.v, p.s, p.ks, 0.0, FinBiS{p.ks}}, gate(p), "bicg s");
+    allreduce_fin(1, [](Part& p) { return FinBiS{p.ks}; }, gate);
+    vcycle(0, [](Part& p) { return (const double*)p.s; }, [](Part& p) { return p.sh; }, gate2, false);
+    exchange(0, [](Part& p) { return p.sh; });
+    for (Part& p : parts)
+        rows(p, p.lv[0].A, OpSpmvDot<2, FinBiOmega>{p.sh, p.s, p.tv, FinBiOmega{p.ks}}, gate2(p), "t=A sh");
+    allreduce_fin(2, [](Part& p) { return FinBiOmega{p.ks}; }, gate2);
+    for (Part& p : parts)
+        vec(p, p.lv[0].n, VBiX{p.xcur, p.r, p.ph, p.sh, p.s, p.tv, p.rhat, p.ks, 0, 0, 0, FinBiX{p.ks}}, gate(p),
+            "bicg x");
+    allreduce_fin(2, [](Part& p) { return FinBiX{p.ks}; }, gate);
 }
 
-amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter, int32_t* iters,
-                         double* rel) {
-    DevLevel& L0 = lv[0];
-    const int64_t n = L0.n;
+// f, x: device vectors.  Single part: length n.  Virtual parts: the GLOBAL
+// vectors (each part works on its slice).  NCCL: this rank's slice.
+amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter, int32_t* iters, double* rel) {
     const bool bicg = prm.solver == 1;
+    const bool dist = distributed();
     const int64_t launches0 = launches;
-    std::fill(acc_ms, acc_ms + 8, 0.0);
-    std::fill(acc_bytes, acc_bytes + 8, 0.0);
-    std::fill(acc_launches, acc_launches + 8, 0);
-    alg_bytes = 0;
     collect(rec_direct, 0, true);  // discard launches issued outside a solve
     alg_bytes = 0;
     std::fill(acc_ms, acc_ms + 8, 0.0);
     std::fill(acc_bytes, acc_bytes + 8, 0.0);
     std::fill(acc_launches, acc_launches + 8, 0);
     cur_iter = -1;
+    GSel nogate = [](Part&) { return (const int32_t*)nullptr; };
     ck(cudaEventRecord(ev0, stream), "event");
+    // right-hand side / solution slices of every part
+    for (Part& p : parts) {
+        const int64_t off = virt ? p.row0 : 0;
+        p.fcur = f + off;
+        if (!dist) {
+            p.xcur = x;  // no ghosts: work on the caller's vector
+        } else {
+            p.xcur = p.xw;
+            ck(cudaMemcpyAsync(p.xw, x + off, p.lv[0].n * sizeof(double), cudaMemcpyDeviceToDevice, stream), "x in");
+        }
+    }
     // scalars: maxiter in, everything else computed on the device
     std::memset(ks_host, 0, sizeof(KState));
     ks_host->maxiter = maxiter;
-    ck(cudaMemcpyAsync(ks, ks_host, sizeof(KState), cudaMemcpyHostToDevice, stream), "ks init");
-    vec(n, VNorm2{f, FinNorm{ks, tol}}, nullptr, "norm f");
-    rows_auto(L0.A, OpResidual<1, FinInitRes>{x, f, r, FinInitRes{ks}}, nullptr, "r0");
-    ck(cudaMemsetAsync(pa, 0, n * sizeof(double), stream), "memset");
-    ck(cudaMemsetAsync(pb, 0, n * sizeof(double), stream), "memset");
-    if (bicg) {
-        ck(cudaMemcpyAsync(rhat, r, n * sizeof(double), cudaMemcpyDeviceToDevice, stream), "copy");
-        ck(cudaMemsetAsync(v, 0, n * sizeof(double), stream), "memset");
+    for (Part& p : parts) ck(cudaMemcpyAsync(p.ks, ks_host, sizeof(KState), cudaMemcpyHostToDevice, stream), "ks init");
+    for (Part& p : parts) vec(p, p.lv[0].n, VNorm2{p.fcur, FinNorm{p.ks, tol}}, nullptr, "norm f");
+    allreduce_fin(1, [tol](Part& p) { return FinNorm{p.ks, tol}; }, nogate);
+    exchange(0, [](Part& p) { return p.xcur; });
+    for (Part& p : parts)
+        rows(p, p.lv[0].A, OpResidual<1, FinInitRes>{p.xcur, p.fcur, p.r, FinInitRes{p.ks}}, nullptr, "r0");
+    allreduce_fin(1, [](Part& p) { return FinInitRes{p.ks}; }, nogate);
+    for (Part& p : parts) {
+        const int64_t n = p.lv[0].n + p.lv[0].ng;
+        ck(cudaMemsetAsync(p.pa, 0, n * sizeof(double), stream), "memset");
+        ck(cudaMemsetAsync(p.pb, 0, n * sizeof(double), stream), "memset");
+        if (bicg) {
+            ck(cudaMemcpyAsync(p.rhat, p.r, p.lv[0].n * sizeof(double), cudaMemcpyDeviceToDevice, stream), "copy");
+            ck(cudaMemsetAsync(p.v, 0, p.lv[0].n * sizeof(double), stream), "memset");
+        }
     }
-    ck(cudaMemcpyAsync(ks_host, ks, sizeof(KState), cudaMemcpyDeviceToHost, stream), "ks read");
+    ck(cudaMemcpyAsync(ks_host, parts[0].ks, sizeof(KState), cudaMemcpyDeviceToHost, stream), "ks read");
     ck(cudaStreamSynchronize(stream), "sync");
     collect(rec_direct, 0, true);
     if (ks_host->nf == 0.0) {  // zero right-hand side: x = 0
-        ck(cudaMemsetAsync(x, 0, n * sizeof(double), stream), "memset");
+        for (Part& p : parts)
+            ck(cudaMemsetAsync(x + (virt ? p.row0 : 0), 0, p.lv[0].n * sizeof(double), stream), "memset");
         ck(cudaStreamSynchronize(stream), "sync");
         *iters = 0;
         *rel = 0.0;
@@ -845,9 +829,9 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
         for (int k = 0; k < 2; ++k) {
             cur_iter = k;
             if (bicg)
-                bicgstab_iteration(x);
+                bicgstab_iteration();
             else
-                cg_iteration(x, k);
+                cg_iteration(k);
         }
         cur_iter = -1;
     };
@@ -881,15 +865,23 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
         } else {
             two_iterations();
         }
-        ck(cudaMemcpyAsync(ks_host, ks, sizeof(KState), cudaMemcpyDeviceToHost, stream), "ks read");
+        ck(cudaMemcpyAsync(ks_host, parts[0].ks, sizeof(KState), cudaMemcpyDeviceToHost, stream), "ks read");
         ck(cudaStreamSynchronize(stream), "sync");
         const int ran = ks_host->iter - iter_before + (ks_host->done && ks_host->status ? 1 : 0);
         collect(use_graph ? rec_graph : rec_direct, ran, !use_graph);
     }
     // true residual |f - A x| / |f|
-    rows_auto(L0.A, OpResidual<1, FinTrueRes>{x, f, r, FinTrueRes{ks}}, nullptr, "true res");
+    exchange(0, [](Part& p) { return p.xcur; });
+    for (Part& p : parts)
+        rows(p, p.lv[0].A, OpResidual<1, FinTrueRes>{p.xcur, p.fcur, p.r, FinTrueRes{p.ks}}, nullptr, "true res");
+    allreduce_fin(1, [](Part& p) { return FinTrueRes{p.ks}; }, nogate);
+    if (dist)
+        for (Part& p : parts)
+            ck(cudaMemcpyAsync(x + (virt ? p.row0 : 0), p.xw, p.lv[0].n * sizeof(double), cudaMemcpyDeviceToDevice,
+                               stream),
+               "x out");
     ck(cudaEventRecord(ev1, stream), "event");
-    ck(cudaMemcpyAsync(ks_host, ks, sizeof(KState), cudaMemcpyDeviceToHost, stream), "ks read");
+    ck(cudaMemcpyAsync(ks_host, parts[0].ks, sizeof(KState), cudaMemcpyDeviceToHost, stream), "ks read");
     ck(cudaStreamSynchronize(stream), "sync");
     collect(rec_direct, 0, true);
     *iters = ks_host->iter;
@@ -917,6 +909,22 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
     const amg_status st = ks_host->res <= ks_host->tolnf ? AMG_OK : AMG_NOT_CONVERGED;
     stats.status = st;
     return st;
+}
+
+// z = M r for every part (r, z: device; global vectors in virtual mode).
+void Handle::precond(const double* r, double* z) {
+    GSel nogate = [](Part&) { return (const int32_t*)nullptr; };
+    if (!distributed()) {
+        vcycle(0, [r](Part&) { return r; }, [z](Part&) { return z; }, nogate, false);
+        return;
+    }
+    for (Part& p : parts)  // the V-cycle input needs a ghost region: copy into p.s
+        ck(cudaMemcpyAsync(p.s, r + (virt ? p.row0 : 0), p.lv[0].n * sizeof(double), cudaMemcpyDeviceToDevice, stream),
+           "copy");
+    vcycle(0, [](Part& p) { return (const double*)p.s; }, [](Part& p) { return p.sh; }, nogate, false);
+    for (Part& p : parts)
+        ck(cudaMemcpyAsync(z + (virt ? p.row0 : 0), p.sh, p.lv[0].n * sizeof(double), cudaMemcpyDeviceToDevice, stream),
+           "copy");
 }
 
 // ---- upload -------------------------------------------------------------------
@@ -970,9 +978,9 @@ DMat upload_mat(Handle& H, const Csr& A, int64_t* bytes) {
     d.ncols = A.ncols;
     d.nnz = A.nnz();
     if (d.nnz >= INT32_MAX) throw CudaError{"level has >= 2^31 nonzeros"};
+    if (d.nrows == 0) return d;
     d.fmt = pick_format(A);
-    d.is_csr = d.fmt == Fmt::CSR;
-    if (d.is_csr) {
+    if (d.fmt == Fmt::CSR) {
         const double avg = A.nrows ? (double)A.nnz() / (double)A.nrows : 0.0;
         int G = 1;
         if (avg >= 96) G = 16;
@@ -1001,7 +1009,6 @@ DMat upload_mat(Handle& H, const Csr& A, int64_t* bytes) {
         d.sell.col = H.upload(S.col);
         d.sell.val = H.upload(S.val);
         d.stored = (int64_t)S.col.size();
-        for (int64_t q = 0; q < S.nslices; ++q) d.sell_wmax = std::max(d.sell_wmax, (S.sptr[q + 1] - S.sptr[q]) / 32);
         *bytes += (int64_t)(S.sptr.size() * 8 + S.col.size() * 12);
     } else {  // TMA-staged SELL-C: lanes per row T from the longest row, C = 32 / T
         int64_t lmax = 0;
@@ -1048,17 +1055,17 @@ void cheb_coeffs(double d, double c, int K, std::vector<double>& a, std::vector<
     }
 }
 
-// Algorithmic HBM bytes of one V-cycle on level l: every matrix
+// Algorithmic HBM bytes of one V-cycle on a level: every matrix
 // read once per pass (12 B per entry + 4 B per row), every vector read or
 // written once per kernel that touches it.
-double level_alg_bytes(const DevLevel& L, const amg_params& p, bool coarsest) {
-    const double n = (double)L.n, z = (double)L.nnzA;
+double level_alg_bytes(int64_t n_, int64_t z_, int64_t p_, int64_t c_, const amg_params& p, bool coarsest) {
+    const double n = (double)n_, z = (double)z_;
     if (coarsest) return 8.0 * n * n + 16.0 * n;
-    const double pp = (double)L.nnzP, c = (double)L.nc;
+    const double pp = (double)p_, c = (double)c_;
     const double apass_relax = 12 * z + 4 * n + 32 * n;  // x, m, f read, out written
     const double restrict_b = 12 * pp + 4 * c + 8 * n + 8 * c;
     if (p.relax == 2) {
-        const double step = 12 * z + 4 * n + 40 * n;  // x, f, p read; p, xo written
+        const double step = 12 * z + 4 * n + 48 * n;  // x, f, diag, p read; p, xo written
         const double K = p.cheb_degree;
         const double pre = p.npre > 0 ? 32 * n + (K * p.npre - 1) * step : 0;
         const double post = p.npost * K * step;
@@ -1068,7 +1075,7 @@ double level_alg_bytes(const DevLevel& L, const amg_params& p, bool coarsest) {
     }
     double pre = 0, prol = 0;
     if (p.npre == 1) {
-        pre = 12 * z + 4 * n + 32 * n;  // m, f read (gathered once), t written
+        pre = 12 * z + 4 * n + 24 * n;            // m, f gathered, t written
         prol = 12 * pp + 4 * n + 8 * c + 24 * n;  // m, f read, x written
     } else {
         pre = (p.npre > 0 ? 24 * n + (p.npre - 1) * apass_relax : 8 * n) + 12 * z + 4 * n + 24 * n;
@@ -1077,14 +1084,108 @@ double level_alg_bytes(const DevLevel& L, const amg_params& p, bool coarsest) {
     return pre + restrict_b + prol + p.npost * apass_relax;
 }
 
+// Upload one rank part into a device Part.
+void upload_part(Handle& H, const RankPart& RP, Part& P) {
+    const amg_params& prm = H.prm;
+    const int nlev = (int)RP.lv.size();
+    P.rank = RP.rank;
+    P.row0 = RP.lv[0].row0;
+    P.row1 = RP.lv[0].row1;
+    P.lv.resize(nlev);
+    for (int l = 0; l < nlev; ++l) {
+        const LevelPart& lp = RP.lv[l];
+        const HostLevel& hl = H.host.levels[l];
+        DevLevel& L = P.lv[l];
+        const bool coarsest = l == nlev - 1;
+        L.replicated = lp.replicated;
+        L.next_replicated = lp.next_replicated;
+        L.n = lp.A.nrows;
+        L.ng = lp.replicated ? 0 : lp.halo.nghost;
+        L.crow0 = lp.crow0;
+        L.crow1 = lp.crow1;
+        L.nnzA = lp.A.nnz();
+        L.nnzP = coarsest ? 0 : lp.P.nnz();
+        L.nnzR = coarsest ? 0 : lp.R.nnz();
+        L.nc = coarsest ? 0 : lp.P.ncols;
+        if (prm.relax == 2 && !coarsest)
+            cheb_coeffs(hl.cheb_d, hl.cheb_c, prm.cheb_degree, L.cheb_alpha, L.cheb_beta);
+        L.alg_bytes = level_alg_bytes(L.n, L.nnzA, L.nnzP, coarsest ? 0 : lp.crow1 - lp.crow0, prm, coarsest);
+        const int64_t nv = L.n + L.ng;
+        if (!coarsest || nlev == 1) {
+            L.A = upload_mat(H, lp.A, &L.dev_bytes);
+            L.padA = L.A.stored;
+        } else {
+            L.padA = L.nnzA;
+        }
+        if (!coarsest) {
+            L.P = upload_mat(H, lp.P, &L.dev_bytes);
+            L.R = upload_mat(H, lp.R, &L.dev_bytes);
+            if (prm.relax != 2) L.m = H.upload(lp.m);
+            if (prm.relax == 2) L.diag = H.upload(lp.diag);  // Chebyshev D^-1 scaling
+            L.x = H.dalloc(nv);
+            L.y = H.dalloc(nv);
+            L.t = H.dalloc(nv);
+            if (prm.relax == 2) L.p = H.dalloc(nv);
+            L.dev_bytes += 8 * nv * (prm.relax == 2 ? 5 : 4);
+        }
+        if (l > 0) {
+            L.f = H.dalloc(nv);
+            L.o = H.dalloc(nv);
+            L.dev_bytes += 16 * nv;
+        }
+        if (!lp.replicated) {
+            L.plan = lp.halo;
+            L.nsend = (int64_t)lp.halo.send_idx.size();
+            if (L.nsend) {
+                L.send_idx = H.upload(lp.halo.send_idx);
+                L.sendbuf = H.dalloc(L.nsend);
+            }
+        }
+    }
+    P.nL = RP.lv.back().A.nrows;
+    P.coarse_inv = H.upload(H.host.coarse_inv);
+    P.lv.back().dev_bytes += 8 * P.nL * P.nL;
+    const int64_t nv0 = P.lv[0].n + P.lv[0].ng;
+    void* pp = nullptr;
+    ck(cudaMalloc(&pp, sizeof(KState)), "cudaMalloc");
+    H.allocs.push_back(pp);
+    P.ks = static_cast<KState*>(pp);
+    ck(cudaMalloc(&pp, (size_t)H.num_sms * 8 * 4 * sizeof(double)), "cudaMalloc");
+    H.allocs.push_back(pp);
+    P.red.partial = static_cast<double*>(pp);
+    ck(cudaMalloc(&pp, 64), "cudaMalloc");
+    H.allocs.push_back(pp);
+    ck(cudaMemset(pp, 0, 64), "memset");
+    P.red.ticket = static_cast<unsigned int*>(pp);
+    if (H.distributed()) P.red.defer = H.dalloc(4);
+    P.r = H.dalloc(nv0);
+    P.z = H.dalloc(nv0);
+    P.pa = H.dalloc(nv0);
+    P.pb = H.dalloc(nv0);
+    P.q = H.dalloc(nv0);
+    if (H.distributed()) {
+        P.xw = H.dalloc(nv0);
+        P.s = H.dalloc(nv0);  // also the precond input buffer
+        P.sh = H.dalloc(nv0);
+    }
+    if (prm.solver == 1) {
+        P.rhat = H.dalloc(nv0);
+        P.v = H.dalloc(nv0);
+        if (!P.s) P.s = H.dalloc(nv0);
+        if (!P.sh) P.sh = H.dalloc(nv0);
+        P.ph = H.dalloc(nv0);
+        P.tv = H.dalloc(nv0);
+    }
+}
+
 }  // namespace
 
 }  // namespace amgb
 
 // ============================================================ C ABI
 
-using amgb::Handle;
 using amgb::ck;
+using amgb::Handle;
 
 struct amg_hierarchy {
     std::unique_ptr<Handle> h;
@@ -1123,7 +1224,8 @@ void amg_params_default(amg_params* p) {
 const char* amg_last_error(void) { return amgb::g_err.c_str(); }
 
 const char* amg_version(void) {
-    return "amgb 0.1 (sm_100a; SELL-32 fp64 solve phase; host SA setup)";
+    return "amgb 0.2 (sm_100a; TMA-staged SELL / SELL-32 / row-block CSR fp64 solve phase; host SA setup; "
+           "NCCL row partition)";
 }
 
 static amg_status check_params(const amg_params& p) {
@@ -1143,13 +1245,17 @@ static amg_status check_params(const amg_params& p) {
     return AMG_OK;
 }
 
-amg_status amg_setup(int64_t n, const int64_t* ptr, const int32_t* col, const double* val,
-                     const amg_params* prm_in, amg_handle* out) {
+// Common setup: host hierarchy, partition, upload.  rank = -1: every part in
+// this process (virtual); nranks = 1: single GPU.
+static amg_status setup_impl(int64_t n, const int64_t* ptr, const int32_t* col, const double* val,
+                             const amg_params* prm_in, int nranks, int rank, int64_t gather_below,
+                             const uint8_t* nccl_id, amg_handle* out) {
     using namespace amgb;
     if (!out) return set_error(AMG_E_INVALID_ARG, "out is NULL");
     *out = nullptr;
     if (n <= 0 || n > INT32_MAX || !ptr || (!col && ptr[n] > 0) || (!val && ptr[n] > 0))
         return set_error(AMG_E_INVALID_ARG, "n must be in [1, 2^31) and ptr/col/val non-NULL");
+    if (nranks < 1 || rank < -1 || rank >= nranks) return set_error(AMG_E_INVALID_ARG, "nranks / rank");
     amg_params prm;
     if (prm_in)
         prm = *prm_in;
@@ -1159,6 +1265,8 @@ amg_status amg_setup(int64_t n, const int64_t* ptr, const int32_t* col, const do
     auto H = std::make_unique<Handle>();
     H->prm = prm;
     H->sync_debug = std::getenv("AMGB_SYNC_DEBUG") != nullptr;
+    H->nranks = nranks;
+    H->virt = nranks > 1 && rank < 0;
     try {
         validate_csr(n, ptr, col);
         Csr A0;
@@ -1180,25 +1288,23 @@ amg_status amg_setup(int64_t n, const int64_t* ptr, const int32_t* col, const do
         sp.max_levels = prm.max_levels;
         sp.dense_max = prm.dense_max;
         H->host = build_hierarchy(std::move(A0), sp);
+        H->lg = first_replicated_level(H->host, nranks, gather_below);
+        H->starts = level_starts(H->host, nranks, H->lg);
+        if (nranks == 1) {
+            H->host_parts.push_back(build_rank_part(H->host, 1, 0, H->lg, H->starts));
+        } else if (rank < 0) {
+            for (int r = 0; r < nranks; ++r)
+                H->host_parts.push_back(build_rank_part(H->host, nranks, r, H->lg, H->starts));
+        } else {
+            H->host_parts.push_back(build_rank_part(H->host, nranks, rank, H->lg, H->starts));
+        }
     } catch (const SetupError& e) {
         return set_error((amg_status)e.code, e.msg);
     } catch (const std::bad_alloc&) {
         return set_error(AMG_E_OOM, "host allocation failed during setup");
+    } catch (const std::exception& e) {
+        return set_error(AMG_E_INVALID_ARG, e.what());
     }
-    const int nlev = (int)H->host.levels.size();
-    H->lv.resize(nlev);
-    for (int l = 0; l < nlev; ++l) {
-        const HostLevel& hl = H->host.levels[l];
-        DevLevel& L = H->lv[l];
-        L.n = hl.A.nrows;
-        L.nnzA = hl.A.nnz();
-        L.nc = l + 1 < nlev ? hl.P.ncols : 0;
-        L.nnzP = l + 1 < nlev ? hl.P.nnz() : 0;
-        if (prm.relax == 2 && l + 1 < nlev)
-            cheb_coeffs(hl.cheb_d, hl.cheb_c, prm.cheb_degree, L.cheb_alpha, L.cheb_beta);
-        L.alg_bytes = level_alg_bytes(L, prm, l == nlev - 1);
-    }
-    H->nL = H->host.levels.back().A.nrows;
     if (prm.device < 0) {
         *out = new amg_hierarchy{std::move(H)};
         return AMG_OK;
@@ -1211,66 +1317,19 @@ amg_status amg_setup(int64_t n, const int64_t* ptr, const int32_t* col, const do
         ck(cudaEventCreate(&H->ev1), "event");
         ck(cudaStreamCreate(&H->own_stream), "stream");  // capture needs a non-legacy stream
         H->stream = H->own_stream;
-        for (int l = 0; l < nlev; ++l) {
-            const HostLevel& hl = H->host.levels[l];
-            DevLevel& L = H->lv[l];
-            const bool coarsest = l == nlev - 1;
-            if (!coarsest) {
-                L.A = upload_mat(*H, hl.A, &L.dev_bytes);
-                L.P = upload_mat(*H, hl.P, &L.dev_bytes);
-                L.R = upload_mat(*H, hl.R, &L.dev_bytes);
-                L.padA = L.A.stored;
-                if (prm.relax != 2) L.m = H->upload(hl.m);
-                if (prm.relax == 2) L.diag = H->upload(hl.diag);  // Chebyshev D^-1 scaling
-                L.x = H->dalloc(L.n);
-                L.y = H->dalloc(L.n);
-                L.t = H->dalloc(L.n);
-                if (prm.relax == 2) L.p = H->dalloc(L.n);
-                L.dev_bytes += 8 * L.n * (prm.relax == 2 ? 5 : 4);
-            } else {
-                L.padA = L.nnzA;
-            }
-            if (l > 0) {
-                L.f = H->dalloc(L.n);
-                L.o = H->dalloc(L.n);
-                L.dev_bytes += 16 * L.n;
-            }
+        if (nranks > 1 && rank >= 0) {
+            Nccl& nc = Nccl::get();
+            if (!nc.ok) return set_error(AMG_E_CUDA, "NCCL unavailable: " + nc.error);
+            ckn(nccl_comm_init(&H->nccl, nranks, nccl_id, rank), "ncclCommInitRank");
         }
-        H->coarse_inv = H->upload(H->host.coarse_inv);
-        H->lv.back().dev_bytes += 8 * H->nL * H->nL;
-        if (nlev == 1) {  // single level: the level-0 A is needed by the Krylov loop
-            int64_t dummy = 0;
-            H->lv[0].A = upload_mat(*H, H->host.levels[0].A, &H->lv[0].dev_bytes);
-            H->lv[0].padA = H->lv[0].A.stored;
-            (void)dummy;
+        H->parts.resize(H->host_parts.size());
+        for (size_t i = 0; i < H->parts.size(); ++i) upload_part(*H, H->host_parts[i], H->parts[i]);
+        if (H->virt) {
+            std::vector<double*> ptrs;
+            for (auto& p : H->parts) ptrs.push_back(p.red.defer);
+            H->d_defer_ptrs = H->upload(ptrs);
         }
-        const int64_t n = H->lv[0].n;
-        void* p = nullptr;
-        ck(cudaMalloc(&p, sizeof(KState)), "cudaMalloc");
-        H->allocs.push_back(p);
-        H->ks = static_cast<amgb::KState*>(p);
-        ck(cudaMallocHost(&H->ks_host, sizeof(amgb::KState)), "cudaMallocHost");
-        ck(cudaMalloc(&p, (size_t)H->num_sms * 8 * 4 * sizeof(double)), "cudaMalloc");
-        H->allocs.push_back(p);
-        H->red.partial = static_cast<double*>(p);
-        ck(cudaMalloc(&p, 64), "cudaMalloc");
-        H->allocs.push_back(p);
-        ck(cudaMemset(p, 0, 64), "memset");
-        H->red.ticket = static_cast<unsigned int*>(p);
-        H->zero_gate = reinterpret_cast<int32_t*>(static_cast<char*>(p) + 32);
-        H->r = H->dalloc(n);
-        H->z = H->dalloc(n);
-        H->pa = H->dalloc(n);
-        H->pb = H->dalloc(n);
-        H->q = H->dalloc(n);
-        if (prm.solver == 1) {
-            H->rhat = H->dalloc(n);
-            H->v = H->dalloc(n);
-            H->s = H->dalloc(n);
-            H->sh = H->dalloc(n);
-            H->ph = H->dalloc(n);
-            H->tv = H->dalloc(n);
-        }
+        ck(cudaMallocHost(&H->ks_host, sizeof(KState)), "cudaMallocHost");
         ck(cudaDeviceSynchronize(), "setup sync");
         H->on_device = true;
     } catch (const amgb::CudaError& e) {
@@ -1279,6 +1338,33 @@ amg_status amg_setup(int64_t n, const int64_t* ptr, const int32_t* col, const do
     }
     *out = new amg_hierarchy{std::move(H)};
     return AMG_OK;
+}
+
+amg_status amg_setup(int64_t n, const int64_t* ptr, const int32_t* col, const double* val,
+                     const amg_params* prm_in, amg_handle* out) {
+    return setup_impl(n, ptr, col, val, prm_in, 1, 0, 0, nullptr, out);
+}
+
+amg_status amg_nccl_unique_id(uint8_t id[128]) {
+    if (!id) return set_error(AMG_E_INVALID_ARG, "id is NULL");
+    amgb::Nccl& nc = amgb::Nccl::get();
+    if (!nc.ok) return set_error(AMG_E_CUDA, "NCCL unavailable: " + nc.error);
+    const int r = nc.getUniqueId(id);
+    if (r != 0) return set_error(AMG_E_CUDA, "ncclGetUniqueId failed");
+    return AMG_OK;
+}
+
+amg_status amg_setup_dist(int64_t n, const int64_t* ptr, const int32_t* col, const double* val,
+                          const amg_params* prm, const amg_dist* d, amg_handle* out) {
+    if (!d) return set_error(AMG_E_INVALID_ARG, "dist descriptor is NULL");
+    const bool on_device = !prm || prm->device >= 0;
+    if (d->nranks > 1 && d->rank >= 0 && on_device) {  // NCCL mode needs rank 0's unique id
+        bool zero = true;
+        for (int i = 0; i < 128; ++i) zero &= d->nccl_id[i] == 0;
+        if (zero) return set_error(AMG_E_INVALID_ARG, "nccl_id not set (amg_nccl_unique_id on rank 0, then broadcast)");
+    }
+    return setup_impl(n, ptr, col, val, prm, d->nranks, d->rank, d->gather_below > 0 ? d->gather_below : (1 << 17),
+                      d->nccl_id, out);
 }
 
 void amg_destroy(amg_handle h) { delete h; }
@@ -1308,7 +1394,7 @@ amg_status amg_solve_host(amg_handle h, const double* f, double* x, double tol, 
     if (amg_status st = need_device(h)) return st;
     if (!f || !x || !iters || !rel) return set_error(AMG_E_INVALID_ARG, "f, x, iters, rel");
     Handle& H = *h->h;
-    const int64_t n = H.lv[0].n;
+    const int64_t n = H.virt ? H.host.levels[0].A.nrows : H.parts[0].lv[0].n;
     try {
         ck(cudaSetDevice(H.device), "cudaSetDevice");
         if (!H.hf) {
@@ -1332,7 +1418,7 @@ amg_status amg_precond_apply(amg_handle h, const double* r, double* z) {
     if (!r || !z || r == z) return set_error(AMG_E_INVALID_ARG, "r, z");
     try {
         ck(cudaSetDevice(h->h->device), "cudaSetDevice");
-        h->h->vcycle_plain(0, r, z, nullptr);
+        h->h->precond(r, z);
         ck(cudaGetLastError(), "launch");
     } catch (const amgb::CudaError& e) {
         return set_error(AMG_E_CUDA, e.msg);
@@ -1367,7 +1453,6 @@ amg_status amg_level_info_get(amg_handle h, int32_t l, amg_level_info* out) {
     const Handle& H = *h->h;
     if (l < 0 || l >= (int)H.host.levels.size()) return set_error(AMG_E_INVALID_ARG, "level out of range");
     const auto& hl = H.host.levels[l];
-    const auto& L = H.lv[l];
     const bool coarsest = l == (int)H.host.levels.size() - 1;
     std::memset(out, 0, sizeof(*out));
     out->rows = hl.A.nrows;
@@ -1376,9 +1461,11 @@ amg_status amg_level_info_get(amg_handle h, int32_t l, amg_level_info* out) {
     out->cols_P = coarsest ? 0 : hl.P.ncols;
     out->aggregates = coarsest ? 0 : hl.n_agg;
     out->is_coarsest = coarsest;
-    out->dev_bytes = L.dev_bytes;
-    out->padded_nnz_A = L.padA;
-    out->alg_bytes_vcycle = L.alg_bytes;
+    out->alg_bytes_vcycle = amgb::level_alg_bytes(hl.A.nrows, hl.A.nnz(), out->nnz_P, out->cols_P, H.prm, coarsest);
+    if (!H.parts.empty()) {
+        out->dev_bytes = H.parts[0].lv[l].dev_bytes;
+        out->padded_nnz_A = H.parts[0].lv[l].padA;
+    }
     return AMG_OK;
 }
 
@@ -1421,32 +1508,93 @@ amg_status amg_solve_stats_get(amg_handle h, amg_solve_stats* out) {
     return AMG_OK;
 }
 
+amg_status amg_dist_info(amg_handle h, int32_t* nranks, int32_t* first_replicated, int64_t* row_starts) {
+    if (!h || !h->h || !nranks || !first_replicated) return set_error(AMG_E_INVALID_ARG, "NULL argument");
+    const Handle& H = *h->h;
+    *nranks = H.nranks;
+    *first_replicated = H.lg;
+    if (row_starts)
+        for (int r = 0; r <= H.nranks; ++r) row_starts[r] = H.starts[0][r];
+    return AMG_OK;
+}
+
+static const amgb::LevelPart* find_part(const Handle& H, int32_t rank, int32_t l) {
+    for (const auto& rp : H.host_parts)
+        if (rp.rank == rank && l >= 0 && l < (int)rp.lv.size()) return &rp.lv[l];
+    return nullptr;
+}
+
+amg_status amg_dist_level_info(amg_handle h, int32_t rank, int32_t l, int64_t out[12]) {
+    if (!h || !h->h || !out) return set_error(AMG_E_INVALID_ARG, "NULL argument");
+    const amgb::LevelPart* lp = find_part(*h->h, rank, l);
+    if (!lp) return set_error(AMG_E_INVALID_ARG, "rank/level not held by this handle");
+    out[0] = lp->row0;
+    out[1] = lp->row1;
+    out[2] = lp->halo.nghost;
+    out[3] = lp->A.nnz();
+    out[4] = lp->P.nrows ? lp->P.nnz() : 0;
+    out[5] = lp->R.nrows ? lp->R.nnz() : 0;
+    out[6] = lp->crow0;
+    out[7] = lp->crow1;
+    out[8] = lp->replicated;
+    out[9] = (int64_t)lp->halo.send_idx.size();
+    out[10] = (int64_t)lp->halo.recv_peer.size();
+    out[11] = (int64_t)lp->halo.send_peer.size();
+    return AMG_OK;
+}
+
+amg_status amg_dist_export(amg_handle h, int32_t rank, int32_t l, const amg_dist_level_export* out) {
+    if (!h || !h->h || !out) return set_error(AMG_E_INVALID_ARG, "NULL argument");
+    const amgb::LevelPart* lp = find_part(*h->h, rank, l);
+    if (!lp) return set_error(AMG_E_INVALID_ARG, "rank/level not held by this handle");
+    copy_csr(lp->A, out->A_ptr, out->A_col, out->A_val);
+    if (lp->P.nrows) copy_csr(lp->P, out->P_ptr, out->P_col, out->P_val);
+    if (lp->R.nrows) copy_csr(lp->R, out->R_ptr, out->R_col, out->R_val);
+    const auto& hp = lp->halo;
+    if (out->ghost_global) std::copy(hp.ghost_global.begin(), hp.ghost_global.end(), out->ghost_global);
+    for (size_t k = 0; k < hp.recv_peer.size(); ++k) {
+        if (out->recv_peer) out->recv_peer[k] = hp.recv_peer[k];
+        if (out->recv_off) out->recv_off[k] = hp.recv_off[k];
+        if (out->recv_cnt) out->recv_cnt[k] = hp.recv_cnt[k];
+    }
+    for (size_t k = 0; k < hp.send_peer.size(); ++k) {
+        if (out->send_peer) out->send_peer[k] = hp.send_peer[k];
+        if (out->send_off) out->send_off[k] = hp.send_off[k];
+        if (out->send_cnt) out->send_cnt[k] = hp.send_cnt[k];
+    }
+    if (out->send_idx) std::copy(hp.send_idx.begin(), hp.send_idx.end(), out->send_idx);
+    return AMG_OK;
+}
+
 amg_status amg_level_op(amg_handle h, int32_t l, int32_t op, const double* x, const double* f, double* y) {
     using namespace amgb;
     if (amg_status st = need_device(h)) return st;
     Handle& H = *h->h;
-    const int nlev = (int)H.lv.size();
+    if (H.distributed()) return set_error(AMG_E_INVALID_ARG, "amg_level_op: single-GPU handles only");
+    Part& p = H.parts[0];
+    const int nlev = (int)p.lv.size();
     if (l < 0 || l >= nlev) return set_error(AMG_E_INVALID_ARG, "level out of range");
     const bool coarsest = l == nlev - 1;
-    DevLevel& L = H.lv[l];
+    DevLevel& L = p.lv[l];
+    Handle::GSel nogate = [](Part&) { return (const int32_t*)nullptr; };
     try {
         ck(cudaSetDevice(H.device), "cudaSetDevice");
         switch (op) {
             case AMG_OP_SPMV_A:
                 if (coarsest && nlev > 1) return set_error(AMG_E_INVALID_ARG, "coarsest A is stored dense");
-                H.rows_auto(L.A, OpSpmv{x, y}, nullptr, "spmv A");
+                H.rows(p, L.A, OpSpmv{x, y}, nullptr, "spmv A");
                 break;
             case AMG_OP_SPMV_P:
             case AMG_OP_SPMV_R:
                 if (coarsest) return set_error(AMG_E_INVALID_ARG, "no P/R on the coarsest level");
                 if (op == AMG_OP_SPMV_P)
-                    H.rows_auto(L.P, OpSpmv{x, y}, nullptr, "spmv P");
+                    H.rows(p, L.P, OpSpmv{x, y}, nullptr, "spmv P");
                 else
-                    H.rows_auto(L.R, OpSpmv{x, y}, nullptr, "spmv R");
+                    H.rows(p, L.R, OpSpmv{x, y}, nullptr, "spmv R");
                 break;
             case AMG_OP_RESIDUAL:
                 if (coarsest && nlev > 1) return set_error(AMG_E_INVALID_ARG, "coarsest A is stored dense");
-                H.rows_auto(L.A, OpResidual<0, NoFin>{x, f, y, {}}, nullptr, "residual");
+                H.rows(p, L.A, OpResidual<0, NoFin>{x, f, y, {}}, nullptr, "residual");
                 break;
             case AMG_OP_RELAX:
                 if (coarsest) return set_error(AMG_E_INVALID_ARG, "no smoother on the coarsest level");
@@ -1457,22 +1605,22 @@ amg_status amg_level_op(amg_handle h, int32_t l, int32_t op, const double* x, co
                     ck(cudaMemcpyAsync(a, x, L.n * sizeof(double), cudaMemcpyDeviceToDevice, H.stream), "copy");
                     for (int k = 0; k < H.prm.cheb_degree; ++k) {
                         double* dst = (k == H.prm.cheb_degree - 1) ? y : b;
-                        H.rows_auto(L.A,
-                                    OpCheb<0, NoFin>{a, f, L.diag, L.p, dst, L.cheb_alpha[k], L.cheb_beta[k],
-                                                     H.prm.cheb_scaled, k == 0, {}},
-                                    nullptr, "cheb");
+                        H.rows(p, L.A,
+                               OpCheb<0, NoFin>{a, f, L.diag, L.p, dst, L.cheb_alpha[k], L.cheb_beta[k],
+                                                H.prm.cheb_scaled, k == 0, {}},
+                               nullptr, "cheb");
                         std::swap(a, b);
                     }
                 } else {
-                    H.rows_auto(L.A, OpRelax<0, NoFin>{x, L.m, f, y, {}}, nullptr, "relax");
+                    H.rows(p, L.A, OpRelax<0, NoFin>{x, L.m, f, y, {}}, nullptr, "relax");
                 }
                 break;
             case AMG_OP_COARSE:
                 if (!coarsest) return set_error(AMG_E_INVALID_ARG, "not the coarsest level");
-                H.vcycle_plain(l, f, y, nullptr);
+                H.vcycle(l, [f](Part&) { return f; }, [y](Part&) { return y; }, nogate, false);
                 break;
             case AMG_OP_VCYCLE:
-                H.vcycle_plain(l, f, y, nullptr);
+                H.vcycle(l, [f](Part&) { return f; }, [y](Part&) { return y; }, nogate, false);
                 break;
             default:
                 return set_error(AMG_E_INVALID_ARG, "unknown op");

@@ -39,6 +39,8 @@ struct KState {
 struct Red {
     double* partial = nullptr;  // >= gridDim.x * 4
     unsigned int* ticket = nullptr;
+    double* defer = nullptr;    // multi-rank: store the block-summed totals here
+                                // (all-reduced, then finalized by fin_kernel)
 };
 
 // ---------------------------------------------------------------- loads
@@ -113,7 +115,11 @@ __device__ __forceinline__ void grid_reduce(double (&v)[NV], const Red& red, con
             for (int w = 0; w < nw; ++w) s += sh[k][w];
             tot[k] = s;
         }
-        fin(tot);
+        if (red.defer) {
+            for (int k = 0; k < NV; ++k) red.defer[k] = tot[k];
+        } else {
+            fin(tot);
+        }
         *red.ticket = 0u;
         __threadfence();
     }

@@ -98,9 +98,11 @@ void strength(const Csr& A, double eps, std::vector<uint8_t>& strong) {
 }
 
 // Greedy aggregation (§8c L2).  Returns the aggregate count.
-int64_t aggregate(const Csr& A, const std::vector<uint8_t>& strong, std::vector<int32_t>& id) {
+int64_t aggregate(const Csr& A, const std::vector<uint8_t>& strong, std::vector<int32_t>& id,
+                  std::vector<int64_t>* root) {
     const int64_t n = A.nrows;
     id.assign(n, -1);
+    if (root) root->clear();
     int64_t next = 0;
     // Phase 1 (sequential by definition: later roots depend on earlier ones)
     for (int64_t i = 0; i < n; ++i) {
@@ -111,6 +113,7 @@ int64_t aggregate(const Csr& A, const std::vector<uint8_t>& strong, std::vector<
         if (!free_nbhd) continue;
         const int32_t a = static_cast<int32_t>(next++);
         id[i] = a;
+        if (root) root->push_back(i);
         for (int64_t k = A.ptr[i]; k < A.ptr[i + 1]; ++k)
             if (strong[k]) id[A.col[k]] = a;
     }
@@ -136,7 +139,10 @@ int64_t aggregate(const Csr& A, const std::vector<uint8_t>& strong, std::vector<
     }
     // Phase 3: leftovers become singletons (provably empty; kept for safety).
     for (int64_t i = 0; i < n; ++i)
-        if (id[i] < 0) id[i] = static_cast<int32_t>(next++);
+        if (id[i] < 0) {
+            id[i] = static_cast<int32_t>(next++);
+            if (root) root->push_back(i);
+        }
     return next;
 }
 
@@ -416,13 +422,15 @@ HostHierarchy build_hierarchy(Csr A0, const SetupParams& prm) {
         std::vector<uint8_t> S;
         strength(L.A, eps, S);
         std::vector<int32_t> id;
-        const int64_t cnt = aggregate(L.A, S, id);
+        std::vector<int64_t> root;
+        const int64_t cnt = aggregate(L.A, S, id, &root);
         const bool slow = static_cast<double>(cnt) > 0.95 * static_cast<double>(n);
         if (cnt == n || (slow && prev_slow)) break;
         prev_slow = slow;
         L.P = prolongation(L.A, S, id, cnt, prm.smoothed, prm.p_omega);
         L.R = transpose(L.P);
         L.agg = std::move(id);
+        L.root = std::move(root);
         L.n_agg = cnt;
         Csr AP = multiply(L.A, L.P);
         Csr Ac = multiply(L.R, AP);

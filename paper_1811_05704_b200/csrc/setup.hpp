@@ -32,6 +32,7 @@ struct SetupParams {
 struct HostLevel {
     Csr A, P, R;                 // P, R empty on the coarsest level
     std::vector<int32_t> agg;    // aggregate of each row (non-coarsest)
+    std::vector<int64_t> root;   // root row of each aggregate (ascending: Phase-1 discovery order)
     int64_t n_agg = 0;
     std::vector<double> m;       // SPAI-0 / Jacobi diagonal
     std::vector<double> diag;    // a_ii (Chebyshev scaling)
@@ -54,7 +55,8 @@ void validate_csr(int64_t n, const int64_t* ptr, const int32_t* col);
 
 // Individual components (exposed for the C++ unit tests through the C ABI).
 void strength(const Csr& A, double eps, std::vector<uint8_t>& strong);
-int64_t aggregate(const Csr& A, const std::vector<uint8_t>& strong, std::vector<int32_t>& id);
+int64_t aggregate(const Csr& A, const std::vector<uint8_t>& strong, std::vector<int32_t>& id,
+                  std::vector<int64_t>* root = nullptr);
 Csr prolongation(const Csr& A, const std::vector<uint8_t>& strong, const std::vector<int32_t>& id,
                  int64_t n_agg, bool smoothed, double omega);
 Csr transpose(const Csr& A);
