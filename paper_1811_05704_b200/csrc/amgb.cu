@@ -298,8 +298,13 @@ struct Handle {
         else
             ck(cudaEventRecord(e, stream), "cudaEventRecord");
     }
+    bool trace = std::getenv("AMGB_TRACE") != nullptr;
     template <class F>
     void launch(int cls, double bytes, const char* what, F&& fn) {
+        if (trace) {
+            std::fprintf(stderr, "[amgb] launch %s\n", what);
+            std::fflush(stderr);
+        }
         Rec rc;
         rc.cls = cls;
         rc.iter = cur_iter;
@@ -452,6 +457,10 @@ struct Handle {
     // send/recv (one part per process) or device copies between parts.
     void exchange(int l, const Sel& sel) {
         if (!distributed() || parts[0].lv[l].replicated) return;
+        if (trace) {
+            std::fprintf(stderr, "[amgb] exchange level %d\n", l);
+            std::fflush(stderr);
+        }
         for (Part& p : parts) {
             DevLevel& L = p.lv[l];
             if (L.nsend == 0) continue;
@@ -516,6 +525,7 @@ struct Handle {
     // full vector sel(part); gather the other ranks' slices.
     void allgather_slices(int l_rep, const Sel& sel) {
         if (!distributed()) return;
+        if (l_rep >= (int)starts.size()) throw CudaError{"allgather_slices: level without a partition"};
         const std::vector<int64_t>& st = starts[l_rep];
         if (virt) {
             for (Part& p : parts)
@@ -658,7 +668,8 @@ bool Handle::vcycle(int l, const CSel& fsel, const Sel& osel, const GSel& gate, 
         // slice [crow0, crow1) of the full vector
         rows(p, L.R, OpSpmv{L.t, C.f + (next_rep ? L.crow0 : 0)}, gate(p), "restrict");
     });
-    if (next_rep) allgather_slices(l + 1, [&](Part& p) { return p.lv[l + 1].f; });
+    // entering the replicated levels: gather the other ranks' slices of f_{l+1}
+    if (next_rep && !parts[0].lv[l].replicated) allgather_slices(l + 1, [&](Part& p) { return p.lv[l + 1].f; });
     vcycle(l + 1, [&](Part& p) { return (const double*)p.lv[l + 1].f; }, [&](Part& p) { return p.lv[l + 1].o; }, gate,
            false);
     exchange(l + 1, [&](Part& p) { return p.lv[l + 1].o; });
