@@ -144,10 +144,11 @@ amg_status amg_setup(int64_t n, const int64_t *ptr, const int32_t *col, const do
 amg_status amg_solve(amg_handle h, const double *f, double *x, double tol, int32_t maxiter,
                      int32_t *iters, double *rel_resid);
 
-/* Same as amg_solve with HOST f and x: copies f and x to the device, solves,
- * copies x back, all inside the call (the end-to-end path). */
-amg_status amg_solve_host(amg_handle h, const double *f, double *x, double tol, int32_t maxiter,
-                          int32_t *iters, double *rel_resid);
+/* Same as amg_solve with HOST buffers (the end-to-end path): copies f (and the
+ * initial guess x0, unless x0 is NULL = zero guess) to the device, solves, and
+ * copies the solution into x, all inside the call.  x0 may equal x. */
+amg_status amg_solve_host(amg_handle h, const double *f, const double *x0, double *x, double tol,
+                          int32_t maxiter, int32_t *iters, double *rel_resid);
 
 /* z = M r: one V-cycle from a zero initial guess.  r, z:
  * DEVICE pointers (length n, distinct).  Asynchronous on the handle stream. */

@@ -100,7 +100,8 @@ _V = C.c_void_p
 _lib.amg_params_default.argtypes = [C.POINTER(AmgParams)]
 _lib.amg_setup.argtypes = [C.c_int64, _V, _V, _V, C.POINTER(AmgParams), C.POINTER(_V)]
 _lib.amg_solve.argtypes = [_V, _V, _V, C.c_double, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_double)]
-_lib.amg_solve_host.argtypes = _lib.amg_solve.argtypes
+_lib.amg_solve_host.argtypes = [_V, _V, _V, _V, C.c_double, C.c_int32, C.POINTER(C.c_int32),
+                                C.POINTER(C.c_double)]
 _lib.amg_precond_apply.argtypes = [_V, _V, _V]
 _lib.amg_set_stream.argtypes = [_V, _V]
 _lib.amg_set_profile.argtypes = [_V, C.c_int32]
@@ -340,15 +341,19 @@ class Hierarchy:
                     "amg_solve")
         return x, it.value, rel.value, st
 
-    def solve_host(self, f: np.ndarray, x: np.ndarray | None = None, tol=1e-8, maxiter=100):
-        """End-to-end solve with HOST arrays (copies inside the library call)."""
+    def solve_host(self, f: np.ndarray, x0: np.ndarray | None = None, tol=1e-8, maxiter=100,
+                   out: np.ndarray | None = None):
+        """End-to-end solve with HOST arrays (copies inside the library call).
+        x0 = None: zero initial guess (not copied).  out: solution buffer."""
         f = np.ascontiguousarray(f, np.float64)
-        x = np.zeros_like(f) if x is None else np.ascontiguousarray(x, np.float64)
+        if out is None:
+            out = np.empty_like(f)
+        x0p = None if x0 is None else _ptr(np.ascontiguousarray(x0, np.float64))
         self._sync_stream()
         it, rel = C.c_int32(), C.c_double()
-        st = _check(_lib.amg_solve_host(self._h, _ptr(f), _ptr(x), tol, maxiter, C.byref(it),
+        st = _check(_lib.amg_solve_host(self._h, _ptr(f), x0p, _ptr(out), tol, maxiter, C.byref(it),
                                         C.byref(rel)), "amg_solve_host")
-        return x, it.value, rel.value, st
+        return out, it.value, rel.value, st
 
     def precond(self, r, z=None):
         """z = M r: one V-cycle from zero (asynchronous on the current stream)."""

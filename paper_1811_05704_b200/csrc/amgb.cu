@@ -1400,8 +1400,8 @@ amg_status amg_solve(amg_handle h, const double* f, double* x, double tol, int32
     }
 }
 
-amg_status amg_solve_host(amg_handle h, const double* f, double* x, double tol, int32_t maxiter,
-                          int32_t* iters, double* rel) {
+amg_status amg_solve_host(amg_handle h, const double* f, const double* x0, double* x, double tol,
+                          int32_t maxiter, int32_t* iters, double* rel) {
     if (amg_status st = need_device(h)) return st;
     if (!f || !x || !iters || !rel) return set_error(AMG_E_INVALID_ARG, "f, x, iters, rel");
     Handle& H = *h->h;
@@ -1413,7 +1413,10 @@ amg_status amg_solve_host(amg_handle h, const double* f, double* x, double tol, 
             H.hx = H.dalloc(n);
         }
         ck(cudaMemcpyAsync(H.hf, f, n * sizeof(double), cudaMemcpyHostToDevice, H.stream), "H2D f");
-        ck(cudaMemcpyAsync(H.hx, x, n * sizeof(double), cudaMemcpyHostToDevice, H.stream), "H2D x");
+        if (x0)
+            ck(cudaMemcpyAsync(H.hx, x0, n * sizeof(double), cudaMemcpyHostToDevice, H.stream), "H2D x0");
+        else
+            ck(cudaMemsetAsync(H.hx, 0, n * sizeof(double), H.stream), "zero x0");
         amg_status st = H.solve(H.hf, H.hx, tol, maxiter, iters, rel);
         ck(cudaMemcpyAsync(x, H.hx, n * sizeof(double), cudaMemcpyDeviceToHost, H.stream), "D2H x");
         ck(cudaStreamSynchronize(H.stream), "sync");

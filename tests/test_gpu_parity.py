@@ -189,6 +189,9 @@ def test_solve_host_end_to_end():
     assert st == amgb.OK and abs(iters - o["iters"]) <= 1
     if iters == o["iters"]:
         assert np.linalg.norm(x - o["x"]) <= 1e-8 * np.linalg.norm(o["x"])
+    # explicit initial guess: restarting from the solution needs 0 iterations
+    x2, iters2, rel2, st2 = h.solve_host(f, x0=x, tol=1e-8)
+    assert iters2 == 0 and np.array_equal(x2, x)
 
 
 def test_configs1_150_permuted_full_size():
