@@ -70,6 +70,12 @@ __global__ void __launch_bounds__(kBlock) ghost_dir_kernel(const double* z, cons
         pn[i] = fma(beta, p[i], z[i]);
 }
 
+// device-side loop test of the Krylov iteration graph (conditional WHILE node):
+// keep iterating while the solve is not done
+__global__ void set_loop_kernel(cudaGraphConditionalHandle h, const int32_t* done) {
+    cudaGraphSetConditional(h, *reinterpret_cast<const volatile int32_t*>(done) ? 0u : 1u);
+}
+
 // ============================================================ host side
 
 namespace {
@@ -222,6 +228,7 @@ struct Handle {
     const double* graph_x = nullptr;
     int graph_prof_mask = 0;
     int64_t graph_kernels = 0;
+    bool graph_loop = false;  // the graph runs the whole loop (conditional WHILE node)
     // accounting
     int64_t launches = 0;
     amg_solve_stats stats{};
@@ -846,11 +853,69 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
         }
         cur_iter = -1;
     };
+    // Device-side loop: one graph launch runs every remaining iteration (a
+    // conditional WHILE node around two iterations + a loop-test kernel); the
+    // host waits once.  Used for single-part handles without event profiling
+    // (event nodes are not allowed inside conditional bodies).
+    const bool use_loop = use_graph && !dist && prof_mask == 0 && std::getenv("AMGB_NO_DEVICE_LOOP") == nullptr;
+    if (use_loop && !ks_host->done) {
+        if (!graph || !graph_loop || graph_x != x) {
+            drop_graph();
+            cudaGraph_t g;
+            ck(cudaGraphCreate(&g, 0), "graph create");
+            cudaGraphConditionalHandle cond;
+            ck(cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault), "cond handle");
+            cudaGraphNodeParams cp = {};
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = cond;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            cudaGraphNode_t node;
+            ck(cudaGraphAddNode(&node, g, nullptr, 0, &cp), "conditional node");
+            cudaGraph_t body = cp.conditional.phGraph_out[0];
+            const int64_t before = launches;
+            ck(cudaStreamBeginCaptureToGraph(stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal),
+               "capture body");
+            capturing = true;
+            try {
+                two_iterations();
+                launch(AMG_PROF_VECTOR, 0, "loop test",
+                       [&] { set_loop_kernel<<<1, 1, 0, stream>>>(cond, &parts[0].ks->done); });
+            } catch (...) {
+                capturing = false;
+                cudaGraph_t dummy;
+                cudaStreamEndCapture(stream, &dummy);
+                cudaGraphDestroy(g);
+                throw;
+            }
+            capturing = false;
+            cudaGraph_t body_out;
+            ck(cudaStreamEndCapture(stream, &body_out), "end capture");
+            graph_kernels = launches - before;
+            launches = before;
+            ck(cudaGraphInstantiate(&graph, g, 0), "instantiate loop graph");
+            cudaGraphDestroy(g);
+            graph_x = x;
+            graph_prof_mask = 0;
+            graph_loop = true;
+        }
+        const int iter_before = ks_host->iter;
+        ck(cudaGraphLaunch(graph, stream), "graph launch");
+        ck(cudaMemcpyAsync(ks_host, parts[0].ks, sizeof(KState), cudaMemcpyDeviceToHost, stream), "ks read");
+        ck(cudaStreamSynchronize(stream), "sync");
+        // the body ran ceil(iters / 2) times; iteration 0 of a body ran that
+        // often, iteration 1 one time less when the count is odd
+        const int ran = ks_host->iter - iter_before + (ks_host->status ? 1 : 0);
+        const int bodies = (ran + 1) / 2;
+        launches += graph_kernels * bodies;
+        for (int b = 0; b < bodies; ++b) collect(rec_graph, std::min(2, ran - 2 * b), false);
+    }
     while (!ks_host->done) {
         const int iter_before = ks_host->iter;
         if (use_graph) {
-            if (!graph || graph_x != x || graph_prof_mask != prof_mask) {
+            if (!graph || graph_loop || graph_x != x || graph_prof_mask != prof_mask) {
                 drop_graph();
+                graph_loop = false;
                 cudaGraph_t g;
                 const int64_t before = launches;
                 ck(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "capture");
