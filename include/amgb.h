@@ -225,6 +225,10 @@ amg_status amg_dist_info(amg_handle h, int32_t *nranks, int32_t *first_replicate
  *              send entries, recv peers, send peers of (rank, level). */
 amg_status amg_dist_level_info(amg_handle h, int32_t rank, int32_t level, int64_t out[12]);
 amg_status amg_dist_export(amg_handle h, int32_t rank, int32_t level, const amg_dist_level_export *out);
+/* Self-test of the NCCL transport on a 1-rank communicator of `device`: grouped
+ * send/recv to self, all-reduce and broadcast, directly and replayed from a
+ * captured CUDA graph, with the same calls the executor makes.  AMG_OK or an error. */
+amg_status amg_nccl_selftest(int32_t device);
 
 void amg_destroy(amg_handle h);
 const char *amg_last_error(void);

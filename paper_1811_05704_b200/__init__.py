@@ -112,6 +112,7 @@ _lib.amg_solve_stats_get.argtypes = [_V, C.POINTER(SolveStats)]
 _lib.amg_level_op.argtypes = [_V, C.c_int32, C.c_int32, _V, _V, _V]
 _lib.amg_destroy.argtypes = [_V]
 _lib.amg_nccl_unique_id.argtypes = [_V]
+_lib.amg_nccl_selftest.argtypes = [C.c_int32]
 _lib.amg_setup_dist.argtypes = [C.c_int64, _V, _V, _V, C.POINTER(AmgParams), C.POINTER(AmgDist),
                                 C.POINTER(_V)]
 _lib.amg_dist_info.argtypes = [_V, C.POINTER(C.c_int32), C.POINTER(C.c_int32), _V]
@@ -122,7 +123,7 @@ _lib.amg_version.restype = C.c_char_p
 for _name in ("amg_setup", "amg_solve", "amg_solve_host", "amg_precond_apply", "amg_set_stream",
               "amg_set_profile", "amg_level_count", "amg_level_info_get", "amg_export_level",
               "amg_solve_stats_get", "amg_level_op", "amg_nccl_unique_id", "amg_setup_dist",
-              "amg_dist_info", "amg_dist_level_info", "amg_dist_export"):
+              "amg_dist_info", "amg_dist_level_info", "amg_dist_export", "amg_nccl_selftest"):
     getattr(_lib, _name).restype = C.c_int
 
 # Exported C symbols (tests check them against include/amgb.h).
@@ -130,7 +131,7 @@ SYMBOLS = ("amg_params_default", "amg_setup", "amg_solve", "amg_solve_host", "am
            "amg_set_stream", "amg_set_profile", "amg_level_count", "amg_level_info_get",
            "amg_export_level", "amg_solve_stats_get", "amg_level_op", "amg_destroy",
            "amg_last_error", "amg_version", "amg_nccl_unique_id", "amg_setup_dist", "amg_dist_info",
-           "amg_dist_level_info", "amg_dist_export")
+           "amg_dist_level_info", "amg_dist_export", "amg_nccl_selftest")
 
 RELAX = {"spai0": 0, "damped_jacobi": 1, "chebyshev": 2}
 COARSENING = {"smoothed_aggregation": 0, "aggregation": 1}
@@ -397,6 +398,11 @@ def nccl_unique_id() -> bytes:
     buf = (C.c_uint8 * 128)()
     _check(_lib.amg_nccl_unique_id(C.cast(buf, C.c_void_p)), "amg_nccl_unique_id")
     return bytes(buf)
+
+
+def nccl_selftest(device: int = 0) -> None:
+    """amg_nccl_selftest: the NCCL calls of the multi-GPU executor on a 1-rank comm."""
+    _check(_lib.amg_nccl_selftest(device), "amg_nccl_selftest")
 
 
 def setup_dist(ptr, col, val, nranks: int, rank: int = -1, gather_below: int = 1 << 17,

@@ -1645,6 +1645,76 @@ amg_status amg_dist_export(amg_handle h, int32_t rank, int32_t l, const amg_dist
     return AMG_OK;
 }
 
+// Exercise the NCCL transport exactly as the multi-GPU executor calls it (grouped
+// send/recv, all-reduce, broadcast, also replayed from a captured CUDA graph) on a
+// 1-rank communicator of `device` (send/recv to self).  Checks the dlopen'ed
+// entry points and their argument order where only one GPU is available.
+amg_status amg_nccl_selftest(int32_t device) {
+    using namespace amgb;
+    Nccl& nc = Nccl::get();
+    if (!nc.ok) return set_error(AMG_E_CUDA, "NCCL unavailable: " + nc.error);
+    void* comm = nullptr;
+    double* buf = nullptr;
+    cudaStream_t s = nullptr;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    amg_status st = AMG_OK;
+    try {
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        uint8_t id[128];
+        ckn(nc.getUniqueId(id), "ncclGetUniqueId");
+        ckn(nccl_comm_init(&comm, 1, id, 0), "ncclCommInitRank");
+        ck(cudaStreamCreate(&s), "stream");
+        const int n = 1000;
+        ck(cudaMalloc(&buf, 4 * n * sizeof(double)), "cudaMalloc");
+        std::vector<double> h(4 * n);
+        for (int i = 0; i < n; ++i) {
+            h[i] = i + 0.5;  // send buffer
+            h[n + i] = -1;   // recv buffer
+            h[2 * n + i] = 2.0 * i;
+            h[3 * n + i] = 3.0 * i;
+        }
+        auto round = [&] {
+            ckn(nc.groupStart(), "ncclGroupStart");
+            ckn(nc.send(buf, n, kNcclDouble, 0, comm, s), "ncclSend");
+            ckn(nc.recv(buf + n, n, kNcclDouble, 0, comm, s), "ncclRecv");
+            ckn(nc.groupEnd(), "ncclGroupEnd");
+            ckn(nc.allReduce(buf + 2 * n, buf + 2 * n, n, kNcclDouble, kNcclSum, comm, s), "ncclAllReduce");
+            ckn(nc.groupStart(), "ncclGroupStart");
+            ckn(nc.broadcast(buf + 3 * n, buf + 3 * n, n, kNcclDouble, 0, comm, s), "ncclBroadcast");
+            ckn(nc.groupEnd(), "ncclGroupEnd");
+        };
+        for (int pass = 0; pass < 2 && st == AMG_OK; ++pass) {
+            ck(cudaMemcpy(buf, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice), "H2D");
+            if (pass == 0) {
+                round();
+            } else {  // captured into a graph, as the Krylov iterations are
+                ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
+                round();
+                ck(cudaStreamEndCapture(s, &g), "end capture");
+                ck(cudaGraphInstantiate(&ge, g, 0), "instantiate");
+                ck(cudaGraphLaunch(ge, s), "graph launch");
+            }
+            ck(cudaStreamSynchronize(s), "sync");
+            std::vector<double> r(4 * n);
+            ck(cudaMemcpy(r.data(), buf, r.size() * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+            for (int i = 0; i < n; ++i)
+                if (r[n + i] != h[i] || r[2 * n + i] != h[2 * n + i] || r[3 * n + i] != h[3 * n + i]) {
+                    st = set_error(AMG_E_CUDA, "NCCL self-test: wrong data (pass " + std::to_string(pass) + ")");
+                    break;
+                }
+        }
+    } catch (const CudaError& e) {
+        st = set_error(AMG_E_CUDA, e.msg);
+    }
+    if (ge) cudaGraphExecDestroy(ge);
+    if (g) cudaGraphDestroy(g);
+    if (buf) cudaFree(buf);
+    if (s) cudaStreamDestroy(s);
+    if (comm && nc.commDestroy) nc.commDestroy(comm);
+    return st;
+}
+
 amg_status amg_level_op(amg_handle h, int32_t l, int32_t op, const double* x, const double* f, double* y) {
     using namespace amgb;
     if (amg_status st = need_device(h)) return st;

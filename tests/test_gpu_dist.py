@@ -85,3 +85,11 @@ def test_virtual_ranks_zero_rhs_and_host_path():
     single = amgb.setup(p, c, v, coarse_enough=60)
     xs, its, _, _ = single.solve(dev(f), tol=1e-8)
     assert it == its and np.linalg.norm(xh - host(xs)) <= 1e-10 * np.linalg.norm(xh)
+
+
+def test_nccl_transport_selftest():
+    """The NCCL entry points (dlopen) with the executor's argument order, directly
+    and inside a captured CUDA graph, on a 1-rank communicator."""
+    import torch as _t
+    _t.cuda.init()
+    amgb.nccl_selftest(0)
