@@ -150,6 +150,18 @@ amg_status amg_solve(amg_handle h, const double *f, double *x, double tol, int32
 amg_status amg_solve_host(amg_handle h, const double *f, const double *x0, double *x, double tol,
                           int32_t maxiter, int32_t *iters, double *rel_resid);
 
+/* Batched solve of A X = F for k right-hand sides (1 <= k <= 8) with one pass over
+ * the hierarchy per iteration serving every column (the hierarchy is reused for
+ * many right-hand sides).  F, X: DEVICE,
+ * column-major, column j at F + j*ldf / X + j*ldx (ld >= n); X holds the initial
+ * guesses on entry and the solutions on return.  Every column runs its own CG
+ * (own scalars, convergence test and iteration count, identical in exact
+ * arithmetic to k separate amg_solve calls).  iters[k], rel_resid[k] (true
+ * residuals) are outputs; the status is the worst over the columns.  CG on
+ * single-GPU handles only.  Synchronous. */
+amg_status amg_solve_batched(amg_handle h, int32_t k, const double *F, int64_t ldf, double *X, int64_t ldx,
+                             double tol, int32_t maxiter, int32_t *iters, double *rel_resid);
+
 /* z = M r: one V-cycle from a zero initial guess.  r, z:
  * DEVICE pointers (length n, distinct).  Asynchronous on the handle stream. */
 amg_status amg_precond_apply(amg_handle h, const double *r, double *z);

@@ -112,6 +112,7 @@ _lib.amg_solve_stats_get.argtypes = [_V, C.POINTER(SolveStats)]
 _lib.amg_level_op.argtypes = [_V, C.c_int32, C.c_int32, _V, _V, _V]
 _lib.amg_destroy.argtypes = [_V]
 _lib.amg_nccl_unique_id.argtypes = [_V]
+_lib.amg_solve_batched.argtypes = [_V, C.c_int32, _V, C.c_int64, _V, C.c_int64, C.c_double, C.c_int32, _V, _V]
 _lib.amg_nccl_selftest.argtypes = [C.c_int32]
 _lib.amg_setup_dist.argtypes = [C.c_int64, _V, _V, _V, C.POINTER(AmgParams), C.POINTER(AmgDist),
                                 C.POINTER(_V)]
@@ -123,7 +124,8 @@ _lib.amg_version.restype = C.c_char_p
 for _name in ("amg_setup", "amg_solve", "amg_solve_host", "amg_precond_apply", "amg_set_stream",
               "amg_set_profile", "amg_level_count", "amg_level_info_get", "amg_export_level",
               "amg_solve_stats_get", "amg_level_op", "amg_nccl_unique_id", "amg_setup_dist",
-              "amg_dist_info", "amg_dist_level_info", "amg_dist_export", "amg_nccl_selftest"):
+              "amg_dist_info", "amg_dist_level_info", "amg_dist_export", "amg_nccl_selftest",
+              "amg_solve_batched"):
     getattr(_lib, _name).restype = C.c_int
 
 # Exported C symbols (tests check them against include/amgb.h).
@@ -131,7 +133,7 @@ SYMBOLS = ("amg_params_default", "amg_setup", "amg_solve", "amg_solve_host", "am
            "amg_set_stream", "amg_set_profile", "amg_level_count", "amg_level_info_get",
            "amg_export_level", "amg_solve_stats_get", "amg_level_op", "amg_destroy",
            "amg_last_error", "amg_version", "amg_nccl_unique_id", "amg_setup_dist", "amg_dist_info",
-           "amg_dist_level_info", "amg_dist_export", "amg_nccl_selftest")
+           "amg_dist_level_info", "amg_dist_export", "amg_nccl_selftest", "amg_solve_batched")
 
 RELAX = {"spai0": 0, "damped_jacobi": 1, "chebyshev": 2}
 COARSENING = {"smoothed_aggregation": 0, "aggregation": 1}
@@ -341,6 +343,22 @@ class Hierarchy:
         st = _check(_lib.amg_solve(self._h, _ptr(f), _ptr(x), tol, maxiter, C.byref(it), C.byref(rel)),
                     "amg_solve")
         return x, it.value, rel.value, st
+
+    def solve_batched(self, F, X=None, tol=1e-8, maxiter=100):
+        """Solve A x_j = f_j for the k rows of the CUDA float64 tensor F (shape
+        (k, n), each right-hand side contiguous).  Returns (X, iters[k],
+        rel_resid[k], status)."""
+        import torch
+        F = F.contiguous()
+        k, n = F.shape
+        if X is None:
+            X = torch.zeros_like(F)
+        self._sync_stream()
+        it = np.zeros(k, np.int32)
+        rel = np.zeros(k)
+        st = _check(_lib.amg_solve_batched(self._h, k, _ptr(F), n, _ptr(X), n, tol, maxiter, it.ctypes.data,
+                                           rel.ctypes.data), "amg_solve_batched")
+        return X, it, rel, st
 
     def solve_host(self, f: np.ndarray, x0: np.ndarray | None = None, tol=1e-8, maxiter=100,
                    out: np.ndarray | None = None):

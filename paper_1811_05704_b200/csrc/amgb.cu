@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "../../include/amgb.h"
+#include "batched.cuh"
 #include "comm.hpp"
 #include "dist.hpp"
 #include "kernels.cuh"
@@ -237,6 +238,7 @@ struct Handle {
 
     bool distributed() const { return nranks > 1; }
 
+
     double* dalloc(int64_t n) {
         void* p = nullptr;
         ck(cudaMalloc(&p, std::max<int64_t>(n, 1) * sizeof(double)), "cudaMalloc");
@@ -253,6 +255,7 @@ struct Handle {
         return static_cast<T*>(p);
     }
     ~Handle() {
+        free_batch();
         if (graph) cudaGraphExecDestroy(graph);
         for (cudaEvent_t e : ev_all) cudaEventDestroy(e);
         for (void* p : allocs) cudaFree(p);
@@ -287,6 +290,28 @@ struct Handle {
     std::vector<cudaEvent_t> ev_pool, ev_all;
     double acc_ms[8] = {}, acc_bytes[8] = {}, alg_bytes = 0;
     int64_t acc_launches[8] = {};
+
+    // ---- batched right-hand sides (single part): interleaved K-column buffers
+    struct BLevel {
+        double *f = nullptr, *x = nullptr, *y = nullptr, *t = nullptr, *p = nullptr, *o = nullptr;
+    };
+    struct Batch {
+        int K = 0;
+        std::vector<BLevel> lv;
+        double *r = nullptr, *z = nullptr, *pa = nullptr, *pb = nullptr, *q = nullptr, *xw = nullptr, *fw = nullptr;
+        KStateB* ks = nullptr;
+        KStateB* ks_host = nullptr;
+        std::vector<void*> mem;
+        cudaGraphExec_t graph = nullptr;
+        std::vector<Rec> rec;
+        int64_t graph_kernels = 0;
+    } batch;
+    void free_batch() {
+        if (batch.graph) cudaGraphExecDestroy(batch.graph);
+        for (void* p : batch.mem) cudaFree(p);
+        if (batch.ks_host) cudaFreeHost(batch.ks_host);
+        batch = Batch{};
+    }
 
     cudaEvent_t get_event() {
         if (ev_pool.empty()) {
@@ -425,13 +450,8 @@ struct Handle {
         const double bytes = 12.0 * M.nnz + 4.0 * M.nrows + 8.0 * M.ncols * Op::GATHER + 8.0 * M.nrows * Op::ROWV;
         const Red& red = p.red;
         launch(mat_class(p, M), bytes, what, [&] {
-            if (M.fmt == Fmt::TMA) {
-                switch (M.tma.T) {
-                    case 1: rows_tma<1>(M.tma, op, gate, red, big); break;
-                    case 2: rows_tma<2>(M.tma, op, gate, red, big); break;
-                    case 4: rows_tma<4>(M.tma, op, gate, red, big); break;
-                    default: rows_tma<8>(M.tma, op, gate, red, big); break;
-                }
+            if (M.fmt == Fmt::TMA) {  // T = 1 lane per row (narrow rows only, pick_format)
+                rows_tma<1>(M.tma, op, gate, red, big);
             } else if (M.fmt == Fmt::CSR) {
                 switch (M.csr.G) {
                     case 1: rows_csr<1>(M.csr, op, gate, red, big); break;
@@ -557,6 +577,15 @@ struct Handle {
     }
 
     bool vcycle(int l, const CSel& f, const Sel& out, const GSel& gate, bool with_rho);
+    template <int K>
+    void ensure_batch();
+    template <int K>
+    bool vcycle_b(int l, const double* f, double* out, const int32_t* gate, bool with_rho);
+    template <int K>
+    void cg_iteration_b(int parity);
+    template <int K>
+    amg_status solve_batched(int k, const double* F, int64_t ldf, double* X, int64_t ldx, double tol, int32_t maxiter,
+                             int32_t* iters, double* rel);
     void cg_iteration(int parity);
     void bicgstab_iteration();
     amg_status solve(const double* f, double* x, double tol, int32_t maxiter, int32_t* iters, double* rel);
@@ -987,6 +1016,289 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
     return st;
 }
 
+// ============================================================ batched solve
+// K interleaved right-hand sides through one hierarchy pass (batched.cuh).
+template <int K>
+void Handle::ensure_batch() {
+    if (batch.K == K) return;
+    free_batch();
+    batch.K = K;
+    Part& p = parts[0];
+    auto alloc = [&](int64_t n) {
+        void* q = nullptr;
+        ck(cudaMalloc(&q, std::max<int64_t>(n, 1) * K * sizeof(double)), "cudaMalloc (batch)");
+        ck(cudaMemset(q, 0, std::max<int64_t>(n, 1) * K * sizeof(double)), "memset");
+        batch.mem.push_back(q);
+        return static_cast<double*>(q);
+    };
+    batch.lv.resize(p.lv.size());
+    for (size_t l = 0; l < p.lv.size(); ++l) {
+        const int64_t n = p.lv[l].n;
+        BLevel& B = batch.lv[l];
+        B.x = alloc(n);
+        B.y = alloc(n);
+        B.t = alloc(n);
+        if (prm.relax == 2) B.p = alloc(n);
+        if (l > 0) {
+            B.f = alloc(n);
+            B.o = alloc(n);
+        }
+    }
+    const int64_t n0 = p.lv[0].n;
+    batch.r = alloc(n0);
+    batch.z = alloc(n0);
+    batch.pa = alloc(n0);
+    batch.pb = alloc(n0);
+    batch.q = alloc(n0);
+    batch.xw = alloc(n0);
+    batch.fw = alloc(n0);
+    void* q = nullptr;
+    ck(cudaMalloc(&q, sizeof(KStateB)), "cudaMalloc");
+    batch.mem.push_back(q);
+    batch.ks = static_cast<KStateB*>(q);
+    ck(cudaMallocHost(&batch.ks_host, sizeof(KStateB)), "cudaMallocHost");
+}
+
+// Algorithm 2 for K interleaved right-hand sides (single part).
+template <int K>
+bool Handle::vcycle_b(int l, const double* f, double* out, const int32_t* gate, bool with_rho) {
+    Part& p = parts[0];
+    const int nlev = (int)p.lv.size();
+    DevLevel& L = p.lv[l];
+    if (l == nlev - 1) {
+        const int64_t warps = std::min<int64_t>(L.n, (int64_t)num_sms * 64);
+        const int g = (int)std::max<int64_t>(1, (warps * 32 + kBlock - 1) / kBlock);
+        launch(AMG_PROF_COARSE_SOLVE, 8.0 * L.n * L.n + 16.0 * K * L.n, "coarse gemm",
+               [&] { dense_gemm_b<K><<<g, kBlock, 0, stream>>>(L.n, p.coarse_inv, f, out, gate); });
+        return false;
+    }
+    BLevel& B = batch.lv[l];
+    BLevel& Bc = batch.lv[l + 1];
+    DevLevel& C = p.lv[l + 1];
+    const bool cheb = prm.relax == 2;
+    const int K_ = prm.cheb_degree;
+    double* x = B.x;
+    double* y = B.y;
+    bool x_is_mf = false;
+    if (!cheb) {
+        if (prm.npre == 1) {
+            x_is_mf = true;
+            rows(p, L.A, OpRes0B<K>{L.m, f, B.t, {}}, gate, "res0 (batched)");
+        } else {
+            if (prm.npre == 0)
+                ck(cudaMemsetAsync(x, 0, L.n * K * sizeof(double), stream), "memset");
+            else
+                vec(p, L.n, VMulDiagB<K>{L.m, f, x, {}}, gate, "x=mf (batched)");
+            for (int s = 1; s < prm.npre; ++s) {
+                rows(p, L.A, OpRelaxB<K, 0, NoFin>{x, L.m, f, y, {}}, gate, "relax (batched)");
+                std::swap(x, y);
+            }
+            rows(p, L.A, OpResidualB<K, 0, NoFin>{x, f, B.t, {}}, gate, "residual (batched)");
+        }
+    } else {
+        for (int s = 0; s < prm.npre; ++s)
+            for (int k = 0; k < K_; ++k) {
+                if (s == 0 && k == 0) {
+                    vec(p, L.n, VCheb0B<K>{f, L.diag, B.p, x, L.cheb_alpha[0], prm.cheb_scaled, {}}, gate,
+                        "cheb0 (batched)");
+                } else {
+                    rows(p, L.A,
+                         OpChebB<K, 0, NoFin>{x, f, L.diag, B.p, y, L.cheb_alpha[k], L.cheb_beta[k], prm.cheb_scaled,
+                                              k == 0, {}},
+                         gate, "cheb (batched)");
+                    std::swap(x, y);
+                }
+            }
+        if (prm.npre == 0) ck(cudaMemsetAsync(x, 0, L.n * K * sizeof(double), stream), "memset");
+        rows(p, L.A, OpResidualB<K, 0, NoFin>{x, f, B.t, {}}, gate, "residual (batched)");
+    }
+    rows(p, L.R, OpSpmvB<K>{B.t, Bc.f}, gate, "restrict (batched)");
+    vcycle_b<K>(l + 1, Bc.f, Bc.o, gate, false);
+    if (x_is_mf)
+        rows(p, L.P, OpProl0B<K>{Bc.o, L.m, f, x, {}}, gate, "prolong0 (batched)");
+    else
+        rows(p, L.P, OpProlAddB<K>{Bc.o, x, {}}, gate, "prolong (batched)");
+    (void)C;
+    if (prm.npost == 0) {
+        ck(cudaMemcpyAsync(out, x, L.n * K * sizeof(double), cudaMemcpyDeviceToDevice, stream), "copy");
+        return false;
+    }
+    const int sweeps = cheb ? prm.npost * K_ : prm.npost;
+    for (int s = 0; s < sweeps; ++s) {
+        const bool last = s == sweeps - 1;
+        double* dst = last ? out : y;
+        if (!cheb) {
+            if (last && with_rho)
+                rows(p, L.A, OpRelaxB<K, 1, FinRhoB<K>>{x, L.m, f, dst, FinRhoB<K>{batch.ks}}, gate, "relax+dot (batched)");
+            else
+                rows(p, L.A, OpRelaxB<K, 0, NoFin>{x, L.m, f, dst, {}}, gate, "relax (batched)");
+        } else {
+            const int k = s % K_;
+            if (last && with_rho)
+                rows(p, L.A,
+                     OpChebB<K, 1, FinRhoB<K>>{x, f, L.diag, B.p, dst, L.cheb_alpha[k], L.cheb_beta[k], prm.cheb_scaled,
+                                               k == 0, FinRhoB<K>{batch.ks}},
+                     gate, "cheb+dot (batched)");
+            else
+                rows(p, L.A,
+                     OpChebB<K, 0, NoFin>{x, f, L.diag, B.p, dst, L.cheb_alpha[k], L.cheb_beta[k], prm.cheb_scaled,
+                                          k == 0, {}},
+                     gate, "cheb (batched)");
+        }
+        if (!last) std::swap(x, y);
+    }
+    return with_rho;
+}
+
+template <int K>
+void Handle::cg_iteration_b(int parity) {
+    Part& p = parts[0];
+    const int32_t* gate = &batch.ks->done;
+    double* pold = parity ? batch.pb : batch.pa;
+    double* pnew = parity ? batch.pa : batch.pb;
+    if (!vcycle_b<K>(0, batch.r, batch.z, gate, true))
+        vec(p, p.lv[0].n, VDotB<K, FinRhoB<K>>{batch.r, batch.z, FinRhoB<K>{batch.ks}}, gate, "dot(r,z) (batched)");
+    rows(p, p.lv[0].A,
+         OpCgDirB<K, FinSigmaB<K>>{batch.z, pold, pnew, batch.q, batch.ks, {}, FinSigmaB<K>{batch.ks}}, gate,
+         "cg dir (batched)");
+    vec(p, p.lv[0].n, VCgUpdateB<K>{batch.xw, batch.r, pnew, batch.q, batch.ks, {}, FinCgUpdateB<K>{batch.ks}}, gate,
+        "cg update (batched)");
+}
+
+template <int K>
+amg_status Handle::solve_batched(int k, const double* F, int64_t ldf, double* X, int64_t ldx, double tol,
+                                 int32_t maxiter, int32_t* iters, double* rel) {
+    ensure_batch<K>();
+    Part& p = parts[0];
+    const int64_t n = p.lv[0].n;
+    const int64_t launches0 = launches;
+    collect(rec_direct, 0, true);
+    alg_bytes = 0;
+    std::fill(acc_ms, acc_ms + 8, 0.0);
+    std::fill(acc_bytes, acc_bytes + 8, 0.0);
+    std::fill(acc_launches, acc_launches + 8, 0);
+    cur_iter = -1;
+    ck(cudaEventRecord(ev0, stream), "event");
+    KStateB* kh = batch.ks_host;
+    std::memset(kh, 0, sizeof(KStateB));
+    kh->k = k;
+    kh->maxiter = maxiter;
+    ck(cudaMemcpyAsync(batch.ks, kh, sizeof(KStateB), cudaMemcpyHostToDevice, stream), "ks init");
+    launch(AMG_PROF_VECTOR, 8.0 * 2 * K * n, "pack F, X", [&] {
+        pack_cols<K><<<grid_for(n), kBlock, 0, stream>>>(F, ldf, k, n, batch.fw, nullptr);
+        pack_cols<K><<<grid_for(n), kBlock, 0, stream>>>(X, ldx, k, n, batch.xw, nullptr);
+    });
+    vec(p, n, VNorm2B<K, FinNormB<K>>{batch.fw, FinNormB<K>{batch.ks, tol}}, nullptr, "norm F");
+    rows(p, p.lv[0].A, OpResidualB<K, 1, FinInitResB<K>>{batch.xw, batch.fw, batch.r, FinInitResB<K>{batch.ks}},
+         nullptr, "r0 (batched)");
+    ck(cudaMemsetAsync(batch.pa, 0, n * K * sizeof(double), stream), "memset");
+    ck(cudaMemsetAsync(batch.pb, 0, n * K * sizeof(double), stream), "memset");
+    ck(cudaMemcpyAsync(kh, batch.ks, sizeof(KStateB), cudaMemcpyDeviceToHost, stream), "ks read");
+    ck(cudaStreamSynchronize(stream), "sync");
+    collect(rec_direct, 0, true);
+    // FinInitResB does not know which columns have f = 0: mark them done
+    // (x = 0 for them) before iterating
+    bool any_zero = false;
+    for (int j = 0; j < k; ++j)
+        if (kh->nf[j] == 0.0 && !kh->cdone[j]) any_zero = true;
+    if (any_zero) {
+        int all = 1;
+        for (int j = 0; j < K; ++j) {
+            if (j < k && kh->nf[j] == 0.0) kh->cdone[j] = 1;
+            all &= kh->cdone[j];
+        }
+        kh->done = all;
+        ck(cudaMemcpyAsync(batch.ks, kh, sizeof(KStateB), cudaMemcpyHostToDevice, stream), "ks update");
+    }
+    if (!kh->done) {
+        if (!batch.graph) {  // conditional WHILE node around two iterations (device-side loop)
+            cudaGraph_t g;
+            ck(cudaGraphCreate(&g, 0), "graph create");
+            cudaGraphConditionalHandle cond;
+            ck(cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault), "cond handle");
+            cudaGraphNodeParams cp = {};
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = cond;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            cudaGraphNode_t node;
+            ck(cudaGraphAddNode(&node, g, nullptr, 0, &cp), "conditional node");
+            const int64_t before = launches;
+            const int saved_mask = prof_mask;
+            prof_mask = 0;  // no event nodes inside conditional bodies
+            ck(cudaStreamBeginCaptureToGraph(stream, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                             cudaStreamCaptureModeThreadLocal),
+               "capture body");
+            capturing = true;
+            std::vector<Rec> saved;
+            saved.swap(rec_graph);
+            try {
+                for (int it = 0; it < 2; ++it) {
+                    cur_iter = it;
+                    cg_iteration_b<K>(it);
+                }
+                cur_iter = -1;
+                launch(AMG_PROF_VECTOR, 0, "loop test",
+                       [&] { set_loop_kernel<<<1, 1, 0, stream>>>(cond, &batch.ks->done); });
+            } catch (...) {
+                capturing = false;
+                prof_mask = saved_mask;
+                cudaGraph_t dummy;
+                cudaStreamEndCapture(stream, &dummy);
+                cudaGraphDestroy(g);
+                rec_graph.swap(saved);
+                throw;
+            }
+            capturing = false;
+            prof_mask = saved_mask;
+            batch.rec.swap(rec_graph);
+            rec_graph.swap(saved);
+            cudaGraph_t body_out;
+            ck(cudaStreamEndCapture(stream, &body_out), "end capture");
+            batch.graph_kernels = launches - before;
+            launches = before;
+            ck(cudaGraphInstantiate(&batch.graph, g, 0), "instantiate");
+            cudaGraphDestroy(g);
+        }
+        ck(cudaGraphLaunch(batch.graph, stream), "graph launch");
+    }
+    rows(p, p.lv[0].A, OpResidualB<K, 1, FinTrueResB<K>>{batch.xw, batch.fw, batch.r, FinTrueResB<K>{batch.ks}},
+         nullptr, "true res (batched)");
+    launch(AMG_PROF_VECTOR, 8.0 * K * n, "unpack X",
+           [&] { unpack_cols<K><<<grid_for(n), kBlock, 0, stream>>>(batch.xw, k, n, X, ldx, batch.ks); });
+    ck(cudaEventRecord(ev1, stream), "event");
+    ck(cudaMemcpyAsync(kh, batch.ks, sizeof(KStateB), cudaMemcpyDeviceToHost, stream), "ks read");
+    ck(cudaStreamSynchronize(stream), "sync");
+    int itmax = 0;
+    for (int j = 0; j < K; ++j) itmax = std::max(itmax, kh->iter[j]);
+    const int bodies = (itmax + 1) / 2;
+    launches += batch.graph_kernels * bodies;
+    for (int b = 0; b < bodies; ++b) collect(batch.rec, std::min(2, itmax - 2 * b), false);
+    collect(rec_direct, 0, true);
+    amg_status st = AMG_OK;
+    for (int j = 0; j < k; ++j) {
+        iters[j] = kh->iter[j];
+        rel[j] = kh->nf[j] == 0.0 ? 0.0 : kh->true_res[j] / kh->nf[j];
+        if (kh->status[j] == AMG_BREAKDOWN)
+            st = AMG_BREAKDOWN;
+        else if (st == AMG_OK && kh->nf[j] != 0.0 && !(kh->res[j] <= kh->tolnf[j]))
+            st = AMG_NOT_CONVERGED;
+    }
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev0, ev1);
+    stats = amg_solve_stats{};
+    stats.iters = itmax;
+    stats.vcycles = itmax;
+    stats.status = st;
+    stats.kernel_launches = launches - launches0;
+    stats.solve_ms = ms;
+    stats.rel_resid = 0;
+    for (int j = 0; j < k; ++j) stats.rel_resid = std::max(stats.rel_resid, rel[j]);
+    stats.alg_bytes = alg_bytes;
+    if (st == AMG_BREAKDOWN) g_err = "CG breakdown in a batched column";
+    return st;
+}
+
 // z = M r for every part (r, z: device; global vectors in virtual mode).
 void Handle::precond(const double* r, double* z) {
     GSel nogate = [](Part&) { return (const int32_t*)nullptr; };
@@ -1089,9 +1401,10 @@ DMat upload_mat(Handle& H, const Csr& A, int64_t* bytes) {
     } else {  // TMA-staged SELL-C: lanes per row T from the longest row, C = 32 / T
         int64_t lmax = 0;
         for (int64_t r = 0; r < A.nrows; ++r) lmax = std::max<int64_t>(lmax, A.ptr[r + 1] - A.ptr[r]);
-        const char* te_env = std::getenv("AMGB_TMA_T");
-        int T = lmax <= 12 ? 1 : lmax <= 24 ? 2 : lmax <= 48 ? 4 : 8;
-        if (te_env) T = std::atoi(te_env);
+        // the kernel supports T lanes per row (SELL-C, C = 32/T); the format policy
+        // only sends narrow rows here, which use one lane per row
+        (void)lmax;
+        const int T = 1;
         const int C = 32 / T;
         HostSell S = to_sell(A, C);
         SellTma& t = d.tma;
@@ -1226,7 +1539,7 @@ void upload_part(Handle& H, const RankPart& RP, Part& P) {
     ck(cudaMalloc(&pp, sizeof(KState)), "cudaMalloc");
     H.allocs.push_back(pp);
     P.ks = static_cast<KState*>(pp);
-    ck(cudaMalloc(&pp, (size_t)H.num_sms * 8 * 4 * sizeof(double)), "cudaMalloc");
+    ck(cudaMalloc(&pp, (size_t)H.num_sms * 8 * kMaxK * sizeof(double)), "cudaMalloc");
     H.allocs.push_back(pp);
     P.red.partial = static_cast<double*>(pp);
     ck(cudaMalloc(&pp, 64), "cudaMalloc");
@@ -1486,6 +1799,27 @@ amg_status amg_solve_host(amg_handle h, const double* f, const double* x0, doubl
         ck(cudaMemcpyAsync(x, H.hx, n * sizeof(double), cudaMemcpyDeviceToHost, H.stream), "D2H x");
         ck(cudaStreamSynchronize(H.stream), "sync");
         return st;
+    } catch (const amgb::CudaError& e) {
+        cudaGetLastError();
+        return set_error(AMG_E_CUDA, e.msg);
+    }
+}
+
+amg_status amg_solve_batched(amg_handle h, int32_t k, const double* F, int64_t ldf, double* X, int64_t ldx,
+                             double tol, int32_t maxiter, int32_t* iters, double* rel) {
+    if (amg_status st = need_device(h)) return st;
+    Handle& H = *h->h;
+    if (H.distributed()) return set_error(AMG_E_INVALID_ARG, "amg_solve_batched: single-GPU handles only");
+    if (H.prm.solver != 0) return set_error(AMG_E_INVALID_ARG, "amg_solve_batched: CG only");
+    const int64_t n = H.parts[0].lv[0].n;
+    if (k < 1 || k > amgb::kMaxK || !F || !X || !iters || !rel || ldf < n || ldx < n)
+        return set_error(AMG_E_INVALID_ARG, "k in [1, 8], F/X/iters/rel non-NULL, ld >= n");
+    if (!(tol >= 0) || maxiter < 0) return set_error(AMG_E_INVALID_ARG, "tol >= 0, maxiter >= 0");
+    try {
+        ck(cudaSetDevice(H.device), "cudaSetDevice");
+        if (k <= 2) return H.solve_batched<2>(k, F, ldf, X, ldx, tol, maxiter, iters, rel);
+        if (k <= 4) return H.solve_batched<4>(k, F, ldf, X, ldx, tol, maxiter, iters, rel);
+        return H.solve_batched<8>(k, F, ldf, X, ldx, tol, maxiter, iters, rel);
     } catch (const amgb::CudaError& e) {
         cudaGetLastError();
         return set_error(AMG_E_CUDA, e.msg);

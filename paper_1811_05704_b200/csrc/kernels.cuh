@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
+#include <utility>
 
 namespace amgb {
 
@@ -53,6 +55,36 @@ __device__ __forceinline__ double ld_mat(const double* p) {
 template <bool STREAM>
 __device__ __forceinline__ int32_t ld_mat(const int32_t* p) {
     if constexpr (STREAM) return __ldcs(p); else return __ldg(p);
+}
+
+// Accumulator of a row kernel: one double (single right-hand side) or Vk<K> (K
+// interleaved right-hand sides of a batched solve, x[c*K + j]).  Ops return
+// their accumulator type from gather(); the kernels are written once for both.
+template <int K>
+struct Vk {
+    double v[K];
+};
+template <class Op>
+using acc_t = decltype(std::declval<Op>().gather(0));
+__device__ __forceinline__ void fma_acc(double& s, double a, double x) { s = fma(a, x, s); }
+template <int K>
+__device__ __forceinline__ void fma_acc(Vk<K>& s, double a, const Vk<K>& x) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) s.v[j] = fma(a, x.v[j], s.v[j]);
+}
+__device__ __forceinline__ double shfl_xor_acc(unsigned m, double s, int o) { return __shfl_xor_sync(m, s, o); }
+template <int K>
+__device__ __forceinline__ Vk<K> shfl_xor_acc(unsigned m, const Vk<K>& s, int o) {
+    Vk<K> r;
+#pragma unroll
+    for (int j = 0; j < K; ++j) r.v[j] = __shfl_xor_sync(m, s.v[j], o);
+    return r;
+}
+__device__ __forceinline__ void add_acc(double& s, double x) { s += x; }
+template <int K>
+__device__ __forceinline__ void add_acc(Vk<K>& s, const Vk<K>& x) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) s.v[j] += x.v[j];
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -164,7 +196,7 @@ __global__ void __launch_bounds__(kBlock, PIPE ? 4 : 6) sell_rows(Sell A, Op op,
         const int w = (int)((A.sptr[s + 1] - beg) >> 5);
         const int32_t* cp = A.col + beg + lane;
         const double* vp = A.val + beg + lane;
-        double sum = 0.0;
+        acc_t<Op> sum{};
         int32_t c[U];
         double v[U];
 #pragma unroll
@@ -173,17 +205,17 @@ __global__ void __launch_bounds__(kBlock, PIPE ? 4 : 6) sell_rows(Sell A, Op op,
             v[u] = u < w ? ld_mat<STREAM>(vp + 32 * u) : 0.0;
         }
         if constexpr (!PIPE) {
-            double xv[U];
+            acc_t<Op> xv[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) xv[u] = u < w ? op.gather(c[u]) : 0.0;
+            for (int u = 0; u < U; ++u) xv[u] = u < w ? op.gather(c[u]) : acc_t<Op>{};
 #pragma unroll
             for (int u = 0; u < U; ++u)
-                if (u < w) sum = fma(v[u], xv[u], sum);
+                if (u < w) fma_acc(sum, v[u], xv[u]);
         }
         for (int k0 = 0; PIPE && k0 < w; k0 += U) {
-            double xv[U];
+            acc_t<Op> xv[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) xv[u] = (k0 + u < w) ? op.gather(c[u]) : 0.0;
+            for (int u = 0; u < U; ++u) xv[u] = (k0 + u < w) ? op.gather(c[u]) : acc_t<Op>{};
             // software pipelining: the next chunk's entries are in flight while
             // this chunk's gathers complete
             int32_t cn[U];
@@ -196,7 +228,7 @@ __global__ void __launch_bounds__(kBlock, PIPE ? 4 : 6) sell_rows(Sell A, Op op,
             }
 #pragma unroll
             for (int u = 0; u < U; ++u)
-                if (k0 + u < w) sum = fma(v[u], xv[u], sum);
+                if (k0 + u < w) fma_acc(sum, v[u], xv[u]);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 c[u] = cn[u];
@@ -337,9 +369,9 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaBlocksPerSM) sell_tma(SellTma
             const double* sv = reinterpret_cast<const double*>(smem + (size_t)s * stage_bytes) + off + r;
             const int32_t* sc =
                 reinterpret_cast<const int32_t*>(smem + (size_t)s * stage_bytes + (size_t)te * 8) + off + r;
-            double sum = 0.0;
+            acc_t<Op> sum{};
             for (int k0 = pt; k0 < w; k0 += 8 * T) {
-                double xv[8];
+                acc_t<Op> xv[8];
                 int32_t c[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
@@ -347,18 +379,18 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaBlocksPerSM) sell_tma(SellTma
                     c[u] = k < w ? sc[C * k] : 0;
                 }
 #pragma unroll
-                for (int u = 0; u < 8; ++u) xv[u] = (k0 + u * T < w) ? op.gather(c[u]) : 0.0;
+                for (int u = 0; u < 8; ++u) xv[u] = (k0 + u * T < w) ? op.gather(c[u]) : acc_t<Op>{};
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     const int k = k0 + u * T;
-                    if (k < w) sum = fma(sv[C * k], xv[u], sum);
+                    if (k < w) fma_acc(sum, sv[C * k], xv[u]);
                 }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(bars + kTmaStages + s));  // stage free
             if constexpr (T > 1) {
 #pragma unroll
-                for (int o = C; o < 32; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+                for (int o = C; o < 32; o <<= 1) add_acc(sum, shfl_xor_acc(0xffffffffu, sum, o));
             }
             if (pt == 0 && has_row) op.row(row, sum, rr, dots);
         }
@@ -401,6 +433,24 @@ __global__ void __launch_bounds__(kBlock) csr_rows(CsrDev A, Op op, const int32_
     const int tid = threadIdx.x;
     const int lig = tid & (G - 1);
     const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << ((tid & 31) & ~(G - 1)));
+    if constexpr (!std::is_same_v<acc_t<Op>, double>) {
+        // batched right-hand sides: G threads per row straight from global
+        // memory (the shared-memory product tile would be K times larger)
+        const int64_t groups = ((int64_t)gridDim.x * blockDim.x) / G;
+        for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + tid) / G; r < A.nrows; r += groups) {
+            const typename Op::Row rr = op.load(r);
+            acc_t<Op> s{};
+            for (int k = A.ptr[r] + lig; k < A.ptr[r + 1]; k += G)
+                fma_acc(s, ld_mat<STREAM>(A.val + k), op.gather(ld_mat<STREAM>(A.col + k)));
+            if constexpr (G > 1) {
+#pragma unroll
+                for (int o = G / 2; o > 0; o >>= 1) add_acc(s, shfl_xor_acc(gmask, s, o));
+            }
+            if (lig == 0) op.row(r, s, rr, dots);
+        }
+        if constexpr (Op::NDOT > 0) grid_reduce<Op::NDOT>(dots, red, op.fin);
+        return;
+    } else {
     for (int64_t b = blockIdx.x; b < A.nblocks; b += gridDim.x) {
         const int rb = A.brow[b], re = A.brow[b + 1];
         const int eb = A.ptr[rb], ne = A.ptr[re] - eb;
@@ -449,6 +499,7 @@ __global__ void __launch_bounds__(kBlock) csr_rows(CsrDev A, Op op, const int32_
             __syncthreads();
         }
     }
+    }  // single right-hand side
     if constexpr (Op::NDOT > 0) grid_reduce<Op::NDOT>(dots, red, op.fin);
 }
 

@@ -205,3 +205,41 @@ def test_configs1_150_permuted_full_size():
     if iters != o["iters"]:
         x, iters, rel, st = h.solve(dev(f), tol=0.0, maxiter=o["iters"])
     assert np.linalg.norm(host(x) - o["x"]) <= 1e-8 * np.linalg.norm(o["x"])
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 31, 33])
+def test_tiny_systems(n):
+    """Degenerate sizes: 1x1 .. a few rows (single level: the dense coarse solve
+    is the whole preconditioner, so CG converges in one iteration)."""
+    p, c, v, f = synth.poisson3d(n, 1, 1)
+    h = amgb.setup(p, c, v)
+    x, iters, rel, st = h.solve(dev(f), tol=1e-12)
+    ref = np.linalg.solve(oracle.Csr(p, c, v).to_dense(), f)
+    assert st == amgb.OK and iters == 1
+    assert np.linalg.norm(host(x) - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+def test_maxiter_one_and_two_levels_ragged():
+    """maxiter = 1 and 2 (odd/even iterations of the two-iteration graph body),
+    on a ragged two-level hierarchy, against the oracle."""
+    p, c, v, f = synth.problem("poisson_perm", 13)  # 2197 rows
+    for maxiter in (1, 2, 3):
+        h = amgb.setup(p, c, v, coarse_enough=200)
+        o = oracle_solve(p, c, v, f, {"coarse_enough": 200}, 0.0, maxiter)
+        x, iters, rel, st = h.solve(dev(f), tol=0.0, maxiter=maxiter)
+        assert iters == maxiter == o["iters"] and st == amgb.NOT_CONVERGED
+        assert np.linalg.norm(host(x) - o["x"]) <= 1e-12 * np.linalg.norm(o["x"])
+        s = h.stats()
+        assert s["iters"] == maxiter and s["vcycles"] == maxiter and s["alg_bytes"] > 0
+
+
+def test_device_loop_and_host_loop_agree():
+    """The conditional-WHILE device loop and the host loop give identical results."""
+    import os
+    p, c, v, f = synth.problem("varcoef", 20)
+    h = amgb.setup(p, c, v, relax="chebyshev", coarse_enough=100)
+    x1, it1, rel1, _ = h.solve(dev(f), tol=1e-9)
+    h.set_profile(1)  # profile mode uses the host loop
+    x2, it2, rel2, _ = h.solve(dev(f), tol=1e-9)
+    h.set_profile(0)
+    assert it1 == it2 and np.array_equal(host(x1), host(x2))
