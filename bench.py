@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--batch", type=int, default=1,
+                    help="k > 1: k right-hand sides per solve (amg_solve_batched); value counts column V-cycles")
     ap.add_argument("--json-out", default=None)
     return ap.parse_args()
 
@@ -201,6 +203,50 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def run_batched(args, cfg, h, f, n, nnz, infos, setup_s, local, stream):
+    """k right-hand sides per solve through amg_solve_batched (1 GPU)."""
+    import torch
+    k = args.batch
+    rng = np.random.default_rng(synth.SEED_VEC)
+    F = rng.standard_normal((k, n))
+    F[0] = f
+    Fd = torch.from_numpy(F).cuda()
+    X = torch.zeros_like(Fd)
+    tol, maxiter = args.tol, cfg["maxiter"]
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            X.zero_()
+            h.solve_batched(Fd, X, tol=tol, maxiter=maxiter)
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        cols, alg, launches = 0, 0.0, 0
+        with ClockSampler(local) as clk:
+            ev0.record(stream)
+            for _ in range(args.steps):
+                X.zero_()
+                _, its, rels, st = h.solve_batched(Fd, X, tol=tol, maxiter=maxiter)
+                s = h.stats()
+                cols += int(np.sum(its))
+                alg += s["alg_bytes"]
+                launches += s["kernel_launches"]
+            ev1.record(stream)
+            torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    peak, peak_src = peaks()
+    line = {
+        "metric": METRIC + " [batched: column V-cycles/s]", "value": cols / (ms / 1e3), "unit": "column V-cycles/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: f = 1 and k-1 seeded N(0,1) right-hand sides",
+        "config": {"workload": workload_name(args, cfg) + f"_batch{k}", "n": n, "nnz": nnz, "batch": k,
+                   "iters_per_column": [int(v) for v in its], "rel_resid_max": float(np.max(rels)),
+                   "solve_alg_GBps": alg / (ms / 1e3) / 1e9, "solve_roofline_frac": alg / (ms / 1e3) / 1e9 / peak,
+                   "levels": len(infos), "setup_s": setup_s},
+        "gpu_launches": launches, "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     cfg = dict(PROBLEM_DEFAULTS[args.problem])
@@ -257,6 +303,9 @@ def main():
     fd = torch.from_numpy(np.ascontiguousarray(f[r0:r1])).cuda()
     x = torch.zeros_like(fd)
     tol, maxiter = args.tol, cfg["maxiter"]
+    if args.batch > 1:
+        return run_batched(args, cfg, h, f, n, nnz, infos, setup_s, local, stream)
+
     def timed_solves(profile_mask):
         """K timed solves from x = 0 (barrier + synchronize on both sides, CUDA
         events on the solve stream)."""
