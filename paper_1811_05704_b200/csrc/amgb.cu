@@ -400,7 +400,7 @@ struct Handle {
     template <int U, bool PIPE, class Op>
     void rows_sell(const Sell& M, const Op& op, const int32_t* gate, const Red& red, bool stream_loads) {
         const int g = (int)std::max<int64_t>(
-            1, std::min<int64_t>((M.nrows + kBlock - 1) / kBlock, (int64_t)num_sms * (PIPE ? 4 : 6)));
+            1, std::min<int64_t>((M.nrows + kBlock - 1) / kBlock, (int64_t)num_sms * minb_of<Op>(PIPE ? 4 : 6)));
         if (stream_loads)
             sell_rows<U, true, PIPE, Op><<<g, kBlock, 0, stream>>>(M, op, gate, red);
         else
@@ -423,7 +423,8 @@ struct Handle {
             ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
             configured = smem;
         }
-        const int g = (int)std::max<int64_t>(1, std::min<int64_t>(M.ntiles, (int64_t)num_sms * kTmaBlocksPerSM));
+        const int g =
+            (int)std::max<int64_t>(1, std::min<int64_t>(M.ntiles, (int64_t)num_sms * minb_of<Op>(kTmaBlocksPerSM)));
         kern<<<g, kTmaThreads, smem, stream>>>(M, op, gate, red);
     }
     template <int T, class Op>

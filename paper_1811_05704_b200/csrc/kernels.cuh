@@ -66,6 +66,16 @@ struct Vk {
 };
 template <class Op>
 using acc_t = decltype(std::declval<Op>().gather(0));
+// columns carried by an op's accumulator (1 = single right-hand side)
+template <class Op>
+constexpr int cols_of() { return (int)(sizeof(acc_t<Op>) / sizeof(double)); }
+// entries in flight per thread: 8 gathers for one column, fewer for K columns
+// (each gather already moves K doubles; keeps the register file from spilling)
+template <class Op>
+constexpr int unroll_of(int u1) { return cols_of<Op>() == 1 ? u1 : (cols_of<Op>() == 2 ? 4 : (cols_of<Op>() == 4 ? 2 : 1)); }
+// resident blocks requested per SM (launch bounds)
+template <class Op>
+constexpr int minb_of(int b1) { return cols_of<Op>() == 1 ? b1 : 2; }
 __device__ __forceinline__ void fma_acc(double& s, double a, double x) { s = fma(a, x, s); }
 template <int K>
 __device__ __forceinline__ void fma_acc(Vk<K>& s, double a, const Vk<K>& x) {
@@ -177,8 +187,10 @@ __device__ __forceinline__ bool gated(const int32_t* gate) {
 // PIPE = false: all U entries of the (narrow, w <= U) row in one chunk, no
 // prefetch registers; launch bounds ask for >= 6 resident blocks (48 warps) so
 // enough loads are in flight per SM.
-template <int U, bool STREAM, bool PIPE, class Op>
-__global__ void __launch_bounds__(kBlock, PIPE ? 4 : 6) sell_rows(Sell A, Op op, const int32_t* gate, Red red) {
+template <int U1, bool STREAM, bool PIPE, class Op>
+__global__ void __launch_bounds__(kBlock, minb_of<Op>(PIPE ? 4 : 6)) sell_rows(Sell A, Op op, const int32_t* gate,
+                                                                                 Red red) {
+    constexpr int U = unroll_of<Op>(U1);
     if (gated(gate)) return;
     op.prepare();
     constexpr int ND = Op::NDOT > 0 ? Op::NDOT : 1;
@@ -188,8 +200,9 @@ __global__ void __launch_bounds__(kBlock, PIPE ? 4 : 6) sell_rows(Sell A, Op op,
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < A.nrows; row += stride) {
         // row-local epilogue operands are requested first, so their latency
-        // overlaps the matrix stream
-        const typename Op::Row rr = op.load(row);
+        // overlaps the matrix stream (single column; K-column rows load later)
+        typename Op::Row rr{};
+        if constexpr (cols_of<Op>() == 1) rr = op.load(row);
         const int64_t s = row >> 5;
         const int lane = (int)(row & 31);
         const int64_t beg = A.sptr[s];
@@ -235,6 +248,7 @@ __global__ void __launch_bounds__(kBlock, PIPE ? 4 : 6) sell_rows(Sell A, Op op,
                 v[u] = vn[u];
             }
         }
+        if constexpr (cols_of<Op>() > 1) rr = op.load(row);
         op.row(row, sum, rr, dots);
     }
     if constexpr (Op::NDOT > 0) grid_reduce<Op::NDOT>(dots, red, op.fin);
@@ -304,8 +318,9 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 }
 
 template <int T, bool STREAM, class Op>
-__global__ void __launch_bounds__(kTmaThreads, kTmaBlocksPerSM) sell_tma(SellTma A, Op op, const int32_t* gate,
-                                                                         Red red) {
+__global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sell_tma(SellTma A, Op op,
+                                                                                      const int32_t* gate, Red red) {
+    constexpr int UN = unroll_of<Op>(8);
     if (gated(gate)) return;
     op.prepare();
     constexpr int C = 32 / T;  // slice height
@@ -358,7 +373,8 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaBlocksPerSM) sell_tma(SellTma
             const int64_t row = slice * C + r;
             const bool has_row = slice < A.nslices && row < A.nrows;
             typename Op::Row rr{};
-            if (pt == 0 && has_row) rr = op.load(row);  // in flight during the wait
+            if constexpr (cols_of<Op>() == 1)
+                if (pt == 0 && has_row) rr = op.load(row);  // in flight during the wait
             int off = 0, w = 0;
             if (slice < A.nslices) {
                 const int64_t e0 = A.sptr[slice];
@@ -370,18 +386,18 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaBlocksPerSM) sell_tma(SellTma
             const int32_t* sc =
                 reinterpret_cast<const int32_t*>(smem + (size_t)s * stage_bytes + (size_t)te * 8) + off + r;
             acc_t<Op> sum{};
-            for (int k0 = pt; k0 < w; k0 += 8 * T) {
-                acc_t<Op> xv[8];
-                int32_t c[8];
+            for (int k0 = pt; k0 < w; k0 += UN * T) {
+                acc_t<Op> xv[UN];
+                int32_t c[UN];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
+                for (int u = 0; u < UN; ++u) {
                     const int k = k0 + u * T;
                     c[u] = k < w ? sc[C * k] : 0;
                 }
 #pragma unroll
-                for (int u = 0; u < 8; ++u) xv[u] = (k0 + u * T < w) ? op.gather(c[u]) : acc_t<Op>{};
+                for (int u = 0; u < UN; ++u) xv[u] = (k0 + u * T < w) ? op.gather(c[u]) : acc_t<Op>{};
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
+                for (int u = 0; u < UN; ++u) {
                     const int k = k0 + u * T;
                     if (k < w) fma_acc(sum, sv[C * k], xv[u]);
                 }
@@ -392,6 +408,8 @@ __global__ void __launch_bounds__(kTmaThreads, kTmaBlocksPerSM) sell_tma(SellTma
 #pragma unroll
                 for (int o = C; o < 32; o <<= 1) add_acc(sum, shfl_xor_acc(0xffffffffu, sum, o));
             }
+            if constexpr (cols_of<Op>() > 1)
+                if (pt == 0 && has_row) rr = op.load(row);
             if (pt == 0 && has_row) op.row(row, sum, rr, dots);
         }
     }
@@ -438,7 +456,6 @@ __global__ void __launch_bounds__(kBlock) csr_rows(CsrDev A, Op op, const int32_
         // memory (the shared-memory product tile would be K times larger)
         const int64_t groups = ((int64_t)gridDim.x * blockDim.x) / G;
         for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + tid) / G; r < A.nrows; r += groups) {
-            const typename Op::Row rr = op.load(r);
             acc_t<Op> s{};
             for (int k = A.ptr[r] + lig; k < A.ptr[r + 1]; k += G)
                 fma_acc(s, ld_mat<STREAM>(A.val + k), op.gather(ld_mat<STREAM>(A.col + k)));
@@ -446,7 +463,7 @@ __global__ void __launch_bounds__(kBlock) csr_rows(CsrDev A, Op op, const int32_
 #pragma unroll
                 for (int o = G / 2; o > 0; o >>= 1) add_acc(s, shfl_xor_acc(gmask, s, o));
             }
-            if (lig == 0) op.row(r, s, rr, dots);
+            if (lig == 0) op.row(r, s, op.load(r), dots);
         }
         if constexpr (Op::NDOT > 0) grid_reduce<Op::NDOT>(dots, red, op.fin);
         return;
