@@ -58,6 +58,7 @@ class AmgParams(C.Structure):
         ("solver", C.c_int32),
         ("device", C.c_int32),
         ("use_graph", C.c_int32),
+        ("precision", C.c_int32),
     ]
 
 
@@ -158,8 +159,10 @@ PARAM_KEYS = {
     "solver.type": "solver",
     "device": "device",
     "use_graph": "use_graph",
+    "precision": "precision",
 }
-_ENUMS = {"relax": RELAX, "coarsening": COARSENING, "solver": SOLVER}
+PRECISION = {"double": 0, "mixed": 1}
+_ENUMS = {"relax": RELAX, "coarsening": COARSENING, "solver": SOLVER, "precision": PRECISION}
 
 
 class AmgError(RuntimeError):

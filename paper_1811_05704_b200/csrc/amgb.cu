@@ -397,27 +397,27 @@ struct Handle {
             if (&M == &L.A) return AMG_PROF_A_COARSE;
         return AMG_PROF_TRANSFER;
     }
-    template <int U, bool PIPE, class Op>
+    template <int U, bool PIPE, bool F32, class Op>
     void rows_sell(const Sell& M, const Op& op, const int32_t* gate, const Red& red, bool stream_loads) {
         const int g = (int)std::max<int64_t>(
             1, std::min<int64_t>((M.nrows + kBlock - 1) / kBlock, (int64_t)num_sms * minb_of<Op>(PIPE ? 4 : 6)));
         if (stream_loads)
-            sell_rows<U, true, PIPE, Op><<<g, kBlock, 0, stream>>>(M, op, gate, red);
+            sell_rows<U, true, PIPE, Op, F32><<<g, kBlock, 0, stream>>>(M, op, gate, red);
         else
-            sell_rows<U, false, PIPE, Op><<<g, kBlock, 0, stream>>>(M, op, gate, red);
+            sell_rows<U, false, PIPE, Op, F32><<<g, kBlock, 0, stream>>>(M, op, gate, red);
     }
-    template <int G, class Op>
+    template <int G, bool F32, class Op>
     void rows_csr(const CsrDev& M, const Op& op, const int32_t* gate, const Red& red, bool stream_loads) {
         const int g = (int)std::max<int64_t>(1, std::min<int64_t>(M.nblocks, (int64_t)num_sms * 8));
         if (stream_loads)
-            csr_rows<G, true, Op><<<g, kBlock, 0, stream>>>(M, op, gate, red);
+            csr_rows<G, true, Op, F32><<<g, kBlock, 0, stream>>>(M, op, gate, red);
         else
-            csr_rows<G, false, Op><<<g, kBlock, 0, stream>>>(M, op, gate, red);
+            csr_rows<G, false, Op, F32><<<g, kBlock, 0, stream>>>(M, op, gate, red);
     }
-    template <int T, bool STREAM, class Op>
+    template <int T, bool STREAM, bool F32, class Op>
     void rows_tma_impl(const SellTma& M, const Op& op, const int32_t* gate, const Red& red) {
-        auto kern = sell_tma<T, STREAM, Op>;
-        const size_t smem = (size_t)kTmaStages * M.tile_ent * 12 + 2 * kTmaStages * 8;
+        auto kern = sell_tma<T, STREAM, Op, F32>;
+        const size_t smem = (size_t)kTmaStages * M.tile_ent * (F32 ? 8 : 12) + 2 * kTmaStages * 8;
         static size_t configured = 0;  // per instantiation
         if (smem > configured) {
             ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
@@ -427,20 +427,21 @@ struct Handle {
             (int)std::max<int64_t>(1, std::min<int64_t>(M.ntiles, (int64_t)num_sms * minb_of<Op>(kTmaBlocksPerSM)));
         kern<<<g, kTmaThreads, smem, stream>>>(M, op, gate, red);
     }
-    template <int T, class Op>
+    template <int T, bool F32, class Op>
     void rows_tma(const SellTma& M, const Op& op, const int32_t* gate, const Red& red, bool stream_loads) {
         if (stream_loads)
-            rows_tma_impl<T, true>(M, op, gate, red);
+            rows_tma_impl<T, true, F32>(M, op, gate, red);
         else
-            rows_tma_impl<T, false>(M, op, gate, red);
+            rows_tma_impl<T, false, F32>(M, op, gate, red);
     }
     // a part with no rows contributes zeros to an all-reduce
     void zero_defer(Part& p) {
         if (p.red.defer) ck(cudaMemsetAsync(p.red.defer, 0, 4 * sizeof(double), stream), "memset");
     }
-    // One pass over matrix M of part p with the fused epilogue op.
-    template <class Op>
-    void rows(Part& p, const DMat& M, const Op& op, const int32_t* gate, const char* what) {
+    // One pass over matrix M of part p with the fused epilogue op; F32: read the
+    // fp32 copy of the matrix values (mixed-precision V-cycle).
+    template <bool F32, class Op>
+    void rows_impl(Part& p, const DMat& M, const Op& op, const int32_t* gate, const char* what) {
         if (M.nrows == 0) {
             if constexpr (Op::NDOT > 0) zero_defer(p);
             return;
@@ -448,23 +449,36 @@ struct Handle {
         // matrices too big for L2 stream their entries (evict-first); the rest
         // keep them cached so coarse levels stay L2-resident across cycles
         const bool big = M.nnz * 12 > (int64_t)48 << 20;
-        const double bytes = 12.0 * M.nnz + 4.0 * M.nrows + 8.0 * M.ncols * Op::GATHER + 8.0 * M.nrows * Op::ROWV;
+        const double mb = F32 ? 8.0 : 12.0;
+        const double bytes = mb * M.nnz + 4.0 * M.nrows + 8.0 * M.ncols * Op::GATHER + 8.0 * M.nrows * Op::ROWV;
         const Red& red = p.red;
         launch(mat_class(p, M), bytes, what, [&] {
             if (M.fmt == Fmt::TMA) {  // T = 1 lane per row (narrow rows only, pick_format)
-                rows_tma<1>(M.tma, op, gate, red, big);
+                rows_tma<1, F32>(M.tma, op, gate, red, big);
             } else if (M.fmt == Fmt::CSR) {
                 switch (M.csr.G) {
-                    case 1: rows_csr<1>(M.csr, op, gate, red, big); break;
-                    case 2: rows_csr<2>(M.csr, op, gate, red, big); break;
-                    case 4: rows_csr<4>(M.csr, op, gate, red, big); break;
-                    case 8: rows_csr<8>(M.csr, op, gate, red, big); break;
-                    default: rows_csr<16>(M.csr, op, gate, red, big); break;
+                    case 1: rows_csr<1, F32>(M.csr, op, gate, red, big); break;
+                    case 2: rows_csr<2, F32>(M.csr, op, gate, red, big); break;
+                    case 4: rows_csr<4, F32>(M.csr, op, gate, red, big); break;
+                    case 8: rows_csr<8, F32>(M.csr, op, gate, red, big); break;
+                    default: rows_csr<16, F32>(M.csr, op, gate, red, big); break;
                 }
             } else {
-                rows_sell<8, true>(M.sell, op, gate, red, big);
+                rows_sell<8, true, F32>(M.sell, op, gate, red, big);
             }
         });
+    }
+    template <class Op>
+    void rows(Part& p, const DMat& M, const Op& op, const int32_t* gate, const char* what) {
+        rows_impl<false>(p, M, op, gate, what);
+    }
+    // V-cycle passes: fp32 hierarchy values when prm.precision == 1
+    template <class Op>
+    void vrows(Part& p, const DMat& M, const Op& op, const int32_t* gate, const char* what) {
+        if (prm.precision == 1)
+            rows_impl<true>(p, M, op, gate, what);
+        else
+            rows_impl<false>(p, M, op, gate, what);
     }
     template <class Op>
     void vec(Part& p, int64_t n, const Op& op, const int32_t* gate, const char* what) {
@@ -639,7 +653,7 @@ bool Handle::vcycle(int l, const CSel& fsel, const Sel& osel, const GSel& gate, 
             x_is_mf = true;  // fused: t = f - A (m o f)
             for_parts([&](Part& p, size_t) {
                 DevLevel& L = p.lv[l];
-                rows(p, L.A, OpRes0{L.m, fsel(p), L.t, {}}, gate(p), "res0");
+                vrows(p, L.A, OpRes0{L.m, fsel(p), L.t, {}}, gate(p), "res0");
             });
         } else {
             for_parts([&](Part& p, size_t i) {
@@ -653,14 +667,14 @@ bool Handle::vcycle(int l, const CSel& fsel, const Sel& osel, const GSel& gate, 
                 exchange(l, xsel);
                 for_parts([&](Part& p, size_t i) {
                     DevLevel& L = p.lv[l];
-                    rows(p, L.A, OpRelax<0, NoFin>{X[i], L.m, fsel(p), Y[i], {}}, gate(p), "relax");
+                    vrows(p, L.A, OpRelax<0, NoFin>{X[i], L.m, fsel(p), Y[i], {}}, gate(p), "relax");
                 });
                 swap_xy();
             }
             exchange(l, xsel);
             for_parts([&](Part& p, size_t i) {
                 DevLevel& L = p.lv[l];
-                rows(p, L.A, OpResidual<0, NoFin>{X[i], fsel(p), L.t, {}}, gate(p), "residual");
+                vrows(p, L.A, OpResidual<0, NoFin>{X[i], fsel(p), L.t, {}}, gate(p), "residual");
             });
         }
     } else {
@@ -676,7 +690,7 @@ bool Handle::vcycle(int l, const CSel& fsel, const Sel& osel, const GSel& gate, 
                     exchange(l, xsel);
                     for_parts([&](Part& p, size_t i) {
                         DevLevel& L = p.lv[l];
-                        rows(p, L.A,
+                        vrows(p, L.A,
                              OpCheb<0, NoFin>{X[i], fsel(p), L.diag, L.p, Y[i], L.cheb_alpha[k], L.cheb_beta[k],
                                               prm.cheb_scaled, k == 0, {}},
                              gate(p), "cheb");
@@ -692,7 +706,7 @@ bool Handle::vcycle(int l, const CSel& fsel, const Sel& osel, const GSel& gate, 
         exchange(l, xsel);
         for_parts([&](Part& p, size_t i) {
             DevLevel& L = p.lv[l];
-            rows(p, L.A, OpResidual<0, NoFin>{X[i], fsel(p), L.t, {}}, gate(p), "residual");
+            vrows(p, L.A, OpResidual<0, NoFin>{X[i], fsel(p), L.t, {}}, gate(p), "residual");
         });
     }
 
@@ -703,7 +717,7 @@ bool Handle::vcycle(int l, const CSel& fsel, const Sel& osel, const GSel& gate, 
         DevLevel& C = p.lv[l + 1];
         // into the next level's vector; a replicated next level receives the
         // slice [crow0, crow1) of the full vector
-        rows(p, L.R, OpSpmv{L.t, C.f + (next_rep ? L.crow0 : 0)}, gate(p), "restrict");
+        vrows(p, L.R, OpSpmv{L.t, C.f + (next_rep ? L.crow0 : 0)}, gate(p), "restrict");
     });
     // entering the replicated levels: gather the other ranks' slices of f_{l+1}
     if (next_rep && !parts[0].lv[l].replicated) allgather_slices(l + 1, [&](Part& p) { return p.lv[l + 1].f; });
@@ -714,9 +728,9 @@ bool Handle::vcycle(int l, const CSel& fsel, const Sel& osel, const GSel& gate, 
         DevLevel& L = p.lv[l];
         DevLevel& C = p.lv[l + 1];
         if (x_is_mf)
-            rows(p, L.P, OpProl0{C.o, L.m, fsel(p), X[i], {}}, gate(p), "prolong0");
+            vrows(p, L.P, OpProl0{C.o, L.m, fsel(p), X[i], {}}, gate(p), "prolong0");
         else
-            rows(p, L.P, OpProlAdd{C.o, X[i], {}}, gate(p), "prolong");
+            vrows(p, L.P, OpProlAdd{C.o, X[i], {}}, gate(p), "prolong");
     });
 
     // ---- post-smoothing; the last sweep writes `out`
@@ -735,18 +749,18 @@ bool Handle::vcycle(int l, const CSel& fsel, const Sel& osel, const GSel& gate, 
             double* dst = last ? osel(p) : Y[i];
             if (!cheb) {
                 if (last && with_rho)
-                    rows(p, L.A, OpRelax<1, FinRho>{X[i], L.m, fsel(p), dst, FinRho{p.ks}}, gate(p), "relax+dot");
+                    vrows(p, L.A, OpRelax<1, FinRho>{X[i], L.m, fsel(p), dst, FinRho{p.ks}}, gate(p), "relax+dot");
                 else
-                    rows(p, L.A, OpRelax<0, NoFin>{X[i], L.m, fsel(p), dst, {}}, gate(p), "relax");
+                    vrows(p, L.A, OpRelax<0, NoFin>{X[i], L.m, fsel(p), dst, {}}, gate(p), "relax");
             } else {
                 const int k = s % K;
                 if (last && with_rho)
-                    rows(p, L.A,
+                    vrows(p, L.A,
                          OpCheb<1, FinRho>{X[i], fsel(p), L.diag, L.p, dst, L.cheb_alpha[k], L.cheb_beta[k],
                                            prm.cheb_scaled, k == 0, FinRho{p.ks}},
                          gate(p), "cheb+dot");
                 else
-                    rows(p, L.A,
+                    vrows(p, L.A,
                          OpCheb<0, NoFin>{X[i], fsel(p), L.diag, L.p, dst, L.cheb_alpha[k], L.cheb_beta[k],
                                           prm.cheb_scaled, k == 0, {}},
                          gate(p), "cheb");
@@ -1361,7 +1375,7 @@ std::vector<int32_t> row_blocks(const Csr& A, int G) {
     return b;
 }
 
-DMat upload_mat(Handle& H, const Csr& A, int64_t* bytes) {
+DMat upload_mat(Handle& H, const Csr& A, int64_t* bytes, bool f32 = false) {
     DMat d;
     d.nrows = A.nrows;
     d.ncols = A.ncols;
@@ -1387,6 +1401,7 @@ DMat upload_mat(Handle& H, const Csr& A, int64_t* bytes) {
         d.csr.col = H.upload(A.col);
         d.csr.val = H.upload(A.val);
         d.csr.brow = H.upload(blocks);
+        if (f32) d.csr.valf = H.upload(std::vector<float>(A.val.begin(), A.val.end()));
         d.stored = d.nnz;
         *bytes += (int64_t)(ptr32.size() * 4 + A.col.size() * 12 + blocks.size() * 4);
     } else if (d.fmt == Fmt::SELL) {
@@ -1397,6 +1412,7 @@ DMat upload_mat(Handle& H, const Csr& A, int64_t* bytes) {
         d.sell.sptr = H.upload(S.sptr);
         d.sell.col = H.upload(S.col);
         d.sell.val = H.upload(S.val);
+        if (f32) d.sell.valf = H.upload(std::vector<float>(S.val.begin(), S.val.end()));
         d.stored = (int64_t)S.col.size();
         *bytes += (int64_t)(S.sptr.size() * 8 + S.col.size() * 12);
     } else {  // TMA-staged SELL-C: lanes per row T from the longest row, C = 32 / T
@@ -1421,6 +1437,7 @@ DMat upload_mat(Handle& H, const Csr& A, int64_t* bytes) {
         t.sptr = H.upload(S.sptr);
         t.col = H.upload(S.col);
         t.val = H.upload(S.val);
+        if (f32) t.valf = H.upload(std::vector<float>(S.val.begin(), S.val.end()));
         d.stored = (int64_t)S.col.size();
         *bytes += (int64_t)(S.sptr.size() * 8 + S.col.size() * 12);
     }
@@ -1449,9 +1466,12 @@ void cheb_coeffs(double d, double c, int K, std::vector<double>& a, std::vector<
 // read once per pass (12 B per entry + 4 B per row), every vector read or
 // written once per kernel that touches it.
 double level_alg_bytes(int64_t n_, int64_t z_, int64_t p_, int64_t c_, const amg_params& p, bool coarsest) {
-    const double n = (double)n_, z = (double)z_;
+    const double n = (double)n_;
     if (coarsest) return 8.0 * n * n + 16.0 * n;
-    const double pp = (double)p_, c = (double)c_;
+    // fp32 hierarchy values: 8 instead of 12 bytes per entry (scale nnz by 2/3)
+    const double mscale = p.precision == 1 ? 8.0 / 12.0 : 1.0;
+    const double z = (double)z_ * mscale;
+    const double pp = (double)p_ * mscale, c = (double)c_;
     const double apass_relax = 12 * z + 4 * n + 32 * n;  // x, m, f read, out written
     const double restrict_b = 12 * pp + 4 * c + 8 * n + 8 * c;
     if (p.relax == 2) {
@@ -1501,15 +1521,16 @@ void upload_part(Handle& H, const RankPart& RP, Part& P) {
             cheb_coeffs(hl.cheb_d, hl.cheb_c, prm.cheb_degree, L.cheb_alpha, L.cheb_beta);
         L.alg_bytes = level_alg_bytes(L.n, L.nnzA, L.nnzP, coarsest ? 0 : lp.crow1 - lp.crow0, prm, coarsest);
         const int64_t nv = L.n + L.ng;
+        const bool f32 = prm.precision == 1;  // fp32 copies of the V-cycle matrix values
         if (!coarsest || nlev == 1) {
-            L.A = upload_mat(H, lp.A, &L.dev_bytes);
+            L.A = upload_mat(H, lp.A, &L.dev_bytes, f32);
             L.padA = L.A.stored;
         } else {
             L.padA = L.nnzA;
         }
         if (!coarsest) {
-            L.P = upload_mat(H, lp.P, &L.dev_bytes);
-            L.R = upload_mat(H, lp.R, &L.dev_bytes);
+            L.P = upload_mat(H, lp.P, &L.dev_bytes, f32);
+            L.R = upload_mat(H, lp.R, &L.dev_bytes, f32);
             if (prm.relax != 2) L.m = H.upload(lp.m);
             if (prm.relax == 2) L.diag = H.upload(lp.diag);  // Chebyshev D^-1 scaling
             L.x = H.dalloc(nv);
@@ -1609,6 +1630,7 @@ void amg_params_default(amg_params* p) {
     p->solver = 0;
     p->device = 0;
     p->use_graph = 1;
+    p->precision = 0;
 }
 
 const char* amg_last_error(void) { return amgb::g_err.c_str(); }
@@ -1632,6 +1654,7 @@ static amg_status check_params(const amg_params& p) {
     if (!(p.p_omega >= 0 && p.p_omega < 2)) return set_error(AMG_E_INVALID_ARG, "p_omega in [0,2)");
     if (p.coarse_enough < 1 || p.max_levels < 1 || p.dense_max < 1)
         return set_error(AMG_E_INVALID_ARG, "coarse_enough, max_levels, dense_max >= 1");
+    if (p.precision < 0 || p.precision > 1) return set_error(AMG_E_INVALID_ARG, "precision must be 0 or 1");
     return AMG_OK;
 }
 

@@ -29,6 +29,7 @@ struct Sell {
     const int64_t* sptr = nullptr;
     const int32_t* col = nullptr;
     const double* val = nullptr;
+    const float* valf = nullptr;  // fp32 copy of val (mixed-precision V-cycle)
 };
 
 // Krylov scalars kept on the device between kernels.
@@ -55,6 +56,15 @@ __device__ __forceinline__ double ld_mat(const double* p) {
 template <bool STREAM>
 __device__ __forceinline__ int32_t ld_mat(const int32_t* p) {
     if constexpr (STREAM) return __ldcs(p); else return __ldg(p);
+}
+template <bool STREAM>
+__device__ __forceinline__ float ld_mat(const float* p) {
+    if constexpr (STREAM) return __ldcs(p); else return __ldg(p);
+}
+// matrix value k of a store: fp64, or the fp32 copy widened to fp64 (F32)
+template <bool STREAM, bool F32, class M>
+__device__ __forceinline__ double ld_val(const M& A, int64_t k) {
+    if constexpr (F32) return (double)ld_mat<STREAM>(A.valf + k); else return ld_mat<STREAM>(A.val + k);
 }
 
 // Accumulator of a row kernel: one double (single right-hand side) or Vk<K> (K
@@ -187,7 +197,7 @@ __device__ __forceinline__ bool gated(const int32_t* gate) {
 // PIPE = false: all U entries of the (narrow, w <= U) row in one chunk, no
 // prefetch registers; launch bounds ask for >= 6 resident blocks (48 warps) so
 // enough loads are in flight per SM.
-template <int U1, bool STREAM, bool PIPE, class Op>
+template <int U1, bool STREAM, bool PIPE, class Op, bool F32 = false>
 __global__ void __launch_bounds__(kBlock, minb_of<Op>(PIPE ? 4 : 6)) sell_rows(Sell A, Op op, const int32_t* gate,
                                                                                  Red red) {
     constexpr int U = unroll_of<Op>(U1);
@@ -208,14 +218,14 @@ __global__ void __launch_bounds__(kBlock, minb_of<Op>(PIPE ? 4 : 6)) sell_rows(S
         const int64_t beg = A.sptr[s];
         const int w = (int)((A.sptr[s + 1] - beg) >> 5);
         const int32_t* cp = A.col + beg + lane;
-        const double* vp = A.val + beg + lane;
+        const int64_t vb = beg + lane;
         acc_t<Op> sum{};
         int32_t c[U];
         double v[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             c[u] = u < w ? ld_mat<STREAM>(cp + 32 * u) : 0;
-            v[u] = u < w ? ld_mat<STREAM>(vp + 32 * u) : 0.0;
+            v[u] = u < w ? ld_val<STREAM, F32>(A, vb + 32 * u) : 0.0;
         }
         if constexpr (!PIPE) {
             acc_t<Op> xv[U];
@@ -237,7 +247,7 @@ __global__ void __launch_bounds__(kBlock, minb_of<Op>(PIPE ? 4 : 6)) sell_rows(S
             for (int u = 0; u < U; ++u) {
                 const int k = k0 + U + u;
                 cn[u] = k < w ? ld_mat<STREAM>(cp + 32 * k) : 0;
-                vn[u] = k < w ? ld_mat<STREAM>(vp + 32 * k) : 0.0;
+                vn[u] = k < w ? ld_val<STREAM, F32>(A, vb + 32 * k) : 0.0;
             }
 #pragma unroll
             for (int u = 0; u < U; ++u)
@@ -274,6 +284,7 @@ struct SellTma {
     const int64_t* sptr = nullptr;  // nslices + 1 element offsets (multiples of C)
     const int32_t* col = nullptr;
     const double* val = nullptr;
+    const float* valf = nullptr;    // fp32 copy of val (mixed-precision V-cycle)
     int32_t T = 1;          // lanes per row; slice height C = 32 / T
     int32_t tile_ent = 0;   // capacity of one stage in entries (max over tiles)
 };
@@ -317,18 +328,20 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
             : "memory");
 }
 
-template <int T, bool STREAM, class Op>
+template <int T, bool STREAM, class Op, bool F32 = false>
 __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sell_tma(SellTma A, Op op,
                                                                                       const int32_t* gate, Red red) {
+    using VT = std::conditional_t<F32, float, double>;
+    constexpr int VB = (int)sizeof(VT);
     constexpr int UN = unroll_of<Op>(8);
     if (gated(gate)) return;
     op.prepare();
     constexpr int C = 32 / T;  // slice height
     constexpr int NS = 8;      // slices per tile (one per consumer warp)
     extern __shared__ __align__(128) unsigned char smem[];
-    // layout: kTmaStages x { val[tile_ent] (8 B), col[tile_ent] (4 B) } | barriers
+    // layout: kTmaStages x { val[tile_ent] (VB bytes), col[tile_ent] (4 B) } | barriers
     const int te = A.tile_ent;
-    const size_t stage_bytes = (size_t)te * 12;
+    const size_t stage_bytes = (size_t)te * (VB + 4);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTmaStages * stage_bytes);  // full[S], empty[S]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -358,9 +371,12 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sel
                 const uint32_t n = (uint32_t)(e1 - e0);
                 const uint32_t full = smem_u32(bars + s);
                 unsigned char* st = smem + (size_t)s * stage_bytes;
-                mbar_expect_tx(full, n * 12u);
-                bulk_g2s<STREAM>(smem_u32(st), A.val + e0, n * 8u, full, policy);
-                bulk_g2s<STREAM>(smem_u32(st + (size_t)te * 8), A.col + e0, n * 4u, full, policy);
+                mbar_expect_tx(full, n * (uint32_t)(VB + 4));
+                if constexpr (F32)
+                    bulk_g2s<STREAM>(smem_u32(st), A.valf + e0, n * 4u, full, policy);
+                else
+                    bulk_g2s<STREAM>(smem_u32(st), A.val + e0, n * 8u, full, policy);
+                bulk_g2s<STREAM>(smem_u32(st + (size_t)te * VB), A.col + e0, n * 4u, full, policy);
             }
         }
     } else {  // ------------------------------------ consumer warps
@@ -382,9 +398,9 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sel
                 w = (int)((A.sptr[slice + 1] - e0) / C);
             }
             mbar_wait(smem_u32(bars + s), (i / kTmaStages) & 1);
-            const double* sv = reinterpret_cast<const double*>(smem + (size_t)s * stage_bytes) + off + r;
+            const VT* sv = reinterpret_cast<const VT*>(smem + (size_t)s * stage_bytes) + off + r;
             const int32_t* sc =
-                reinterpret_cast<const int32_t*>(smem + (size_t)s * stage_bytes + (size_t)te * 8) + off + r;
+                reinterpret_cast<const int32_t*>(smem + (size_t)s * stage_bytes + (size_t)te * VB) + off + r;
             acc_t<Op> sum{};
             for (int k0 = pt; k0 < w; k0 += UN * T) {
                 acc_t<Op> xv[UN];
@@ -399,7 +415,7 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sel
 #pragma unroll
                 for (int u = 0; u < UN; ++u) {
                     const int k = k0 + u * T;
-                    if (k < w) fma_acc(sum, sv[C * k], xv[u]);
+                    if (k < w) fma_acc(sum, (double)sv[C * k], xv[u]);
                 }
             }
             __syncwarp();
@@ -435,11 +451,12 @@ struct CsrDev {
     const int32_t* ptr = nullptr;   // nrows + 1 (nnz < 2^31 per level)
     const int32_t* col = nullptr;
     const double* val = nullptr;
+    const float* valf = nullptr;    // fp32 copy of val (mixed-precision V-cycle)
     const int32_t* brow = nullptr;  // nblocks + 1 first rows of the row blocks
     int32_t G = 1;                  // threads per row in the summation phase
 };
 
-template <int G, bool STREAM, class Op>
+template <int G, bool STREAM, class Op, bool F32 = false>
 __global__ void __launch_bounds__(kBlock) csr_rows(CsrDev A, Op op, const int32_t* gate, Red red) {
     if (gated(gate)) return;
     op.prepare();
@@ -458,7 +475,7 @@ __global__ void __launch_bounds__(kBlock) csr_rows(CsrDev A, Op op, const int32_
         for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + tid) / G; r < A.nrows; r += groups) {
             acc_t<Op> s{};
             for (int k = A.ptr[r] + lig; k < A.ptr[r + 1]; k += G)
-                fma_acc(s, ld_mat<STREAM>(A.val + k), op.gather(ld_mat<STREAM>(A.col + k)));
+                fma_acc(s, ld_val<STREAM, F32>(A, k), op.gather(ld_mat<STREAM>(A.col + k)));
             if constexpr (G > 1) {
 #pragma unroll
                 for (int o = G / 2; o > 0; o >>= 1) add_acc(s, shfl_xor_acc(gmask, s, o));
@@ -480,7 +497,7 @@ __global__ void __launch_bounds__(kBlock) csr_rows(CsrDev A, Op op, const int32_
                 const int e = tid + k * kBlock;
                 if (e < ne) {
                     c[k] = ld_mat<STREAM>(A.col + eb + e);
-                    v[k] = ld_mat<STREAM>(A.val + eb + e);
+                    v[k] = ld_val<STREAM, F32>(A, eb + e);
                 }
             }
 #pragma unroll
@@ -504,7 +521,7 @@ __global__ void __launch_bounds__(kBlock) csr_rows(CsrDev A, Op op, const int32_
         } else {  // one long row
             double s = 0.0;
             for (int e = tid; e < ne; e += kBlock)
-                s += ld_mat<STREAM>(A.val + eb + e) * op.gather(ld_mat<STREAM>(A.col + eb + e));
+                s += ld_val<STREAM, F32>(A, eb + e) * op.gather(ld_mat<STREAM>(A.col + eb + e));
             s = warp_sum(s);
             if ((tid & 31) == 0) prod[tid >> 5] = s;
             __syncthreads();
