@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--batch", type=int, default=1,
                     help="k > 1: k right-hand sides per solve (amg_solve_batched); value counts column V-cycles")
+    ap.add_argument("--precision", default="double", choices=["double", "mixed"],
+                    help="mixed: fp32 hierarchy values in the V-cycle (not the headline; SURVEY §8f rank 2)")
     ap.add_argument("--json-out", default=None)
     return ap.parse_args()
 
@@ -142,7 +144,8 @@ def problem_arrays(name, n):
 
 
 def workload_name(args, cfg):
-    return f"{args.problem}{args.n}^3_{cfg['solver']}_sa_{cfg['relax']}"
+    w = f"{args.problem}{args.n}^3_{cfg['solver']}_sa_{cfg['relax']}"
+    return w + ("_mixed" if getattr(args, "precision", "double") == "mixed" else "")
 
 
 def cpu_baseline_full_solve(ptr, col, val, f, cfg, tol, maxiter):
@@ -279,7 +282,7 @@ def main():
 
     ptr, col, val, f = problem_arrays(args.problem, args.n)
     n, nnz = len(f), int(ptr[-1])
-    prm = {"precond.relax.type": cfg["relax"], "solver.type": cfg["solver"]}
+    prm = {"precond.relax.type": cfg["relax"], "solver.type": cfg["solver"], "precision": args.precision}
     t0 = time.perf_counter()
     if world == 1:
         h = amgb.setup(ptr, col, val, prm, device=local, use_graph=0 if args.no_graph else 1)
@@ -420,7 +423,8 @@ def main():
             "metric": METRIC,
             "value": value, "unit": "V-cycles/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if args.precision == "double" else "f64 (V-cycle matrix values f32)",
             "data": "synthetic (seeded generators, synth/): 7-point FD Poisson, f = 1",
             "config": {
                 "workload": workload_name(args, cfg), "n": n, "nnz": nnz, "tol": tol,
