@@ -120,6 +120,9 @@ def lib():
             L.or_bicgstab.argtypes = [_P, C.c_int64, _I64P, _I32P, _F64P, C.c_int, _F64P, _F64P,
                                       C.c_double, C.c_int32, C.POINTER(C.c_int32),
                                       C.POINTER(C.c_double), C.POINTER(C.c_int32)]
+            L.or_gmres.argtypes = [_P, C.c_int64, _I64P, _I32P, _F64P, C.c_int, C.c_int32, _F64P, _F64P,
+                                   C.c_double, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_double),
+                                   C.POINTER(C.c_int32), C.c_void_p]
             _lib = L
     return _lib
 
@@ -366,3 +369,19 @@ def bicgstab(A: Csr, f, x0=None, tol=1e-8, maxiter=100, hier: Hierarchy | None =
                                   1 if hier else 0, f, x, tol, maxiter, C.byref(it),
                                   C.byref(rel), C.byref(vc)))
     return dict(x=x, iters=it.value, rel_resid=rel.value, status=rc, vcycles=vc.value)
+
+
+def gmres(A: Csr, f, x0=None, tol=1e-8, maxiter=100, m=30, hier: Hierarchy | None = None, history=False):
+    """Restarted right-preconditioned GMRES(m); hier=None means M = I."""
+    n = A.nrows
+    f = np.ascontiguousarray(f, np.float64)
+    x = np.zeros(n) if x0 is None else np.array(x0, np.float64, copy=True)
+    it, rel, vc = C.c_int32(), C.c_double(), C.c_int32()
+    hist = np.zeros(maxiter + 1) if history else None
+    rc = _check(lib().or_gmres(hier._h if hier else None, n, A.ptr, A.col, A.val, 1 if hier else 0, m, f, x,
+                               tol, maxiter, C.byref(it), C.byref(rel), C.byref(vc),
+                               hist.ctypes.data_as(C.c_void_p) if history else None))
+    out = dict(x=x, iters=it.value, rel_resid=rel.value, status=rc, vcycles=vc.value)
+    if history:
+        out["history"] = hist[:it.value + 1]
+    return out

@@ -948,3 +948,133 @@ int or_bicgstab(const or_hier *h, int64_t n, const int64_t *ptr, const int32_t *
     free(t);
     return status;
 }
+
+/* Restarted right-preconditioned GMRES(m) (PAPER.md:212 names GMRES; the
+ * algorithm is Saad, Iterative Methods for Sparse Linear Systems, 2nd ed.,
+ * Alg. 9.5 "GMRES with right preconditioning", restarted every m steps):
+ *   r = f - A x; beta = |r|; converged if beta <= tol |f|
+ *   cycle:  v_0 = r / beta;  g = beta e_0
+ *     for j = 0 .. m-1:
+ *        z = M v_j; w = A z
+ *        for i = 0 .. j:  h_ij = (w, v_i); w = w - h_ij v_i      (modified Gram-Schmidt)
+ *        h_{j+1,j} = |w|; v_{j+1} = w / h_{j+1,j}
+ *        apply the previous Givens rotations to column j of H; build rotation j
+ *        that zeroes h_{j+1,j}; g_{j+1} = -s_j g_j, g_j = c_j g_j
+ *        k += 1; stop the cycle if |g_{j+1}| <= tol |f| or k == maxiter
+ *     solve the upper-triangular H y = g (size j+1); x = x + M (V y)
+ *     r = f - A x; beta = |r|; converged if beta <= tol |f|  (true residual)
+ * A zero h_{j+1,j} (lucky breakdown) ends the cycle with the exact solution. */
+int or_gmres(const or_hier *h, int64_t n, const int64_t *ptr, const int32_t *col, const double *val,
+             int precond, int32_t m, const double *f, double *x, double tol, int32_t maxiter,
+             int32_t *iters, double *rel_resid, int32_t *vcycles, double *hist) {
+    or_csr A = {n, n, ptr[n], (int64_t *)ptr, (int32_t *)col, (double *)val};
+    double nf = sqrt(dot(n, f, f));
+    *iters = 0;
+    *rel_resid = 0.0;
+    *vcycles = 0;
+    if (m < 1) {
+        set_err("gmres: restart m must be >= 1");
+        return OR_E_INVALID;
+    }
+    if (nf == 0.0) {
+        for (int64_t i = 0; i < n; i++) x[i] = 0.0;
+        if (hist) hist[0] = 0.0;
+        return OR_OK;
+    }
+    size_t bytes = (size_t)n * sizeof(double);
+    double *V = (double *)malloc(bytes * (size_t)(m + 1));
+    double *H = (double *)calloc((size_t)(m + 1) * (size_t)m, sizeof(double)); /* H[i*m + j] */
+    double *cs = (double *)malloc((size_t)m * sizeof(double));
+    double *sn = (double *)malloc((size_t)m * sizeof(double));
+    double *g = (double *)malloc((size_t)(m + 1) * sizeof(double));
+    double *y = (double *)malloc((size_t)m * sizeof(double));
+    double *r = (double *)malloc(bytes), *z = (double *)malloc(bytes), *w = (double *)malloc(bytes);
+    double *u = (double *)malloc(bytes);
+    residual(&A, f, x, r);
+    double beta = sqrt(dot(n, r, r));
+    if (hist) hist[0] = beta;
+    int32_t k = 0, vc = 0;
+    int status = OR_OK;
+    while (beta > tol * nf && k < maxiter) {
+        for (int64_t i = 0; i < n; i++) V[i] = r[i] / beta;
+        for (int i = 0; i <= m; i++) g[i] = 0.0;
+        g[0] = beta;
+        int jlast = -1;
+        for (int j = 0; j < m; j++) {
+            double *vj = V + (size_t)j * n;
+            if (precond) {
+                or_precond(h, vj, z);
+                vc++;
+            } else {
+                memcpy(z, vj, bytes);
+            }
+            spmv_csr(&A, z, w);
+            for (int i = 0; i <= j; i++) {
+                double *vi = V + (size_t)i * n;
+                double hij = dot(n, w, vi);
+                H[i * m + j] = hij;
+                for (int64_t q = 0; q < n; q++) w[q] = w[q] - hij * vi[q];
+            }
+            double hn = sqrt(dot(n, w, w));
+            H[(j + 1) * m + j] = hn;
+            if (hn != 0.0)
+                for (int64_t q = 0; q < n; q++) V[(size_t)(j + 1) * n + q] = w[q] / hn;
+            for (int i = 0; i < j; i++) { /* previous rotations on column j */
+                double a = H[i * m + j], b = H[(i + 1) * m + j];
+                H[i * m + j] = cs[i] * a + sn[i] * b;
+                H[(i + 1) * m + j] = -sn[i] * a + cs[i] * b;
+            }
+            double a = H[j * m + j], b = H[(j + 1) * m + j];
+            double d = sqrt(a * a + b * b);
+            cs[j] = d == 0.0 ? 1.0 : a / d;
+            sn[j] = d == 0.0 ? 0.0 : b / d;
+            H[j * m + j] = d;
+            H[(j + 1) * m + j] = 0.0;
+            g[j + 1] = -sn[j] * g[j];
+            g[j] = cs[j] * g[j];
+            k += 1;
+            jlast = j;
+            if (hist) hist[k] = fabs(g[j + 1]);
+            if (fabs(g[j + 1]) <= tol * nf || k >= maxiter || hn == 0.0) break;
+        }
+        /* y = H^-1 g (upper triangular, back substitution) */
+        for (int i = jlast; i >= 0; i--) {
+            double s = g[i];
+            for (int q = i + 1; q <= jlast; q++) s -= H[i * m + q] * y[q];
+            if (H[i * m + i] == 0.0) {
+                set_err("gmres: singular Hessenberg");
+                status = OR_BREAKDOWN;
+                break;
+            }
+            y[i] = s / H[i * m + i];
+        }
+        if (status != OR_OK) break;
+        for (int64_t q = 0; q < n; q++) u[q] = 0.0; /* u = V y */
+        for (int i = 0; i <= jlast; i++)
+            for (int64_t q = 0; q < n; q++) u[q] = u[q] + y[i] * V[(size_t)i * n + q];
+        if (precond) {
+            or_precond(h, u, z);
+            vc++;
+        } else {
+            memcpy(z, u, bytes);
+        }
+        for (int64_t q = 0; q < n; q++) x[q] = x[q] + z[q];
+        residual(&A, f, x, r);
+        beta = sqrt(dot(n, r, r));
+    }
+    if (status == OR_OK && beta > tol * nf) status = OR_NOT_CONVERGED;
+    *iters = k;
+    *vcycles = vc;
+    *rel_resid = beta / nf;
+    free(V);
+    free(H);
+    free(cs);
+    free(sn);
+    free(g);
+    free(y);
+    free(r);
+    free(z);
+    free(w);
+    free(u);
+    return status;
+}

@@ -109,5 +109,12 @@ int or_cg(const or_hier *h, int64_t n, const int64_t *ptr, const int32_t *col, c
 int or_bicgstab(const or_hier *h, int64_t n, const int64_t *ptr, const int32_t *col,
                 const double *val, int precond, const double *f, double *x, double tol,
                 int32_t maxiter, int32_t *iters, double *rel_resid, int32_t *vcycles);
+/* Restarted right-preconditioned GMRES(m) (Saad 2003 Alg. 9.5 with
+ * modified Gram-Schmidt and Givens rotations).  iters = Arnoldi steps; vcycles
+ * counts preconditioner applications (one per step + one per restart cycle for
+ * x += M (V y)).  resid_hist (maxiter+1 or NULL): estimated residual norms. */
+int or_gmres(const or_hier *h, int64_t n, const int64_t *ptr, const int32_t *col, const double *val,
+             int precond, int32_t m, const double *f, double *x, double tol, int32_t maxiter,
+             int32_t *iters, double *rel_resid, int32_t *vcycles, double *resid_hist);
 
 #endif

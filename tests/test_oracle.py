@@ -684,3 +684,66 @@ def test_bicgstab_amg_convdiff():
     assert r["status"] == oracle.OK
     np.testing.assert_allclose(r["x"], np.linalg.solve(A.to_dense(), f), rtol=1e-8)
     assert r["vcycles"] in (2 * r["iters"], 2 * r["iters"] - 1)
+
+
+# --------------------------------------------------------------------- GMRES
+
+def test_gmres_examples():
+    """A = I: one step; the SPEC's non-symmetric 2x2 example is
+    solved in <= 2 steps; f = 0 -> 0 steps."""
+    r = oracle.gmres(csr_from_dense(np.eye(4)), np.arange(1.0, 5.0))
+    assert r["iters"] == 1 and np.allclose(r["x"], np.arange(1.0, 5.0), rtol=1e-15)
+    A = csr_from_dense([[2.0, 1.0], [0.0, 2.0]])
+    r = oracle.gmres(A, np.array([3.0, 2.0]), tol=1e-12)
+    assert r["iters"] <= 2
+    np.testing.assert_allclose(r["x"], [1.0, 1.0], rtol=1e-12)
+    r = oracle.gmres(A, np.zeros(2))
+    assert r["iters"] == 0 and r["status"] == oracle.OK
+
+
+def test_gmres_minimises_residual_over_krylov_space():
+    """Brute force: after k steps (no restart, M = I, x0 = 0) GMRES returns
+    argmin_{x in K_k(A, f)} |f - A x|, computed here from an explicit Krylov
+    basis with numpy least squares; the residual estimate is non-increasing."""
+    rng = np.random.default_rng(11)
+    n = 24
+    D = np.eye(n) * 4 + rng.standard_normal((n, n)) * 0.4
+    A = csr_from_dense(D)
+    f = rng.standard_normal(n)
+    for k in range(1, 9):
+        r = oracle.gmres(A, f, tol=0.0, maxiter=k, m=50, history=True)
+        K = np.empty((n, k))
+        v = f / np.linalg.norm(f)
+        for j in range(k):  # orthonormal Krylov basis (numpy QR for stability)
+            K[:, j] = v
+            Q, _ = np.linalg.qr(K[:, :j + 1])
+            v = D @ Q[:, j]
+        Q, _ = np.linalg.qr(K)
+        c, *_ = np.linalg.lstsq(D @ Q, f, rcond=None)
+        np.testing.assert_allclose(r["x"], Q @ c, rtol=1e-9, atol=1e-12)
+        h = r["history"]
+        assert np.all(np.diff(h) <= 1e-12 * h[0])
+
+
+def test_gmres_full_terminates_and_restart():
+    """Without restart GMRES terminates in <= n steps (exact arithmetic bound);
+    with restarts it still converges on a diagonally dominant system; the
+    AMG-preconditioned solve of a small conv-diff system matches the dense solve."""
+    rng = np.random.default_rng(5)
+    n = 12
+    D = np.eye(n) * 3 + rng.standard_normal((n, n)) * 0.3
+    A = csr_from_dense(D)
+    f = rng.standard_normal(n)
+    r = oracle.gmres(A, f, tol=1e-12, maxiter=100, m=100)
+    assert r["iters"] <= n and r["status"] == oracle.OK
+    np.testing.assert_allclose(r["x"], np.linalg.solve(D, f), rtol=1e-10)
+    r = oracle.gmres(A, f, tol=1e-10, maxiter=200, m=3)
+    assert r["status"] == oracle.OK and r["iters"] > 3
+    np.testing.assert_allclose(r["x"], np.linalg.solve(D, f), rtol=1e-8)
+    p, c, v, f = synth.convdiff3d(10)
+    A = oracle.Csr(p, c, v)
+    h = oracle.Hierarchy(A, coarse_enough=50, relax="damped_jacobi")
+    r = oracle.gmres(A, f, hier=h, tol=1e-10, m=30)
+    assert r["status"] == oracle.OK and r["rel_resid"] <= 1e-10
+    np.testing.assert_allclose(r["x"], np.linalg.solve(A.to_dense(), f), rtol=1e-8)
+    assert r["vcycles"] >= r["iters"] + 1
