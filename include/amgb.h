@@ -72,13 +72,14 @@ typedef struct {
     int64_t coarse_enough;  /* stop coarsening at <= this many rows [3000] */
     int32_t max_levels;     /* [30] */
     int64_t dense_max;      /* error if the coarsest level is larger [20000] */
-    int32_t solver;         /* "solver.type": 0 cg [0], 1 bicgstab */
+    int32_t solver;         /* "solver.type": 0 cg [0], 1 bicgstab, 2 gmres (restarted, right-preconditioned) */
     int32_t device;         /* CUDA device ordinal [0]; -1 = host-only handle (setup + export) */
     int32_t use_graph;      /* 1: replay Krylov iterations as a CUDA graph [1] */
     int32_t precision;      /* 0: fp64 throughout [0]; 1: mixed -- the V-cycle reads fp32 copies of
                                the hierarchy values (arithmetic and vectors stay fp64; the Krylov
                                method and its A stay fp64).  SURVEY §8f rank 2; value types
                                "double or float", PAPER.md:186-191 */
+    int32_t gmres_m;        /* GMRES restart length m in [1, 64] [30] ("solver.M") */
 } amg_params;
 
 /* Per-level statistics (amg_level_info). */

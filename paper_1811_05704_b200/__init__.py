@@ -59,6 +59,7 @@ class AmgParams(C.Structure):
         ("device", C.c_int32),
         ("use_graph", C.c_int32),
         ("precision", C.c_int32),
+        ("gmres_m", C.c_int32),
     ]
 
 
@@ -138,7 +139,7 @@ SYMBOLS = ("amg_params_default", "amg_setup", "amg_solve", "amg_solve_host", "am
 
 RELAX = {"spai0": 0, "damped_jacobi": 1, "chebyshev": 2}
 COARSENING = {"smoothed_aggregation": 0, "aggregation": 1}
-SOLVER = {"cg": 0, "bicgstab": 1}
+SOLVER = {"cg": 0, "bicgstab": 1, "gmres": 2}
 
 # dotted keys (Listing 2 style) -> amg_params field
 PARAM_KEYS = {
@@ -160,6 +161,7 @@ PARAM_KEYS = {
     "device": "device",
     "use_graph": "use_graph",
     "precision": "precision",
+    "solver.M": "gmres_m",
 }
 PRECISION = {"double": 0, "mixed": 1}
 _ENUMS = {"relax": RELAX, "coarsening": COARSENING, "solver": SOLVER, "precision": PRECISION}

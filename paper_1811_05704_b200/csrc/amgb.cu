@@ -30,6 +30,7 @@
 #include "batched.cuh"
 #include "comm.hpp"
 #include "dist.hpp"
+#include "gmres.cuh"
 #include "kernels.cuh"
 #include "ops.cuh"
 #include "setup.hpp"
@@ -256,6 +257,7 @@ struct Handle {
     }
     ~Handle() {
         free_batch();
+        free_gmres();
         if (graph) cudaGraphExecDestroy(graph);
         for (cudaEvent_t e : ev_all) cudaEventDestroy(e);
         for (void* p : allocs) cudaFree(p);
@@ -306,6 +308,26 @@ struct Handle {
         std::vector<Rec> rec;
         int64_t graph_kernels = 0;
     } batch;
+    // ---- GMRES(m) buffers (single part)
+    struct Gmres {
+        int m = 0;
+        double *V = nullptr, *w = nullptr, *z = nullptr, *u = nullptr, *r = nullptr, *partial = nullptr;
+        int64_t nchunks = 0, chunk = 0;
+        KStateG* ks = nullptr;
+        KStateG* ks_host = nullptr;
+        std::vector<void*> mem;
+        cudaGraphExec_t graph = nullptr;
+        const double* graph_x = nullptr;
+        const double* graph_f = nullptr;
+        std::vector<Rec> rec;
+        int64_t graph_kernels = 0;
+    } gm;
+    void free_gmres() {
+        if (gm.graph) cudaGraphExecDestroy(gm.graph);
+        for (void* p : gm.mem) cudaFree(p);
+        if (gm.ks_host) cudaFreeHost(gm.ks_host);
+        gm = Gmres{};
+    }
     void free_batch() {
         if (batch.graph) cudaGraphExecDestroy(batch.graph);
         for (void* p : batch.mem) cudaFree(p);
@@ -602,6 +624,9 @@ struct Handle {
     amg_status solve_batched(int k, const double* F, int64_t ldf, double* X, int64_t ldx, double tol, int32_t maxiter,
                              int32_t* iters, double* rel);
     void cg_iteration(int parity);
+    void gmres_step(int j);
+    void gmres_cycle_end(const double* f, double* x);
+    amg_status solve_gmres(const double* f, double* x, double tol, int32_t maxiter, int32_t* iters, double* rel);
     void bicgstab_iteration();
     amg_status solve(const double* f, double* x, double tol, int32_t maxiter, int32_t* iters, double* rel);
     void precond(const double* r, double* z);
@@ -1314,6 +1339,201 @@ amg_status Handle::solve_batched(int k, const double* F, int64_t ldf, double* X,
     return st;
 }
 
+// ============================================================ GMRES(m)
+template <class Fin>
+struct VNorm2T {  // (a, a) with a chosen finalizer
+    static constexpr int NDOT = 1, STREAMS = 1;
+    const double* a;
+    Fin fin;
+    __device__ void prepare() {}
+    __device__ void elem(int64_t i, double* d) const { d[0] += a[i] * a[i]; }
+};
+struct FinTrueResG {
+    KStateG* ks;
+    __device__ void operator()(const double* t) const { ks->beta = sqrt(t[0]); }
+};
+
+// Arnoldi step j of the current cycle (gated on stop_step): z = M v_j, w = A z,
+// two classical Gram-Schmidt passes against v_0..v_j, |w|, Givens, v_{j+1}.
+void Handle::gmres_step(int j) {
+    Part& p = parts[0];
+    const int64_t n = p.lv[0].n;
+    const int32_t* gate = &gm.ks->stop_step;
+    GSel g = [gate](Part&) { return gate; };
+    double* vj = gm.V + (int64_t)j * n;
+    vcycle(0, [vj](Part&) { return (const double*)vj; }, [this](Part&) { return gm.z; }, g, false);
+    rows(p, p.lv[0].A, OpSpmv{gm.z, gm.w}, gate, "gmres w = A z");
+    const int J = j + 1;
+    for (int pass = 0; pass < 2; ++pass) {
+        launch(AMG_PROF_VECTOR, 8.0 * (J + 1) * n, "gmres dots", [&] {
+            gmres_dots<<<dim3(J, (unsigned)gm.nchunks), kBlock, 0, stream>>>(gm.w, gm.V, n, gm.chunk, gm.partial, gate);
+            gmres_dots_fin<<<1, 96, 0, stream>>>(gm.partial, J, (int)gm.nchunks, gm.ks, pass, gate);
+        });
+        if (pass == 0) {
+            launch(AMG_PROF_VECTOR, 8.0 * (J + 2) * n, "gmres axpy", [&] {
+                vec_kernel<VGmresAxpy<0>><<<grid_for(n), kBlock, 0, stream>>>(
+                    n, VGmresAxpy<0>{gm.w, gm.V, n, J, gm.ks, FinGmresStep{gm.ks, j}}, gate, p.red);
+            });
+        } else {
+            launch(AMG_PROF_VECTOR, 8.0 * (J + 2) * n, "gmres axpy+norm", [&] {
+                vec_kernel<VGmresAxpy<1>><<<grid_for(n), kBlock, 0, stream>>>(
+                    n, VGmresAxpy<1>{gm.w, gm.V, n, J, gm.ks, FinGmresStep{gm.ks, j}}, gate, p.red);
+            });
+        }
+    }
+    if (j + 1 <= gm.m) vec(p, n, VGmresScale{gm.w, gm.V + (int64_t)(j + 1) * n, &gm.ks->hn, {}}, gate, "gmres v");
+}
+
+// End of a restart cycle (gated on done): y = H^-1 g, x += M (V y), r = f - A x,
+// restart test, v_0 = r / |r|.
+void Handle::gmres_cycle_end(const double* f, double* x) {
+    Part& p = parts[0];
+    const int64_t n = p.lv[0].n;
+    const int32_t* gate = &gm.ks->done;
+    GSel g = [gate](Part&) { return gate; };
+    launch(AMG_PROF_VECTOR, 0, "gmres y", [&] { gmres_solve_y<<<1, 1, 0, stream>>>(gm.ks, gate); });
+    launch(AMG_PROF_VECTOR, 8.0 * (gm.m + 1) * n, "gmres u = V y", [&] {
+        vec_kernel<VGmresCombine><<<grid_for(n), kBlock, 0, stream>>>(n, VGmresCombine{gm.u, gm.V, n, gm.ks, {}},
+                                                                       gate, p.red);
+    });
+    vcycle(0, [this](Part&) { return (const double*)gm.u; }, [this](Part&) { return gm.z; }, g, false);
+    vec(p, n, VAdd{x, gm.z, {}}, gate, "gmres x += z");
+    rows(p, p.lv[0].A, OpResidual<1, FinGmresRestart>{x, f, gm.r, FinGmresRestart{gm.ks}}, gate, "gmres r");
+    vec(p, n, VGmresScale{gm.r, gm.V, &gm.ks->hn, {}}, gate, "gmres v0");
+}
+
+amg_status Handle::solve_gmres(const double* f, double* x, double tol, int32_t maxiter, int32_t* iters, double* rel) {
+    Part& p = parts[0];
+    const int64_t n = p.lv[0].n;
+    const int m = prm.gmres_m;
+    if (gm.m != m) {
+        free_gmres();
+        gm.m = m;
+        auto alloc = [&](int64_t cnt) {
+            void* q = nullptr;
+            ck(cudaMalloc(&q, std::max<int64_t>(cnt, 1) * sizeof(double)), "cudaMalloc (gmres)");
+            gm.mem.push_back(q);
+            return static_cast<double*>(q);
+        };
+        gm.V = alloc((int64_t)(m + 1) * n);
+        gm.w = alloc(n);
+        gm.z = alloc(n);
+        gm.u = alloc(n);
+        gm.r = alloc(n);
+        gm.chunk = std::max<int64_t>(4096, (n + 255) / 256);
+        gm.nchunks = (n + gm.chunk - 1) / gm.chunk;
+        gm.partial = alloc((int64_t)(m + 1) * gm.nchunks);
+        void* q = nullptr;
+        ck(cudaMalloc(&q, sizeof(KStateG)), "cudaMalloc");
+        gm.mem.push_back(q);
+        gm.ks = static_cast<KStateG*>(q);
+        ck(cudaMallocHost(&gm.ks_host, sizeof(KStateG)), "cudaMallocHost");
+    }
+    const int64_t launches0 = launches;
+    collect(rec_direct, 0, true);
+    alg_bytes = 0;
+    std::fill(acc_ms, acc_ms + 8, 0.0);
+    std::fill(acc_bytes, acc_bytes + 8, 0.0);
+    std::fill(acc_launches, acc_launches + 8, 0);
+    cur_iter = -1;
+    ck(cudaEventRecord(ev0, stream), "event");
+    KStateG* kh = gm.ks_host;
+    std::memset(kh, 0, sizeof(KStateG));
+    kh->m = m;
+    kh->maxiter = maxiter;
+    ck(cudaMemcpyAsync(gm.ks, kh, sizeof(KStateG), cudaMemcpyHostToDevice, stream), "ks init");
+    vec(p, n, VNorm2T<FinGmresNorm>{f, FinGmresNorm{gm.ks, tol}}, nullptr, "norm f");
+    rows(p, p.lv[0].A, OpResidual<1, FinGmresRestart>{x, f, gm.r, FinGmresRestart{gm.ks}}, nullptr, "gmres r0");
+    vec(p, n, VGmresScale{gm.r, gm.V, &gm.ks->hn, {}}, &gm.ks->done, "gmres v0");
+    ck(cudaMemcpyAsync(kh, gm.ks, sizeof(KStateG), cudaMemcpyDeviceToHost, stream), "ks read");
+    ck(cudaStreamSynchronize(stream), "sync");
+    collect(rec_direct, 0, true);
+    if (kh->nf == 0.0) {  // zero right-hand side: x = 0
+        ck(cudaMemsetAsync(x, 0, n * sizeof(double), stream), "memset");
+        ck(cudaStreamSynchronize(stream), "sync");
+        *iters = 0;
+        *rel = 0.0;
+        stats = amg_solve_stats{};
+        stats.kernel_launches = launches - launches0;
+        return AMG_OK;
+    }
+    int cycles = 0;
+    const bool use_graph = prm.use_graph && !sync_debug;
+    while (!kh->done) {
+        if (use_graph) {  // one restart cycle (m gated steps + the update) per graph launch
+            if (!gm.graph || gm.graph_x != x || gm.graph_f != f) {
+                if (gm.graph) cudaGraphExecDestroy(gm.graph);
+                gm.graph = nullptr;
+                cudaGraph_t g;
+                const int64_t before = launches;
+                const int saved_mask = prof_mask;
+                prof_mask = 0;
+                std::vector<Rec> saved;
+                saved.swap(rec_graph);
+                ck(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "capture");
+                capturing = true;
+                try {
+                    for (int j = 0; j < m; ++j) gmres_step(j);
+                    gmres_cycle_end(f, x);
+                } catch (...) {
+                    capturing = false;
+                    prof_mask = saved_mask;
+                    cudaStreamEndCapture(stream, &g);
+                    rec_graph.swap(saved);
+                    throw;
+                }
+                capturing = false;
+                prof_mask = saved_mask;
+                ck(cudaStreamEndCapture(stream, &g), "end capture");
+                gm.rec.swap(rec_graph);
+                rec_graph.swap(saved);
+                gm.graph_kernels = launches - before;
+                launches = before;
+                ck(cudaGraphInstantiate(&gm.graph, g, 0), "instantiate");
+                cudaGraphDestroy(g);
+                gm.graph_x = x;
+                gm.graph_f = f;
+            }
+            ck(cudaGraphLaunch(gm.graph, stream), "graph launch");
+            launches += gm.graph_kernels;
+            ck(cudaMemcpyAsync(kh, gm.ks, sizeof(KStateG), cudaMemcpyDeviceToHost, stream), "ks read");
+            ck(cudaStreamSynchronize(stream), "sync");
+            collect(gm.rec, 0, false);  // bytes of the whole cycle graph (gated steps included)
+        } else {
+            for (int j = 0; j < m; ++j) gmres_step(j);
+            gmres_cycle_end(f, x);
+            ck(cudaMemcpyAsync(kh, gm.ks, sizeof(KStateG), cudaMemcpyDeviceToHost, stream), "ks read");
+            ck(cudaStreamSynchronize(stream), "sync");
+            collect(rec_direct, 0, true);
+        }
+        ++cycles;
+    }
+    rows(p, p.lv[0].A, OpResidual<1, FinTrueResG>{x, f, gm.r, FinTrueResG{gm.ks}}, nullptr, "true res");
+    ck(cudaEventRecord(ev1, stream), "event");
+    ck(cudaMemcpyAsync(kh, gm.ks, sizeof(KStateG), cudaMemcpyDeviceToHost, stream), "ks read");
+    ck(cudaStreamSynchronize(stream), "sync");
+    collect(rec_direct, 0, true);
+    *iters = kh->k;
+    *rel = kh->beta / kh->nf;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev0, ev1);
+    stats = amg_solve_stats{};
+    stats.iters = kh->k;
+    stats.vcycles = kh->k + cycles;
+    stats.kernel_launches = launches - launches0;
+    stats.solve_ms = ms;
+    stats.rel_resid = *rel;
+    stats.alg_bytes = alg_bytes;
+    if (kh->status == AMG_BREAKDOWN) {
+        g_err = "GMRES breakdown: singular Hessenberg";
+        stats.status = AMG_BREAKDOWN;
+        return AMG_BREAKDOWN;
+    }
+    const amg_status st = *rel <= tol ? AMG_OK : AMG_NOT_CONVERGED;
+    stats.status = st;
+    return st;
+}
+
 // z = M r for every part (r, z: device; global vectors in virtual mode).
 void Handle::precond(const double* r, double* z) {
     GSel nogate = [](Part&) { return (const int32_t*)nullptr; };
@@ -1631,6 +1851,7 @@ void amg_params_default(amg_params* p) {
     p->device = 0;
     p->use_graph = 1;
     p->precision = 0;
+    p->gmres_m = 30;
 }
 
 const char* amg_last_error(void) { return amgb::g_err.c_str(); }
@@ -1644,7 +1865,9 @@ static amg_status check_params(const amg_params& p) {
     if (p.struct_size != sizeof(amg_params)) return set_error(AMG_E_INVALID_ARG, "amg_params: struct_size mismatch");
     if (p.coarsening < 0 || p.coarsening > 1) return set_error(AMG_E_INVALID_ARG, "coarsening must be 0 or 1");
     if (p.relax < 0 || p.relax > 2) return set_error(AMG_E_INVALID_ARG, "relax must be 0, 1 or 2");
-    if (p.solver < 0 || p.solver > 1) return set_error(AMG_E_INVALID_ARG, "solver must be 0 or 1");
+    if (p.solver < 0 || p.solver > 2) return set_error(AMG_E_INVALID_ARG, "solver must be 0 (cg), 1 (bicgstab) or 2 (gmres)");
+    if (p.solver == 2 && (p.gmres_m < 1 || p.gmres_m > amgb::kGmresMaxM))
+        return set_error(AMG_E_INVALID_ARG, "gmres_m in [1, 64]");
     if (p.npre < 0 || p.npost < 0 || p.npre + p.npost < 1)
         return set_error(AMG_E_INVALID_ARG, "npre, npost >= 0 and npre + npost >= 1");
     if (p.relax == 2 && (p.cheb_degree < 1 || !(p.cheb_lower > 0 && p.cheb_lower < 1)))
@@ -1795,6 +2018,10 @@ amg_status amg_solve(amg_handle h, const double* f, double* x, double tol, int32
     if (!(tol >= 0) || maxiter < 0) return set_error(AMG_E_INVALID_ARG, "tol >= 0, maxiter >= 0");
     try {
         ck(cudaSetDevice(h->h->device), "cudaSetDevice");
+        if (h->h->prm.solver == 2) {
+            if (h->h->distributed()) return set_error(AMG_E_INVALID_ARG, "GMRES: single-GPU handles only");
+            return h->h->solve_gmres(f, x, tol, maxiter, iters, rel);
+        }
         return h->h->solve(f, x, tol, maxiter, iters, rel);
     } catch (const amgb::CudaError& e) {
         cudaGetLastError();
@@ -1819,7 +2046,8 @@ amg_status amg_solve_host(amg_handle h, const double* f, const double* x0, doubl
             ck(cudaMemcpyAsync(H.hx, x0, n * sizeof(double), cudaMemcpyHostToDevice, H.stream), "H2D x0");
         else
             ck(cudaMemsetAsync(H.hx, 0, n * sizeof(double), H.stream), "zero x0");
-        amg_status st = H.solve(H.hf, H.hx, tol, maxiter, iters, rel);
+        amg_status st = H.prm.solver == 2 && !H.distributed() ? H.solve_gmres(H.hf, H.hx, tol, maxiter, iters, rel)
+                                                               : H.solve(H.hf, H.hx, tol, maxiter, iters, rel);
         ck(cudaMemcpyAsync(x, H.hx, n * sizeof(double), cudaMemcpyDeviceToHost, H.stream), "D2H x");
         ck(cudaStreamSynchronize(H.stream), "sync");
         return st;
