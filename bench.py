@@ -148,6 +148,11 @@ def workload_name(args, cfg):
     return w + ("_mixed" if getattr(args, "precision", "double") == "mixed" else "")
 
 
+def oracle_solver(cfg):
+    import oracle
+    return {"cg": oracle.cg, "bicgstab": oracle.bicgstab, "gmres": oracle.gmres}[cfg["solver"]]
+
+
 def cpu_baseline_full_solve(ptr, col, val, f, cfg, tol, maxiter):
     """The oracle as it stands on the host cores: untimed setup, then one full
     solve of the same system (timed).  Also returns its iterations/solution for
@@ -157,9 +162,8 @@ def cpu_baseline_full_solve(ptr, col, val, f, cfg, tol, maxiter):
     t0 = time.perf_counter()
     hier = oracle.Hierarchy(A, relax=cfg["relax"])
     t_setup = time.perf_counter() - t0
-    fn = oracle.bicgstab if cfg["solver"] == "bicgstab" else oracle.cg
     t0 = time.perf_counter()
-    res = fn(A, f, tol=tol, maxiter=maxiter, hier=hier)
+    res = oracle_solver(cfg)(A, f, tol=tol, maxiter=maxiter, hier=hier)
     t_solve = time.perf_counter() - t0
     vcyc = res.get("vcycles", res["iters"])
     return dict(setup_s=t_setup, solve_s=t_solve, iters=res["iters"], vcycles=vcyc, x=res["x"],
@@ -177,7 +181,7 @@ def run_reference(args, cfg):
     t0 = time.perf_counter()
     hier = oracle.Hierarchy(A, relax=cfg["relax"])
     t_setup = time.perf_counter() - t0
-    fn = oracle.bicgstab if cfg["solver"] == "bicgstab" else oracle.cg
+    fn = oracle_solver(cfg)
     x = np.zeros(len(f))
     # one step = one Krylov iteration (maxiter = 1, restarted from the current x)
     for _ in range(args.warmup):

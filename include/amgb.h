@@ -213,9 +213,9 @@ amg_status amg_level_op(amg_handle h, int32_t level, int32_t op, const double *x
  * Results equal the single-GPU solve up to the order of the dot-product sums
  * (row sums keep the global column order). */
 typedef struct {
-    int32_t nranks;
+    int32_t nranks;         /* ranks of the partition */
     int32_t rank;           /* >= 0: NCCL rank of this process; -1: all ranks here */
-    int64_t gather_below;   /* replicate levels with fewer rows [0 -> 131072] */
+    int64_t gather_below;   /* replicate levels with fewer rows [0 -> 16384 * nranks] */
     uint8_t nccl_id[128];   /* ncclUniqueId from amg_nccl_unique_id (rank >= 0) */
 } amg_dist;
 

@@ -428,7 +428,7 @@ def nccl_selftest(device: int = 0) -> None:
     _check(_lib.amg_nccl_selftest(device), "amg_nccl_selftest")
 
 
-def setup_dist(ptr, col, val, nranks: int, rank: int = -1, gather_below: int = 1 << 17,
+def setup_dist(ptr, col, val, nranks: int, rank: int = -1, gather_below: int = 0,
                nccl_id: bytes | None = None, params: dict | None = None, **kw) -> Hierarchy:
     """amg_setup_dist: row-partitioned hierarchy (rank = -1: every rank in this
     process on one GPU; rank >= 0: one NCCL rank per process)."""

@@ -1473,9 +1473,14 @@ amg_status Handle::solve_gmres(const double* f, double* x, double tol, int32_t m
                 ck(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "capture");
                 capturing = true;
                 try {
-                    for (int j = 0; j < m; ++j) gmres_step(j);
+                    for (int j = 0; j < m; ++j) {
+                        cur_iter = j;  // step tag: only executed steps are accounted
+                        gmres_step(j);
+                    }
+                    cur_iter = -1;
                     gmres_cycle_end(f, x);
                 } catch (...) {
+                    cur_iter = -1;
                     capturing = false;
                     prof_mask = saved_mask;
                     cudaStreamEndCapture(stream, &g);
@@ -1494,11 +1499,12 @@ amg_status Handle::solve_gmres(const double* f, double* x, double tol, int32_t m
                 gm.graph_x = x;
                 gm.graph_f = f;
             }
+            const int k_before = kh->k;
             ck(cudaGraphLaunch(gm.graph, stream), "graph launch");
             launches += gm.graph_kernels;
             ck(cudaMemcpyAsync(kh, gm.ks, sizeof(KStateG), cudaMemcpyDeviceToHost, stream), "ks read");
             ck(cudaStreamSynchronize(stream), "sync");
-            collect(gm.rec, 0, false);  // bytes of the whole cycle graph (gated steps included)
+            collect(gm.rec, kh->k - k_before, false);  // steps that ran + the cycle end
         } else {
             for (int j = 0; j < m; ++j) gmres_step(j);
             gmres_cycle_end(f, x);
@@ -1999,8 +2005,10 @@ amg_status amg_setup_dist(int64_t n, const int64_t* ptr, const int32_t* col, con
         for (int i = 0; i < 128; ++i) zero &= d->nccl_id[i] == 0;
         if (zero) return set_error(AMG_E_INVALID_ARG, "nccl_id not set (amg_nccl_unique_id on rank 0, then broadcast)");
     }
-    return setup_impl(n, ptr, col, val, prm, d->nranks, d->rank, d->gather_below > 0 ? d->gather_below : (1 << 17),
-                      d->nccl_id, out);
+    // default: replicate a level once it has fewer than 16384 rows per rank (below
+    // that, a distributed pass is dominated by its halo-exchange latency)
+    const int64_t gb = d->gather_below > 0 ? d->gather_below : (int64_t)16384 * std::max(1, d->nranks);
+    return setup_impl(n, ptr, col, val, prm, d->nranks, d->rank, gb, d->nccl_id, out);
 }
 
 void amg_destroy(amg_handle h) { delete h; }
