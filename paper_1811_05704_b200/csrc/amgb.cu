@@ -268,6 +268,29 @@ struct Handle {
         if (nccl && Nccl::get().commDestroy) Nccl::get().commDestroy(nccl);
     }
 
+    // Kernels that start with pdl_wait() are launched with programmatic stream
+    // serialization (AMGB_PDL=0 disables it): inside the iteration graph they
+    // become programmatic edges, so a kernel's launch overlaps the tail of the
+    // previous one.
+    bool pdl = [] {
+        const char* e = std::getenv("AMGB_PDL");
+        return !(e && std::string(e) == "0");
+    }();
+    template <class... KArgs, class... Args>
+    void klaunch(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, Args&&... args) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = g;
+        cfg.blockDim = b;
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        ck(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...), "cudaLaunchKernelEx");
+    }
+
     int grid_for(int64_t n) const {
         const int64_t b = (n + kBlock - 1) / kBlock;
         return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)num_sms * 8));
@@ -424,17 +447,17 @@ struct Handle {
         const int g = (int)std::max<int64_t>(
             1, std::min<int64_t>((M.nrows + kBlock - 1) / kBlock, (int64_t)num_sms * minb_of<Op>(PIPE ? 4 : 6)));
         if (stream_loads)
-            sell_rows<U, true, PIPE, Op, F32><<<g, kBlock, 0, stream>>>(M, op, gate, red);
+            klaunch(sell_rows<U, true, PIPE, Op, F32>, g, kBlock, 0, M, op, gate, red);
         else
-            sell_rows<U, false, PIPE, Op, F32><<<g, kBlock, 0, stream>>>(M, op, gate, red);
+            klaunch(sell_rows<U, false, PIPE, Op, F32>, g, kBlock, 0, M, op, gate, red);
     }
     template <int G, bool F32, class Op>
     void rows_csr(const CsrDev& M, const Op& op, const int32_t* gate, const Red& red, bool stream_loads) {
         const int g = (int)std::max<int64_t>(1, std::min<int64_t>(M.nblocks, (int64_t)num_sms * 8));
         if (stream_loads)
-            csr_rows<G, true, Op, F32><<<g, kBlock, 0, stream>>>(M, op, gate, red);
+            klaunch(csr_rows<G, true, Op, F32>, g, kBlock, 0, M, op, gate, red);
         else
-            csr_rows<G, false, Op, F32><<<g, kBlock, 0, stream>>>(M, op, gate, red);
+            klaunch(csr_rows<G, false, Op, F32>, g, kBlock, 0, M, op, gate, red);
     }
     template <int T, bool STREAM, bool F32, class Op>
     void rows_tma_impl(const SellTma& M, const Op& op, const int32_t* gate, const Red& red) {
@@ -447,7 +470,7 @@ struct Handle {
         }
         const int g =
             (int)std::max<int64_t>(1, std::min<int64_t>(M.ntiles, (int64_t)num_sms * minb_of<Op>(kTmaBlocksPerSM)));
-        kern<<<g, kTmaThreads, smem, stream>>>(M, op, gate, red);
+        klaunch(kern, g, kTmaThreads, smem, M, op, gate, red);
     }
     template <int T, bool F32, class Op>
     void rows_tma(const SellTma& M, const Op& op, const int32_t* gate, const Red& red, bool stream_loads) {
@@ -509,7 +532,7 @@ struct Handle {
             return;
         }
         launch(AMG_PROF_VECTOR, 8.0 * n * Op::STREAMS, what,
-               [&] { vec_kernel<Op><<<grid_for(n), kBlock, 0, stream>>>(n, op, gate, p.red); });
+               [&] { klaunch(vec_kernel<Op>, grid_for(n), kBlock, 0, n, op, gate, p.red); });
     }
 
     // ------------------------------------------------------------ collectives
@@ -646,7 +669,7 @@ bool Handle::vcycle(int l, const CSel& fsel, const Sel& osel, const GSel& gate, 
             double* out = osel(p);
             const int32_t* gt = gate(p);
             launch(AMG_PROF_COARSE_SOLVE, 8.0 * L.n * L.n + 16.0 * L.n, "coarse gemv",
-                   [&] { dense_gemv<<<g, kBlock, 0, stream>>>(L.n, p.coarse_inv, f, out, gt); });
+                   [&] { klaunch(dense_gemv, g, kBlock, 0, L.n, (const double*)p.coarse_inv, f, out, gt); });
         }
         return false;
     }

@@ -181,6 +181,14 @@ struct NoFin {
     __device__ void operator()(const double*) const {}
 };
 
+// Programmatic dependent launch (sm_90+): a kernel launched with the
+// programmatic-stream-serialization attribute may start while its predecessor
+// finishes; pdl_wait() blocks until the predecessor grid has completed and its
+// writes are visible (a no-op for normal launches), pdl_trigger() lets the
+// successor start launching once every block of this grid has triggered.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ bool gated(const int32_t* gate) {
     return gate != nullptr && *reinterpret_cast<const volatile int32_t*>(gate) != 0;
 }
@@ -201,6 +209,7 @@ template <int U1, bool STREAM, bool PIPE, class Op, bool F32 = false>
 __global__ void __launch_bounds__(kBlock, minb_of<Op>(PIPE ? 4 : 6)) sell_rows(Sell A, Op op, const int32_t* gate,
                                                                                  Red red) {
     constexpr int U = unroll_of<Op>(U1);
+    pdl_wait();
     if (gated(gate)) return;
     op.prepare();
     constexpr int ND = Op::NDOT > 0 ? Op::NDOT : 1;
@@ -261,6 +270,7 @@ __global__ void __launch_bounds__(kBlock, minb_of<Op>(PIPE ? 4 : 6)) sell_rows(S
         if constexpr (cols_of<Op>() > 1) rr = op.load(row);
         op.row(row, sum, rr, dots);
     }
+    pdl_trigger();
     if constexpr (Op::NDOT > 0) grid_reduce<Op::NDOT>(dots, red, op.fin);
 }
 
@@ -334,6 +344,7 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sel
     using VT = std::conditional_t<F32, float, double>;
     constexpr int VB = (int)sizeof(VT);
     constexpr int UN = unroll_of<Op>(8);
+    pdl_wait();
     if (gated(gate)) return;
     op.prepare();
     constexpr int C = 32 / T;  // slice height
@@ -429,6 +440,7 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sel
             if (pt == 0 && has_row) op.row(row, sum, rr, dots);
         }
     }
+    pdl_trigger();
     if constexpr (Op::NDOT > 0) grid_reduce<Op::NDOT>(dots, red, op.fin);
 }
 
@@ -458,6 +470,7 @@ struct CsrDev {
 
 template <int G, bool STREAM, class Op, bool F32 = false>
 __global__ void __launch_bounds__(kBlock) csr_rows(CsrDev A, Op op, const int32_t* gate, Red red) {
+    pdl_wait();
     if (gated(gate)) return;
     op.prepare();
     __shared__ double prod[kEnt];
@@ -482,6 +495,7 @@ __global__ void __launch_bounds__(kBlock) csr_rows(CsrDev A, Op op, const int32_
             }
             if (lig == 0) op.row(r, s, op.load(r), dots);
         }
+        pdl_trigger();
         if constexpr (Op::NDOT > 0) grid_reduce<Op::NDOT>(dots, red, op.fin);
         return;
     } else {
@@ -534,12 +548,14 @@ __global__ void __launch_bounds__(kBlock) csr_rows(CsrDev A, Op op, const int32_
         }
     }
     }  // single right-hand side
+    pdl_trigger();
     if constexpr (Op::NDOT > 0) grid_reduce<Op::NDOT>(dots, red, op.fin);
 }
 
 // ----------------------------------------------------------------- vector kernel
 template <class Op>
 __global__ void __launch_bounds__(kBlock) vec_kernel(int64_t n, Op op, const int32_t* gate, Red red) {
+    pdl_wait();
     if (gated(gate)) return;
     op.prepare();
     double dots[Op::NDOT > 0 ? Op::NDOT : 1];
@@ -547,6 +563,7 @@ __global__ void __launch_bounds__(kBlock) vec_kernel(int64_t n, Op op, const int
     for (int k = 0; k < (Op::NDOT > 0 ? Op::NDOT : 1); ++k) dots[k] = 0.0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) op.elem(i, dots);
+    pdl_trigger();
     if constexpr (Op::NDOT > 0) grid_reduce<Op::NDOT>(dots, red, op.fin);
 }
 

@@ -16,6 +16,7 @@ namespace amgb {
 __global__ void __launch_bounds__(kBlock) dense_gemv(int64_t n, const double* __restrict__ M,
                                                      const double* __restrict__ x, double* __restrict__ y,
                                                      const int32_t* gate) {
+    pdl_wait();
     if (gated(gate)) return;
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
