@@ -268,13 +268,13 @@ struct Handle {
         if (nccl && Nccl::get().commDestroy) Nccl::get().commDestroy(nccl);
     }
 
-    // Kernels that start with pdl_wait() are launched with programmatic stream
-    // serialization (AMGB_PDL=0 disables it): inside the iteration graph they
-    // become programmatic edges, so a kernel's launch overlaps the tail of the
-    // previous one.
+    // Kernels that start with pdl_wait() can be launched with programmatic stream
+    // serialization (AMGB_PDL=1), which lets a launch overlap the tail of the
+    // previous kernel.  Off by default: measured on the 256^3 solve it made the
+    // iteration graph 38% SLOWER (62.5 vs 45.2 ms), so plain stream order it is.
     bool pdl = [] {
         const char* e = std::getenv("AMGB_PDL");
-        return !(e && std::string(e) == "0");
+        return e && std::string(e) == "1";
     }();
     template <class... KArgs, class... Args>
     void klaunch(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, Args&&... args) {
