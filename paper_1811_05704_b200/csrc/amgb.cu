@@ -195,7 +195,7 @@ struct Part {
     KState* ks = nullptr;
     Red red;
     // Krylov vectors (level-0 local length + ghosts where gathered)
-    double *r = nullptr, *z = nullptr, *pa = nullptr, *pb = nullptr, *q = nullptr, *xw = nullptr;
+    double *r = nullptr, *r2 = nullptr, *z = nullptr, *pa = nullptr, *pb = nullptr, *q = nullptr, *xw = nullptr;
     double *rhat = nullptr, *v = nullptr, *s = nullptr, *sh = nullptr, *ph = nullptr, *tv = nullptr;
     const double* fcur = nullptr;  // right-hand side of the current solve (local slice)
     double* xcur = nullptr;        // solution vector of the current solve (with ghosts if needed)
@@ -231,6 +231,7 @@ struct Handle {
     int graph_prof_mask = 0;
     int64_t graph_kernels = 0;
     bool graph_loop = false;  // the graph runs the whole loop (conditional WHILE node)
+    bool graph_fused = false; // the graph holds fused CG iterations
     // accounting
     int64_t launches = 0;
     amg_solve_stats stats{};
@@ -637,6 +638,11 @@ struct Handle {
     }
 
     bool vcycle(int l, const CSel& f, const Sel& out, const GSel& gate, bool with_rho);
+    // fused CG: the level-0 res0 of the next V-cycle also applies r -= alpha q
+    const double* fuse_r_old = nullptr;
+    double* fuse_r_new = nullptr;
+    bool cg_fused = false;
+    void cg_iteration_fused(int parity);
     template <int K>
     void ensure_batch();
     template <int K>
@@ -701,7 +707,12 @@ bool Handle::vcycle(int l, const CSel& fsel, const Sel& osel, const GSel& gate, 
             x_is_mf = true;  // fused: t = f - A (m o f)
             for_parts([&](Part& p, size_t) {
                 DevLevel& L = p.lv[l];
-                vrows(p, L.A, OpRes0{L.m, fsel(p), L.t, {}}, gate(p), "res0");
+                if (l == 0 && fuse_r_new)  // + the previous CG iteration's r -= alpha q
+                    vrows(p, L.A,
+                          OpRes0Upd<FinRes0Upd>{L.m, fuse_r_old, p.q, fuse_r_new, L.t, p.ks, 0.0, FinRes0Upd{p.ks}},
+                          gate(p), "res0 + r update");
+                else
+                    vrows(p, L.A, OpRes0{L.m, fsel(p), L.t, {}}, gate(p), "res0");
             });
         } else {
             for_parts([&](Part& p, size_t i) {
@@ -850,6 +861,26 @@ void Handle::cg_iteration(int parity) {
     allreduce_fin(1, [](Part& p) { return FinCgUpdate{p.ks}; }, gate);
 }
 
+// Fused CG iteration k (single part, SPAI-0/Jacobi, npre = 1, >= 2 levels):
+// the same arithmetic as cg_iteration with iteration k-1's r update moved
+// into this V-cycle's first kernel and its x update into this CG direction
+// kernel (one kernel and 16n bytes less per iteration).
+void Handle::cg_iteration_fused(int parity) {
+    Part& p = parts[0];
+    GSel gate = [](Part& q) { return (const int32_t*)&q.ks->done; };
+    double* r_old = parity ? p.r2 : p.r;
+    double* r_new = parity ? p.r : p.r2;
+    double* pold = parity ? p.pb : p.pa;
+    double* pnew = parity ? p.pa : p.pb;
+    fuse_r_old = r_old;
+    fuse_r_new = r_new;
+    vcycle(0, [r_new](Part&) { return (const double*)r_new; }, [](Part& q) { return q.z; }, gate, true);
+    fuse_r_old = nullptr;
+    fuse_r_new = nullptr;
+    rows(p, p.lv[0].A, OpCgDirX<FinSigmaX>{p.z, pold, pnew, p.q, p.xcur, p.ks, 0.0, 0.0, FinSigmaX{p.ks}},
+         gate(p), "cg dir + x update");
+}
+
 // One BiCGStab iteration (§8c c-1).
 void Handle::bicgstab_iteration() {
     GSel gate = [](Part& p) { return (const int32_t*)&p.ks->done; };
@@ -935,11 +966,15 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
     // Krylov loop: two iterations per host round trip, replayed from a CUDA
     // graph; kernels of iterations past convergence exit at their gate.
     const bool use_graph = prm.use_graph && !sync_debug;
+    cg_fused = !bicg && !dist && prm.relax != 2 && prm.npre == 1 && parts[0].lv.size() >= 2 &&
+               std::getenv("AMGB_NO_CG_FUSION") == nullptr;
     auto two_iterations = [&] {
         for (int k = 0; k < 2; ++k) {
             cur_iter = k;
             if (bicg)
                 bicgstab_iteration();
+            else if (cg_fused)
+                cg_iteration_fused(k);
             else
                 cg_iteration(k);
         }
@@ -990,6 +1025,7 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
             graph_x = x;
             graph_prof_mask = 0;
             graph_loop = true;
+            graph_fused = cg_fused;
         }
         const int iter_before = ks_host->iter;
         ck(cudaGraphLaunch(graph, stream), "graph launch");
@@ -1005,7 +1041,7 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
     while (!ks_host->done) {
         const int iter_before = ks_host->iter;
         if (use_graph) {
-            if (!graph || graph_loop || graph_x != x || graph_prof_mask != prof_mask) {
+            if (!graph || graph_loop || graph_x != x || graph_prof_mask != prof_mask || graph_fused != cg_fused) {
                 drop_graph();
                 graph_loop = false;
                 cudaGraph_t g;
@@ -1027,6 +1063,7 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
                 cudaGraphDestroy(g);
                 graph_x = x;
                 graph_prof_mask = prof_mask;
+                graph_fused = cg_fused;
             }
             ck(cudaGraphLaunch(graph, stream), "graph launch");
             launches += graph_kernels;
@@ -1037,6 +1074,13 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
         ck(cudaStreamSynchronize(stream), "sync");
         const int ran = ks_host->iter - iter_before + (ks_host->done && ks_host->status ? 1 : 0);
         collect(use_graph ? rec_graph : rec_direct, ran, !use_graph);
+    }
+    // fused CG: an r update already applied may still owe its x update
+    if (cg_fused && ks_host->xpend) {
+        Part& p = parts[0];
+        const int last = ks_host->iter - 1;  // the iteration whose alpha, p are pending
+        double* plast = (last % 2) ? p.pa : p.pb;
+        vec(p, p.lv[0].n, VAxpyAlpha{p.xcur, plast, p.ks, 0.0, {}}, nullptr, "cg final x update");
     }
     // true residual |f - A x| / |f|
     exchange(0, [](Part& p) { return p.xcur; });
@@ -1819,6 +1863,7 @@ void upload_part(Handle& H, const RankPart& RP, Part& P) {
     P.red.ticket = static_cast<unsigned int*>(pp);
     if (H.distributed()) P.red.defer = H.dalloc(4);
     P.r = H.dalloc(nv0);
+    P.r2 = H.dalloc(nv0);  // fused CG: ping-pong r
     P.z = H.dalloc(nv0);
     P.pa = H.dalloc(nv0);
     P.pb = H.dalloc(nv0);

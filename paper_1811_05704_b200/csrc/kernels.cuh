@@ -36,6 +36,8 @@ struct Sell {
 struct KState {
     double nf, tolnf, res, rho, rho_prev, sigma, alpha, beta, omega, rhat_norm, true_res, ss;
     int32_t iter, maxiter, done, skip2, status, half;
+    int32_t upd;    // fused CG: alpha of this iteration awaits its r update (next res0)
+    int32_t xpend;  // fused CG: an applied r update awaits its x update (next CG direction)
 };
 
 // Deterministic single-pass grid reduction scratch: per-block partials + ticket.
@@ -746,6 +748,69 @@ struct OpCgDir {
         pn[i] = pi;
         q[i] = s;
         d[0] += pi * s;
+    }
+};
+
+// Fused CG (single part, SPAI-0/Jacobi, npre = 1): the first level-0 kernel
+// of iteration k also applies iteration k-1's r -= alpha q (formed inside the
+// gather -- bitwise the same fma as the separate update -- and stored once to a
+// ping-pong r buffer) and computes (r, r) for the loop test:
+//   rn = r - alpha q;  t = rn - A (m o rn);  (rn, rn)
+template <class Fin>
+struct OpRes0Upd {
+    static constexpr int GATHER = 3, ROWV = 2;  // m, r, q gathered; rn, t written
+    static constexpr int NDOT = 1;
+    const double* m;
+    const double* r;
+    const double* q;
+    double* rn;
+    double* t;
+    const KState* ks;
+    double alpha;
+    Fin fin;
+    struct Row {
+        double r, q;
+    };
+    __device__ void prepare() { alpha = ks->upd ? ks->alpha : 0.0; }
+    __device__ Row load(int64_t i) const { return {r[i], q[i]}; }
+    __device__ double gather(int32_t c) const { return __ldg(m + c) * fma(-alpha, __ldg(q + c), __ldg(r + c)); }
+    __device__ void row(int64_t i, double s, const Row& rr, double* d) const {
+        const double v = fma(-alpha, rr.q, rr.r);
+        rn[i] = v;
+        t[i] = v - s;
+        d[0] += v * v;
+    }
+};
+
+// Fused CG direction: OpCgDir plus iteration k-1's x += alpha p (p = the old
+// direction this kernel reads anyway).
+template <class Fin>
+struct OpCgDirX {
+    static constexpr int GATHER = 2, ROWV = 4;  // z, p gathered; pn, q written; x read + written
+    static constexpr int NDOT = 1;
+    const double* z;
+    const double* p;
+    double* pn;
+    double* q;
+    double* x;
+    const KState* ks;
+    double beta, xa;
+    Fin fin;
+    struct Row {
+        double z, p;
+    };
+    __device__ void prepare() {
+        beta = ks->beta;
+        xa = ks->xpend ? ks->alpha : 0.0;
+    }
+    __device__ Row load(int64_t i) const { return {z[i], p[i]}; }
+    __device__ double gather(int32_t c) const { return fma(beta, __ldg(p + c), __ldg(z + c)); }
+    __device__ void row(int64_t i, double s, const Row& rr, double* d) const {
+        const double pi = fma(beta, rr.p, rr.z);
+        pn[i] = pi;
+        q[i] = s;
+        d[0] += pi * s;
+        if (xa != 0.0) x[i] = fma(xa, rr.p, x[i]);
     }
 };
 

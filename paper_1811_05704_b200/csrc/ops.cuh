@@ -99,6 +99,50 @@ struct FinCgUpdate {  // CG: res = |r|; k += 1; loop test of §8c c-1
     }
 };
 
+// Fused CG (see OpRes0Upd / OpCgDirX): the r update of iteration k-1 landed
+// in this iteration's first kernel: res, k += 1, loop test of §8c c-1.
+struct FinRes0Upd {
+    KState* ks;
+    __device__ void operator()(const double* t) const {
+        if (!ks->upd) return;  // iteration 0: nothing was updated
+        ks->res = sqrt(t[0]);
+        ks->iter += 1;
+        ks->rho_prev = ks->rho;
+        ks->upd = 0;
+        ks->xpend = 1;
+        ks->done = !(ks->iter < ks->maxiter && ks->res > ks->tolnf);
+    }
+};
+
+struct FinSigmaX {  // FinSigma + bookkeeping of the deferred updates
+    KState* ks;
+    __device__ void operator()(const double* t) const {
+        ks->xpend = 0;  // the CG direction kernel just applied it
+        const double sigma = t[0];
+        if (!(sigma > 0.0)) {
+            ks->status = AMG_BREAKDOWN;
+            ks->done = 1;
+            ks->upd = 0;
+            return;
+        }
+        ks->sigma = sigma;
+        ks->alpha = ks->rho / sigma;
+        ks->upd = 1;
+    }
+};
+
+// x += alpha p (the last deferred x update after the loop)
+struct VAxpyAlpha {
+    static constexpr int NDOT = 0, STREAMS = 3;
+    double* x;
+    const double* p;
+    const KState* ks;
+    double alpha;
+    NoFin fin;
+    __device__ void prepare() { alpha = ks->alpha; }
+    __device__ void elem(int64_t i, double*) const { x[i] = fma(alpha, p[i], x[i]); }
+};
+
 // BiCGStab finalizers (§8c c-1, right-preconditioned van der Vorst)
 struct FinBiAlpha {  // alpha = rho / (rhat, v)
     KState* ks;
