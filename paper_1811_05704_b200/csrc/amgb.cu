@@ -176,6 +176,7 @@ struct DevLevel {
     double* t = nullptr;     // residual
     double* p = nullptr;     // Chebyshev direction
     double* o = nullptr;     // V-cycle output (levels >= 1)
+    double* mf = nullptr;    // m o f, written by the restriction into this level (levels >= 1)
     std::vector<double> cheb_alpha, cheb_beta;
     double alg_bytes = 0;
     int64_t dev_bytes = 0;
@@ -697,8 +698,15 @@ bool Handle::vcycle(int l, const CSel& fsel, const Sel& osel, const GSel& gate, 
         for (size_t i = 0; i < parts.size(); ++i) std::swap(X[i], Y[i]);
     };
 
+    // m o f of this level was produced by the restriction above (levels >= 1,
+    // SPAI-0/Jacobi, npre = 1): the zero-start residual gathers it instead of
+    // m and f, the prolongation reads it instead of m and f
+    const bool have_mf = l > 0 && parts[0].lv[l].mf != nullptr;
     // the right-hand side of a distributed level is gathered by the first pass
-    exchange(l, [&](Part& p) { return const_cast<double*>(fsel(p)); });
+    if (have_mf)
+        exchange(l, [&](Part& p) { return p.lv[l].mf; });
+    else
+        exchange(l, [&](Part& p) { return const_cast<double*>(fsel(p)); });
 
     // ---- pre-smoothing from x = 0 and residual t = f - A x
     bool x_is_mf = false;  // x == m o f implicitly (not materialised)
@@ -711,6 +719,8 @@ bool Handle::vcycle(int l, const CSel& fsel, const Sel& osel, const GSel& gate, 
                     vrows(p, L.A,
                           OpRes0Upd<FinRes0Upd>{L.m, fuse_r_old, p.q, fuse_r_new, L.t, p.ks, 0.0, FinRes0Upd{p.ks}},
                           gate(p), "res0 + r update");
+                else if (have_mf)
+                    vrows(p, L.A, OpRes0MF{L.mf, fsel(p), L.t, {}}, gate(p), "res0 (mf)");
                 else
                     vrows(p, L.A, OpRes0{L.m, fsel(p), L.t, {}}, gate(p), "res0");
             });
@@ -776,17 +786,26 @@ bool Handle::vcycle(int l, const CSel& fsel, const Sel& osel, const GSel& gate, 
         DevLevel& C = p.lv[l + 1];
         // into the next level's vector; a replicated next level receives the
         // slice [crow0, crow1) of the full vector
-        vrows(p, L.R, OpSpmv{L.t, C.f + (next_rep ? L.crow0 : 0)}, gate(p), "restrict");
+        const int64_t off = next_rep ? L.crow0 : 0;
+        if (C.mf)
+            vrows(p, L.R, OpSpmvMF{L.t, C.f + off, C.m + off, C.mf + off, {}}, gate(p), "restrict (+mf)");
+        else
+            vrows(p, L.R, OpSpmv{L.t, C.f + off}, gate(p), "restrict");
     });
     // entering the replicated levels: gather the other ranks' slices of f_{l+1}
-    if (next_rep && !parts[0].lv[l].replicated) allgather_slices(l + 1, [&](Part& p) { return p.lv[l + 1].f; });
+    if (next_rep && !parts[0].lv[l].replicated) {
+        allgather_slices(l + 1, [&](Part& p) { return p.lv[l + 1].f; });
+        if (parts[0].lv[l + 1].mf) allgather_slices(l + 1, [&](Part& p) { return p.lv[l + 1].mf; });
+    }
     vcycle(l + 1, [&](Part& p) { return (const double*)p.lv[l + 1].f; }, [&](Part& p) { return p.lv[l + 1].o; }, gate,
            false);
     exchange(l + 1, [&](Part& p) { return p.lv[l + 1].o; });
     for_parts([&](Part& p, size_t i) {
         DevLevel& L = p.lv[l];
         DevLevel& C = p.lv[l + 1];
-        if (x_is_mf)
+        if (x_is_mf && have_mf)
+            vrows(p, L.P, OpProl0MF{C.o, L.mf, X[i], {}}, gate(p), "prolong0 (mf)");
+        else if (x_is_mf)
             vrows(p, L.P, OpProl0{C.o, L.m, fsel(p), X[i], {}}, gate(p), "prolong0");
         else
             vrows(p, L.P, OpProlAdd{C.o, X[i], {}}, gate(p), "prolong");
@@ -1836,6 +1855,10 @@ void upload_part(Handle& H, const RankPart& RP, Part& P) {
             L.f = H.dalloc(nv);
             L.o = H.dalloc(nv);
             L.dev_bytes += 16 * nv;
+            if (!coarsest && prm.relax != 2 && prm.npre == 1 && !std::getenv("AMGB_NO_MF")) {
+                L.mf = H.dalloc(nv);
+                L.dev_bytes += 8 * nv;
+            }
         }
         if (!lp.replicated) {
             L.plan = lp.halo;

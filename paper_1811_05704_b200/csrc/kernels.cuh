@@ -617,6 +617,62 @@ struct OpResidual {
     }
 };
 
+// Restriction that also emits the next level's m o f (a2 feeding a1): y = R t,
+// mf = m_c o y -- so the next level's zero-start residual gathers one vector.
+struct OpSpmvMF {
+    static constexpr int GATHER = 1, ROWV = 3;  // t gathered; y, mf written, m_c read
+    static constexpr int NDOT = 0;
+    const double* x;
+    double* y;
+    const double* mc;
+    double* mf;
+    NoFin fin;
+    struct Row {
+        double m;
+    };
+    __device__ void prepare() {}
+    __device__ Row load(int64_t i) const { return {mc[i]}; }
+    __device__ double gather(int32_t c) const { return __ldg(x + c); }
+    __device__ void row(int64_t i, double s, const Row& rr, double*) const {
+        y[i] = s;
+        mf[i] = rr.m * s;
+    }
+};
+
+// Zero-start residual with a precomputed mf = m o f: t = f - A mf.
+struct OpRes0MF {
+    static constexpr int GATHER = 1, ROWV = 2;  // mf gathered; f read, t written
+    static constexpr int NDOT = 0;
+    const double* mf;
+    const double* f;
+    double* t;
+    NoFin fin;
+    struct Row {
+        double f;
+    };
+    __device__ void prepare() {}
+    __device__ Row load(int64_t i) const { return {f[i]}; }
+    __device__ double gather(int32_t c) const { return __ldg(mf + c); }
+    __device__ void row(int64_t i, double s, const Row& rr, double*) const { t[i] = rr.f - s; }
+};
+
+// Prolongation after a zero-start sweep with a precomputed mf: x = mf + P e.
+struct OpProl0MF {
+    static constexpr int GATHER = 1, ROWV = 2;  // e gathered; mf read, x written
+    static constexpr int NDOT = 0;
+    const double* e;
+    const double* mf;
+    double* x;
+    NoFin fin;
+    struct Row {
+        double mf;
+    };
+    __device__ void prepare() {}
+    __device__ Row load(int64_t i) const { return {mf[i]}; }
+    __device__ double gather(int32_t c) const { return __ldg(e + c); }
+    __device__ void row(int64_t i, double s, const Row& rr, double*) const { x[i] = rr.mf + s; }
+};
+
 // Zero-start smoother + residual (a1): with x = m o f (the first SPAI-0/Jacobi
 // sweep from x = 0), t = f - A x, computing x_j = m_j f_j inside the gather.
 struct OpRes0 {
