@@ -438,6 +438,7 @@ def main():
                 f"{h.dist_info()['first_replicated']} distributed, coarser replicated)",
                 "levels": len(infos), "rows_per_level": [i["rows"] for i in infos],
                 "nnz_per_level": [i["nnz_A"] for i in infos],
+                "dict_slice_frac_A0": round(infos[0]["dict_slices_A"] / max(1, (infos[0]["rows"] + 31) // 32), 4),
                 "iters_per_solve": iters_all[-1], "rel_resid": rels[-1], "status": statuses[-1],
                 "solve_ms": t_max_ms / args.steps, "setup_s": setup_s,
                 "l2": "inputs larger than L2 (level-0 matrix %.2f GB + hierarchy vs 126 MB L2); no flush"

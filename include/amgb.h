@@ -87,7 +87,8 @@ typedef struct {
     int64_t rows, nnz_A, nnz_P, cols_P; /* nnz_P = nnz(R); 0 on the coarsest level */
     int64_t aggregates;                 /* = cols_P */
     int32_t is_coarsest;
-    int32_t reserved;
+    int32_t dict_slices_A;              /* 32-row slices of A stored with a column-offset
+                                           dictionary (TMA SELL-32 format) */
     int64_t dev_bytes;                  /* device bytes of this level's store */
     int64_t padded_nnz_A;               /* stored (sliced-ELL) entries of A incl. padding */
     double alg_bytes_vcycle;            /* algorithmic HBM bytes of this level per V-cycle */
@@ -109,7 +110,7 @@ typedef struct {
     int32_t iters;          /* Krylov iterations (loop trips, DESIGN.md §3 R19) */
     int32_t vcycles;        /* preconditioner applications */
     int32_t status;
-    int32_t reserved;
+    int32_t flags;          /* bit 0: the fused CG iteration ran */
     int64_t kernel_launches;/* kernels this library launched during the solve */
     double solve_ms;        /* device time of the solve (events on the handle stream) */
     double rel_resid;       /* true |f - A x| / |f| */

@@ -66,7 +66,7 @@ class AmgParams(C.Structure):
 class LevelInfo(C.Structure):
     _fields_ = [
         ("rows", C.c_int64), ("nnz_A", C.c_int64), ("nnz_P", C.c_int64), ("cols_P", C.c_int64),
-        ("aggregates", C.c_int64), ("is_coarsest", C.c_int32), ("reserved", C.c_int32),
+        ("aggregates", C.c_int64), ("is_coarsest", C.c_int32), ("dict_slices_A", C.c_int32),
         ("dev_bytes", C.c_int64), ("padded_nnz_A", C.c_int64), ("alg_bytes_vcycle", C.c_double),
     ]
 
@@ -91,7 +91,7 @@ class DistLevelExport(C.Structure):
 
 class SolveStats(C.Structure):
     _fields_ = [
-        ("iters", C.c_int32), ("vcycles", C.c_int32), ("status", C.c_int32), ("reserved", C.c_int32),
+        ("iters", C.c_int32), ("vcycles", C.c_int32), ("status", C.c_int32), ("flags", C.c_int32),
         ("kernel_launches", C.c_int64), ("solve_ms", C.c_double), ("rel_resid", C.c_double),
         ("alg_bytes", C.c_double), ("prof_ms", C.c_double * 8), ("prof_bytes", C.c_double * 8),
         ("prof_launches", C.c_int64 * 8),

@@ -147,6 +147,93 @@ HostSell to_sell(const Csr& A, int C = 32) {
     return S;
 }
 
+// Column storage of the TMA-staged SELL-32 format ("offset
+// dictionary").  A slice whose 32 rows share one sorted set U of column offsets
+// (col - row) with |U| = the slice width, and for which every row + u is a
+// valid column, stores U once (w ints) instead of 32 w column indices; its
+// values are re-laid out at U's positions with zeros where a row lacks an
+// offset (0 * x_j added in column order leaves every row sum unchanged).  Other
+// slices keep explicit indices.  cptr[s]: first int of slice s; each tile of 8
+// slices starts 16-byte aligned (cp.async.bulk), so a slice is a dictionary iff
+// cptr[s+1] - cptr[s] < 32 w.
+struct HostTmaCols {
+    std::vector<int64_t> cptr;
+    std::vector<int32_t> col;
+    int64_t idx_bytes = 0;  // index bytes the format needs (excl. alignment/padding)
+    int64_t ndict = 0;      // dictionary slices
+};
+
+HostTmaCols tma_cols(const Csr& A, HostSell& S, bool allow_dict) {
+    constexpr int C = 32;
+    const int64_t ns = S.nslices;
+    std::vector<std::vector<int32_t>> U(ns);
+    std::vector<int64_t> true_nnz(ns, 0);
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t s = 0; s < ns; ++s) {
+        const int64_t w = (S.sptr[s + 1] - S.sptr[s]) / C;
+        const int64_t r0 = s * C, r1 = std::min<int64_t>(A.nrows, r0 + C);
+        true_nnz[s] = A.ptr[r1] - A.ptr[r0];
+        if (!allow_dict || w == 0 || r1 - r0 < C) continue;
+        std::vector<int64_t> offs;
+        offs.reserve((size_t)true_nnz[s]);
+        for (int64_t r = r0; r < r1; ++r)
+            for (int64_t e = A.ptr[r]; e < A.ptr[r + 1]; ++e) offs.push_back((int64_t)A.col[e] - r);
+        std::sort(offs.begin(), offs.end());
+        offs.erase(std::unique(offs.begin(), offs.end()), offs.end());
+        if ((int64_t)offs.size() != w) continue;
+        bool ok = true;
+        for (int64_t r = r0; r < r1 && ok; ++r)
+            ok = r + offs.front() >= 0 && r + offs.back() < A.ncols;
+        if (!ok) continue;
+        U[s].assign(offs.begin(), offs.end());
+        // values at U's positions (the row's entries are ascending, so are U's)
+        for (int lane = 0; lane < C; ++lane) {
+            const int64_t r = r0 + lane;
+            int64_t k = 0;
+            for (int64_t e = A.ptr[r]; e < A.ptr[r + 1]; ++e) {
+                const int64_t u = (int64_t)A.col[e] - r;
+                for (; U[s][k] != u; ++k) {
+                    S.val[S.sptr[s] + C * k + lane] = 0.0;
+                    S.col[S.sptr[s] + C * k + lane] = (int32_t)(r + U[s][k]);
+                }
+                S.val[S.sptr[s] + C * k + lane] = A.val[e];
+                S.col[S.sptr[s] + C * k + lane] = A.col[e];
+                ++k;
+            }
+            for (; k < w; ++k) {
+                S.val[S.sptr[s] + C * k + lane] = 0.0;
+                S.col[S.sptr[s] + C * k + lane] = (int32_t)(r + U[s][k]);
+            }
+        }
+    }
+    HostTmaCols T;
+    T.cptr.assign(ns + 1, 0);
+    int64_t cur = 0;
+    for (int64_t s = 0; s < ns; ++s) {
+        if (s % 8 == 0) cur = (cur + 3) & ~int64_t(3);
+        T.cptr[s] = cur;
+        const int64_t w = (S.sptr[s + 1] - S.sptr[s]) / C;
+        if (!U[s].empty()) {
+            cur += w;
+            T.idx_bytes += 4 * w;
+            ++T.ndict;
+        } else {
+            cur += C * w;
+            T.idx_bytes += 4 * true_nnz[s];
+        }
+    }
+    T.cptr[ns] = (cur + 3) & ~int64_t(3);
+    T.col.assign(T.cptr[ns], 0);
+#pragma omp parallel for schedule(static)
+    for (int64_t s = 0; s < ns; ++s) {
+        if (!U[s].empty())
+            std::copy(U[s].begin(), U[s].end(), T.col.begin() + T.cptr[s]);
+        else
+            std::copy(S.col.begin() + S.sptr[s], S.col.begin() + S.sptr[s + 1], T.col.begin() + T.cptr[s]);
+    }
+    return T;
+}
+
 // A device matrix in the format chosen for it.
 enum class Fmt { CSR, SELL, TMA };
 
@@ -156,6 +243,12 @@ struct DMat {
     SellTma tma;
     CsrDev csr;
     int64_t nrows = 0, ncols = 0, nnz = 0, stored = 0;
+    int64_t idx_bytes = -1;  // column-index bytes the format needs (-1: 4 per entry)
+    int64_t ndict = 0;       // TMA slices stored with an offset dictionary
+    // algorithmic matrix bytes of one pass: values + the indices the format needs
+    double mat_bytes(bool f32) const {
+        return (f32 ? 4.0 : 8.0) * nnz + (idx_bytes < 0 ? 4.0 * nnz : (double)idx_bytes);
+    }
 };
 
 // One level of one part.  Vectors that are gathered by a matrix pass have a
@@ -166,7 +259,7 @@ struct DevLevel {
     int64_t ng = 0;                // ghost entries
     int64_t nc = 0;                // columns of P (coarse local + ghost, or the full coarse size)
     int64_t crow0 = 0, crow1 = 0;  // local rows of R (slice of level l+1)
-    int64_t nnzA = 0, nnzP = 0, nnzR = 0, padA = 0;
+    int64_t nnzA = 0, nnzP = 0, nnzR = 0, padA = 0, dictA = 0;
     DMat A, P, R;
     double* m = nullptr;     // SPAI-0 / Jacobi diagonal (local + ghost)
     double* diag = nullptr;  // a_ii (Chebyshev)
@@ -232,7 +325,7 @@ struct Handle {
     int graph_prof_mask = 0;
     int64_t graph_kernels = 0;
     bool graph_loop = false;  // the graph runs the whole loop (conditional WHILE node)
-    bool graph_fused = false; // the graph holds fused CG iterations
+    int graph_variant = -1;   // cg_fused | mf0 << 1 of the captured iterations
     // accounting
     int64_t launches = 0;
     amg_solve_stats stats{};
@@ -496,8 +589,7 @@ struct Handle {
         // matrices too big for L2 stream their entries (evict-first); the rest
         // keep them cached so coarse levels stay L2-resident across cycles
         const bool big = M.nnz * 12 > (int64_t)48 << 20;
-        const double mb = F32 ? 8.0 : 12.0;
-        const double bytes = mb * M.nnz + 4.0 * M.nrows + 8.0 * M.ncols * Op::GATHER + 8.0 * M.nrows * Op::ROWV;
+        const double bytes = M.mat_bytes(F32) + 4.0 * M.nrows + 8.0 * M.ncols * Op::GATHER + 8.0 * M.nrows * Op::ROWV;
         const Red& red = p.red;
         launch(mat_class(p, M), bytes, what, [&] {
             if (M.fmt == Fmt::TMA) {  // T = 1 lane per row (narrow rows only, pick_format)
@@ -643,6 +735,7 @@ struct Handle {
     const double* fuse_r_old = nullptr;
     double* fuse_r_new = nullptr;
     bool cg_fused = false;
+    bool mf0 = false;  // the unfused CG keeps m o r in lv[0].mf (VCgUpdateMF)
     void cg_iteration_fused(int parity);
     template <int K>
     void ensure_batch();
@@ -701,7 +794,7 @@ bool Handle::vcycle(int l, const CSel& fsel, const Sel& osel, const GSel& gate, 
     // m o f of this level was produced by the restriction above (levels >= 1,
     // SPAI-0/Jacobi, npre = 1): the zero-start residual gathers it instead of
     // m and f, the prolongation reads it instead of m and f
-    const bool have_mf = l > 0 && parts[0].lv[l].mf != nullptr;
+    const bool have_mf = parts[0].lv[l].mf != nullptr && (l > 0 || mf0);
     // the right-hand side of a distributed level is gathered by the first pass
     if (have_mf)
         exchange(l, [&](Part& p) { return p.lv[l].mf; });
@@ -876,7 +969,12 @@ void Handle::cg_iteration(int parity) {
         rows(p, p.lv[0].A, OpCgDir<FinSigma>{p.z, pold(p), pnew(p), p.q, p.ks, 0.0, FinSigma{p.ks}}, gate(p), "cg dir");
     allreduce_fin(1, [](Part& p) { return FinSigma{p.ks}; }, gate);
     for (Part& p : parts)
-        vec(p, p.lv[0].n, VCgUpdate{p.xcur, p.r, pnew(p), p.q, p.ks, 0.0, FinCgUpdate{p.ks}}, gate(p), "cg update");
+        if (mf0)
+            vec(p, p.lv[0].n,
+                VCgUpdateMF{p.xcur, p.r, pnew(p), p.q, p.lv[0].m, p.lv[0].mf, p.ks, 0.0, FinCgUpdate{p.ks}}, gate(p),
+                "cg update (+mf)");
+        else
+            vec(p, p.lv[0].n, VCgUpdate{p.xcur, p.r, pnew(p), p.q, p.ks, 0.0, FinCgUpdate{p.ks}}, gate(p), "cg update");
     allreduce_fin(1, [](Part& p) { return FinCgUpdate{p.ks}; }, gate);
 }
 
@@ -935,6 +1033,19 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
     std::fill(acc_bytes, acc_bytes + 8, 0.0);
     std::fill(acc_launches, acc_launches + 8, 0);
     cur_iter = -1;
+    // Fused CG iteration (opt-in, AMGB_CG_FUSION=1): its first kernel gathers m,
+    // r and q to save the 48 n-byte update kernel.  Measured (interleaved A/B,
+    // DESIGN.md §6): no gain on 256^3 Poisson (42.1 vs 41.8 ms), a loss where
+    // gathers are random (permuted 150^3: 29.7 vs 18.5 ms).
+    const char* fz = std::getenv("AMGB_CG_FUSION");
+    cg_fused = !bicg && !dist && prm.relax != 2 && prm.npre == 1 && parts[0].lv.size() >= 2 && fz && fz[0] == '1';
+    // unfused CG: the update kernel also writes m o r for the level-0 residual
+    mf0 = !bicg && !cg_fused && parts[0].lv[0].mf != nullptr && std::getenv("AMGB_NO_MF0") == nullptr;
+    const int variant = (cg_fused ? 1 : 0) | (mf0 ? 2 : 0);
+    struct FlagReset {  // precond / GMRES / level_op V-cycles never see mf0
+        bool& f;
+        ~FlagReset() { f = false; }
+    } mf0_reset{mf0};
     GSel nogate = [](Part&) { return (const int32_t*)nullptr; };
     ck(cudaEventRecord(ev0, stream), "event");
     // right-hand side / solution slices of every part
@@ -958,6 +1069,9 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
     for (Part& p : parts)
         rows(p, p.lv[0].A, OpResidual<1, FinInitRes>{p.xcur, p.fcur, p.r, FinInitRes{p.ks}}, nullptr, "r0");
     allreduce_fin(1, [](Part& p) { return FinInitRes{p.ks}; }, nogate);
+    if (mf0)
+        for (Part& p : parts)
+            vec(p, p.lv[0].n, VMulDiag{p.lv[0].m, p.r, p.lv[0].mf, {}}, nullptr, "m o r0");
     for (Part& p : parts) {
         const int64_t n = p.lv[0].n + p.lv[0].ng;
         ck(cudaMemsetAsync(p.pa, 0, n * sizeof(double), stream), "memset");
@@ -985,8 +1099,6 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
     // Krylov loop: two iterations per host round trip, replayed from a CUDA
     // graph; kernels of iterations past convergence exit at their gate.
     const bool use_graph = prm.use_graph && !sync_debug;
-    cg_fused = !bicg && !dist && prm.relax != 2 && prm.npre == 1 && parts[0].lv.size() >= 2 &&
-               std::getenv("AMGB_NO_CG_FUSION") == nullptr;
     auto two_iterations = [&] {
         for (int k = 0; k < 2; ++k) {
             cur_iter = k;
@@ -1005,7 +1117,7 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
     // (event nodes are not allowed inside conditional bodies).
     const bool use_loop = use_graph && !dist && prof_mask == 0 && std::getenv("AMGB_NO_DEVICE_LOOP") == nullptr;
     if (use_loop && !ks_host->done) {
-        if (!graph || !graph_loop || graph_x != x) {
+        if (!graph || !graph_loop || graph_x != x || graph_variant != variant) {
             drop_graph();
             cudaGraph_t g;
             ck(cudaGraphCreate(&g, 0), "graph create");
@@ -1044,7 +1156,7 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
             graph_x = x;
             graph_prof_mask = 0;
             graph_loop = true;
-            graph_fused = cg_fused;
+            graph_variant = variant;
         }
         const int iter_before = ks_host->iter;
         ck(cudaGraphLaunch(graph, stream), "graph launch");
@@ -1060,7 +1172,7 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
     while (!ks_host->done) {
         const int iter_before = ks_host->iter;
         if (use_graph) {
-            if (!graph || graph_loop || graph_x != x || graph_prof_mask != prof_mask || graph_fused != cg_fused) {
+            if (!graph || graph_loop || graph_x != x || graph_prof_mask != prof_mask || graph_variant != variant) {
                 drop_graph();
                 graph_loop = false;
                 cudaGraph_t g;
@@ -1082,7 +1194,7 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
                 cudaGraphDestroy(g);
                 graph_x = x;
                 graph_prof_mask = prof_mask;
-                graph_fused = cg_fused;
+                graph_variant = variant;
             }
             ck(cudaGraphLaunch(graph, stream), "graph launch");
             launches += graph_kernels;
@@ -1123,6 +1235,7 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
     stats.iters = ks_host->iter;
     stats.vcycles = bicg ? 2 * ks_host->iter - (ks_host->half ? 1 : 0) : ks_host->iter;
     stats.status = ks_host->status;
+    stats.flags = cg_fused ? 1 : 0;
     stats.kernel_launches = launches - launches0;
     stats.solve_ms = ms;
     stats.rel_resid = *rel;
@@ -1745,13 +1858,19 @@ DMat upload_mat(Handle& H, const Csr& A, int64_t* bytes, bool f32 = false) {
         int64_t te = 0;
         for (int64_t q = 0; q < t.ntiles; ++q)
             te = std::max(te, S.sptr[std::min<int64_t>((q + 1) * 8, S.nslices)] - S.sptr[q * 8]);
+        HostTmaCols TC = tma_cols(A, S, !std::getenv("AMGB_NO_DICT"));
+        for (int64_t q = 0; q < t.ntiles; ++q)
+            te = std::max(te, TC.cptr[std::min<int64_t>((q + 1) * 8, S.nslices)] - TC.cptr[q * 8]);
         t.tile_ent = (int32_t)(((std::max<int64_t>(te, 32) + 31) / 32) * 32);
         t.sptr = H.upload(S.sptr);
-        t.col = H.upload(S.col);
+        t.cptr = H.upload(TC.cptr);
+        t.col = H.upload(TC.col);
         t.val = H.upload(S.val);
         if (f32) t.valf = H.upload(std::vector<float>(S.val.begin(), S.val.end()));
         d.stored = (int64_t)S.col.size();
-        *bytes += (int64_t)(S.sptr.size() * 8 + S.col.size() * 12);
+        d.idx_bytes = TC.idx_bytes;
+        d.ndict = TC.ndict;
+        *bytes += (int64_t)(S.sptr.size() * 16 + S.val.size() * 8 + TC.col.size() * 4);
     }
     return d;
 }
@@ -1837,6 +1956,7 @@ void upload_part(Handle& H, const RankPart& RP, Part& P) {
         if (!coarsest || nlev == 1) {
             L.A = upload_mat(H, lp.A, &L.dev_bytes, f32);
             L.padA = L.A.stored;
+            L.dictA = L.A.ndict;
         } else {
             L.padA = L.nnzA;
         }
@@ -1859,6 +1979,10 @@ void upload_part(Handle& H, const RankPart& RP, Part& P) {
                 L.mf = H.dalloc(nv);
                 L.dev_bytes += 8 * nv;
             }
+        } else if (!coarsest && prm.solver == 0 && prm.relax != 2 && prm.npre == 1 && !std::getenv("AMGB_NO_MF")) {
+            // level 0 (CG): m o r, written by the unfused CG update (Handle::mf0)
+            L.mf = H.dalloc(nv);
+            L.dev_bytes += 8 * nv;
         }
         if (!lp.replicated) {
             L.plan = lp.halo;
@@ -2229,6 +2353,7 @@ amg_status amg_level_info_get(amg_handle h, int32_t l, amg_level_info* out) {
     if (!H.parts.empty()) {
         out->dev_bytes = H.parts[0].lv[l].dev_bytes;
         out->padded_nnz_A = H.parts[0].lv[l].padA;
+        out->dict_slices_A = (int32_t)H.parts[0].lv[l].dictA;
     }
     return AMG_OK;
 }

@@ -294,6 +294,7 @@ constexpr int kTmaThreads = kBlock + 32;  // 8 consumer warps + 1 producer warp
 struct SellTma {
     int64_t nrows = 0, ncols = 0, nslices = 0, ntiles = 0;
     const int64_t* sptr = nullptr;  // nslices + 1 element offsets (multiples of C)
+    const int64_t* cptr = nullptr;  // nslices + 1 offsets into col (offset dictionary, amgb.cu tma_cols)
     const int32_t* col = nullptr;
     const double* val = nullptr;
     const float* valf = nullptr;    // fp32 copy of val (mixed-precision V-cycle)
@@ -381,15 +382,16 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sel
                 const int64_t s0 = t * NS;
                 const int64_t s1 = s0 + NS < A.nslices ? s0 + NS : A.nslices;
                 const int64_t e0 = A.sptr[s0], e1 = A.sptr[s1];
-                const uint32_t n = (uint32_t)(e1 - e0);
+                const int64_t c0 = A.cptr[s0], c1 = A.cptr[s1];
+                const uint32_t n = (uint32_t)(e1 - e0), nc = (uint32_t)(c1 - c0);
                 const uint32_t full = smem_u32(bars + s);
                 unsigned char* st = smem + (size_t)s * stage_bytes;
-                mbar_expect_tx(full, n * (uint32_t)(VB + 4));
+                mbar_expect_tx(full, n * (uint32_t)VB + nc * 4u);
                 if constexpr (F32)
                     bulk_g2s<STREAM>(smem_u32(st), A.valf + e0, n * 4u, full, policy);
                 else
                     bulk_g2s<STREAM>(smem_u32(st), A.val + e0, n * 8u, full, policy);
-                bulk_g2s<STREAM>(smem_u32(st + (size_t)te * VB), A.col + e0, n * 4u, full, policy);
+                if (nc) bulk_g2s<STREAM>(smem_u32(st + (size_t)te * VB), A.col + c0, nc * 4u, full, policy);
             }
         }
     } else {  // ------------------------------------ consumer warps
@@ -404,33 +406,46 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sel
             typename Op::Row rr{};
             if constexpr (cols_of<Op>() == 1)
                 if (pt == 0 && has_row) rr = op.load(row);  // in flight during the wait
-            int off = 0, w = 0;
+            int off = 0, w = 0, coff = 0;
+            bool dict = false;  // the slice's columns are row + a shared offset list
             if (slice < A.nslices) {
                 const int64_t e0 = A.sptr[slice];
                 off = (int)(e0 - A.sptr[t * NS]);
                 w = (int)((A.sptr[slice + 1] - e0) / C);
+                const int64_t c0 = A.cptr[slice];
+                coff = (int)(c0 - A.cptr[t * NS]);
+                dict = A.cptr[slice + 1] - c0 < (int64_t)C * w;
             }
             mbar_wait(smem_u32(bars + s), (i / kTmaStages) & 1);
             const VT* sv = reinterpret_cast<const VT*>(smem + (size_t)s * stage_bytes) + off + r;
-            const int32_t* sc =
-                reinterpret_cast<const int32_t*>(smem + (size_t)s * stage_bytes + (size_t)te * VB) + off + r;
+            const int32_t* sc = reinterpret_cast<const int32_t*>(smem + (size_t)s * stage_bytes + (size_t)te * VB) +
+                                coff + (dict ? 0 : r);
             acc_t<Op> sum{};
-            for (int k0 = pt; k0 < w; k0 += UN * T) {
-                acc_t<Op> xv[UN];
-                int32_t c[UN];
+            // entry k's column: sc[CS k] (+ row for a dictionary slice); the
+            // stride is a template constant so every load is an immediate offset
+            auto run = [&](auto cs, int32_t cbase) {
+                constexpr int CS = decltype(cs)::value;
+                for (int k0 = pt; k0 < w; k0 += UN * T) {
+                    acc_t<Op> xv[UN];
+                    int32_t c[UN];
 #pragma unroll
-                for (int u = 0; u < UN; ++u) {
-                    const int k = k0 + u * T;
-                    c[u] = k < w ? sc[C * k] : 0;
+                    for (int u = 0; u < UN; ++u) {
+                        const int k = k0 + u * T;
+                        c[u] = k < w ? sc[CS * k] + cbase : 0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < UN; ++u) xv[u] = (k0 + u * T < w) ? op.gather(c[u]) : acc_t<Op>{};
+#pragma unroll
+                    for (int u = 0; u < UN; ++u) {
+                        const int k = k0 + u * T;
+                        if (k < w) fma_acc(sum, (double)sv[C * k], xv[u]);
+                    }
                 }
-#pragma unroll
-                for (int u = 0; u < UN; ++u) xv[u] = (k0 + u * T < w) ? op.gather(c[u]) : acc_t<Op>{};
-#pragma unroll
-                for (int u = 0; u < UN; ++u) {
-                    const int k = k0 + u * T;
-                    if (k < w) fma_acc(sum, (double)sv[C * k], xv[u]);
-                }
-            }
+            };
+            if (dict)
+                run(std::integral_constant<int, 1>{}, (int32_t)row);
+            else
+                run(std::integral_constant<int, C>{}, 0);
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(bars + kTmaStages + s));  // stage free
             if constexpr (T > 1) {

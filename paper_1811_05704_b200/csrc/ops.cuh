@@ -286,6 +286,30 @@ struct VCgUpdate {
     }
 };
 
+// The same update, also writing mf = m o r_new for the next V-cycle's level-0
+// zero-start residual (one gathered vector instead of m and r).
+struct VCgUpdateMF {
+    static constexpr int STREAMS = 8;  // + m read, mf written
+    static constexpr int NDOT = 1;
+    double* x;
+    double* r;
+    const double* p;
+    const double* q;
+    const double* m;
+    double* mf;
+    const KState* ks;
+    double alpha;
+    FinCgUpdate fin;
+    __device__ void prepare() { alpha = ks->alpha; }
+    __device__ void elem(int64_t i, double* d) const {
+        x[i] = fma(alpha, p[i], x[i]);
+        const double rn = fma(-alpha, q[i], r[i]);
+        r[i] = rn;
+        mf[i] = m[i] * rn;
+        d[0] += rn * rn;
+    }
+};
+
 struct VBiP {
     static constexpr int STREAMS = 3;  // n-vectors moved; p = r (k = 0) or r + beta (p - omega v)
     static constexpr int NDOT = 0;
