@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -1940,29 +1941,29 @@ void upload_part(Handle& H, const RankPart& RP, Part& P) {
         const bool coarsest = l == nlev - 1;
         L.replicated = lp.replicated;
         L.next_replicated = lp.next_replicated;
-        L.n = lp.A.nrows;
+        L.n = lp.ma().nrows;
         L.ng = lp.replicated ? 0 : lp.halo.nghost;
         L.crow0 = lp.crow0;
         L.crow1 = lp.crow1;
-        L.nnzA = lp.A.nnz();
-        L.nnzP = coarsest ? 0 : lp.P.nnz();
-        L.nnzR = coarsest ? 0 : lp.R.nnz();
-        L.nc = coarsest ? 0 : lp.P.ncols;
+        L.nnzA = lp.ma().nnz();
+        L.nnzP = coarsest ? 0 : lp.mp().nnz();
+        L.nnzR = coarsest ? 0 : lp.mr().nnz();
+        L.nc = coarsest ? 0 : lp.mp().ncols;
         if (prm.relax == 2 && !coarsest)
             cheb_coeffs(hl.cheb_d, hl.cheb_c, prm.cheb_degree, L.cheb_alpha, L.cheb_beta);
         L.alg_bytes = level_alg_bytes(L.n, L.nnzA, L.nnzP, coarsest ? 0 : lp.crow1 - lp.crow0, prm, coarsest);
         const int64_t nv = L.n + L.ng;
         const bool f32 = prm.precision == 1;  // fp32 copies of the V-cycle matrix values
         if (!coarsest || nlev == 1) {
-            L.A = upload_mat(H, lp.A, &L.dev_bytes, f32);
+            L.A = upload_mat(H, lp.ma(), &L.dev_bytes, f32);
             L.padA = L.A.stored;
             L.dictA = L.A.ndict;
         } else {
             L.padA = L.nnzA;
         }
         if (!coarsest) {
-            L.P = upload_mat(H, lp.P, &L.dev_bytes, f32);
-            L.R = upload_mat(H, lp.R, &L.dev_bytes, f32);
+            L.P = upload_mat(H, lp.mp(), &L.dev_bytes, f32);
+            L.R = upload_mat(H, lp.mr(), &L.dev_bytes, f32);
             if (prm.relax != 2) L.m = H.upload(lp.m);
             if (prm.relax == 2) L.diag = H.upload(lp.diag);  // Chebyshev D^-1 scaling
             L.x = H.dalloc(nv);
@@ -1993,7 +1994,7 @@ void upload_part(Handle& H, const RankPart& RP, Part& P) {
             }
         }
     }
-    P.nL = RP.lv.back().A.nrows;
+    P.nL = RP.lv.back().ma().nrows;
     P.coarse_inv = H.upload(H.host.coarse_inv);
     P.lv.back().dev_bytes += 8 * P.nL * P.nL;
     const int64_t nv0 = P.lv[0].n + P.lv[0].ng;
@@ -2144,7 +2145,9 @@ static amg_status setup_impl(int64_t n, const int64_t* ptr, const int32_t* col, 
         sp.coarse_enough = prm.coarse_enough;
         sp.max_levels = prm.max_levels;
         sp.dense_max = prm.dense_max;
+        const auto t0 = std::chrono::steady_clock::now();
         H->host = build_hierarchy(std::move(A0), sp);
+        const auto t1 = std::chrono::steady_clock::now();
         H->lg = first_replicated_level(H->host, nranks, gather_below);
         H->starts = level_starts(H->host, nranks, H->lg);
         if (nranks == 1) {
@@ -2155,6 +2158,10 @@ static amg_status setup_impl(int64_t n, const int64_t* ptr, const int32_t* col, 
         } else {
             H->host_parts.push_back(build_rank_part(H->host, nranks, rank, H->lg, H->starts));
         }
+        if (std::getenv("AMGB_SETUP_TIMING"))
+            std::fprintf(stderr, "[setup] hierarchy %.1f ms, partition %.1f ms\n",
+                         std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count());
     } catch (const SetupError& e) {
         return set_error((amg_status)e.code, e.msg);
     } catch (const std::bad_alloc&) {
@@ -2420,9 +2427,9 @@ amg_status amg_dist_level_info(amg_handle h, int32_t rank, int32_t l, int64_t ou
     out[0] = lp->row0;
     out[1] = lp->row1;
     out[2] = lp->halo.nghost;
-    out[3] = lp->A.nnz();
-    out[4] = lp->P.nrows ? lp->P.nnz() : 0;
-    out[5] = lp->R.nrows ? lp->R.nnz() : 0;
+    out[3] = lp->ma().nnz();
+    out[4] = lp->mp().nrows ? lp->mp().nnz() : 0;
+    out[5] = lp->mr().nrows ? lp->mr().nnz() : 0;
     out[6] = lp->crow0;
     out[7] = lp->crow1;
     out[8] = lp->replicated;
@@ -2436,9 +2443,9 @@ amg_status amg_dist_export(amg_handle h, int32_t rank, int32_t l, const amg_dist
     if (!h || !h->h || !out) return set_error(AMG_E_INVALID_ARG, "NULL argument");
     const amgb::LevelPart* lp = find_part(*h->h, rank, l);
     if (!lp) return set_error(AMG_E_INVALID_ARG, "rank/level not held by this handle");
-    copy_csr(lp->A, out->A_ptr, out->A_col, out->A_val);
-    if (lp->P.nrows) copy_csr(lp->P, out->P_ptr, out->P_col, out->P_val);
-    if (lp->R.nrows) copy_csr(lp->R, out->R_ptr, out->R_col, out->R_val);
+    copy_csr(lp->ma(), out->A_ptr, out->A_col, out->A_val);
+    if (lp->mp().nrows) copy_csr(lp->mp(), out->P_ptr, out->P_col, out->P_val);
+    if (lp->mr().nrows) copy_csr(lp->mr(), out->R_ptr, out->R_col, out->R_val);
     const auto& hp = lp->halo;
     if (out->ghost_global) std::copy(hp.ghost_global.begin(), hp.ghost_global.end(), out->ghost_global);
     for (size_t k = 0; k < hp.recv_peer.size(); ++k) {

@@ -99,7 +99,7 @@ RankPart build_rank_part(const HostHierarchy& H, int nranks, int rank, int lg,
     std::vector<std::vector<int64_t>> G(L);
     std::vector<Numbering> num(L);
     for (int l = 0; l < L; ++l) {
-        if (l < lg) {
+        if (l < lg && nranks > 1) {
             G[l] = ghosts_of(H, st, l, rank);
             num[l].lo = st[l][rank];
             num[l].hi = st[l][rank + 1];
@@ -112,14 +112,22 @@ RankPart build_rank_part(const HostHierarchy& H, int nranks, int rank, int lg,
         const HostLevel& hl = H.levels[l];
         LevelPart& lp = RP.lv[l];
         const bool coarsest = l == L - 1;
-        if (l >= lg) {  // replicated
+        if (l >= lg || nranks == 1) {  // replicated (one rank: the whole level, no renumbering)
             lp.replicated = true;
             lp.row0 = 0;
             lp.row1 = hl.A.nrows;
-            lp.A = hl.A;
+            if (nranks == 1)
+                lp.pA = &hl.A;
+            else
+                lp.A = hl.A;
             if (!coarsest) {
-                lp.P = hl.P;
-                lp.R = hl.R;
+                if (nranks == 1) {
+                    lp.pP = &hl.P;
+                    lp.pR = &hl.R;
+                } else {
+                    lp.P = hl.P;
+                    lp.R = hl.R;
+                }
                 lp.crow0 = 0;
                 lp.crow1 = hl.P.ncols;
                 lp.next_replicated = true;

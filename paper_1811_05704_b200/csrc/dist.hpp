@@ -42,6 +42,11 @@ struct LevelPart {
     int64_t crow0 = 0, crow1 = 0;  // owned rows of level l+1 (local rows of R)
     bool next_replicated = false;  // level l+1 is replicated
     Csr A, P, R;                   // local matrices (renumbered columns); P/R empty on the coarsest
+    // one rank: the host hierarchy's own matrices, not copies (ma/mp/mr read through)
+    const Csr *pA = nullptr, *pP = nullptr, *pR = nullptr;
+    const Csr& ma() const { return pA ? *pA : A; }
+    const Csr& mp() const { return pP ? *pP : P; }
+    const Csr& mr() const { return pR ? *pR : R; }
     HaloPlan halo;                 // plan for vectors of this level (distributed levels)
     std::vector<double> m, diag;   // local rows then ghost values
 };

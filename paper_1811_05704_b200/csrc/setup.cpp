@@ -10,6 +10,9 @@
 // with -ffp-contract=off, so the values are reproducible bit for bit and
 // independent of the OpenMP thread count (every parallel loop is over
 // independent rows).
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include "setup.hpp"
 
 #include <algorithm>
@@ -381,26 +384,39 @@ std::vector<double> dense_inverse(const Csr& A) {
             for (int64_t j = k + 1; j < n; ++j) ri[j] -= l * rk[j];
         }
     }
-    // inverse: solve L U X = P I column by column; store X row-major
+    if (std::getenv("AMGB_SETUP_TIMING")) std::fprintf(stderr, "[setup] coarse LU done (n = %lld)\n", (long long)n);
+    // inverse: solve L U X = P I for all columns at once, row by row, in blocks
+    // of columns: element (i, c) sees exactly the operations of a column-by-
+    // column substitution (ascending j, multiply then subtract), but the inner
+    // loop runs over contiguous columns (vectorisable, no reduction chain)
     std::vector<double> inv(n * n);
-#pragma omp parallel
-    {
-        std::vector<double> y(n);
-#pragma omp for schedule(dynamic, 16)
-        for (int64_t c = 0; c < n; ++c) {
-            for (int64_t i = 0; i < n; ++i) y[i] = (perm[i] == c) ? 1.0 : 0.0;
-            for (int64_t i = 0; i < n; ++i) {
-                double s = y[i];
-                for (int64_t j = 0; j < i; ++j) s -= lu[i * n + j] * y[j];
-                y[i] = s;
+    constexpr int64_t kCols = 64;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t c0 = 0; c0 < n; c0 += kCols) {
+        const int64_t w = std::min(kCols, n - c0);
+        std::vector<double> X(n * w);  // rows of the column block
+        for (int64_t i = 0; i < n; ++i)
+            for (int64_t c = 0; c < w; ++c) X[i * w + c] = (perm[i] == c0 + c) ? 1.0 : 0.0;
+        for (int64_t i = 0; i < n; ++i) {  // forward: unit lower L
+            double* xi = &X[i * w];
+            for (int64_t j = 0; j < i; ++j) {
+                const double l = lu[i * n + j];
+                const double* xj = &X[j * w];
+                for (int64_t c = 0; c < w; ++c) xi[c] -= l * xj[c];
             }
-            for (int64_t i = n - 1; i >= 0; --i) {
-                double s = y[i];
-                for (int64_t j = i + 1; j < n; ++j) s -= lu[i * n + j] * y[j];
-                y[i] = s / lu[i * n + i];
-            }
-            for (int64_t i = 0; i < n; ++i) inv[i * n + c] = y[i];
         }
+        for (int64_t i = n - 1; i >= 0; --i) {  // backward: U
+            double* xi = &X[i * w];
+            for (int64_t j = i + 1; j < n; ++j) {
+                const double u = lu[i * n + j];
+                const double* xj = &X[j * w];
+                for (int64_t c = 0; c < w; ++c) xi[c] -= u * xj[c];
+            }
+            const double d = lu[i * n + i];
+            for (int64_t c = 0; c < w; ++c) xi[c] = xi[c] / d;
+        }
+        for (int64_t i = 0; i < n; ++i)
+            for (int64_t c = 0; c < w; ++c) inv[i * n + c0 + c] = X[i * w + c];
     }
     return inv;
 }
@@ -410,6 +426,16 @@ std::vector<double> dense_inverse(const Csr& A) {
 // Algorithm 1 with the stopping rules of §8c L9 (coarse_enough, max_levels,
 // stagnation: no reduction, or > 95% of the rows kept on two levels in a row).
 HostHierarchy build_hierarchy(Csr A0, const SetupParams& prm) {
+    // AMGB_SETUP_TIMING=1: per-level phase times on stderr
+    const bool timing = std::getenv("AMGB_SETUP_TIMING") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what, size_t l) {
+        if (!timing) return;
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[setup] level %zu %-12s %8.1f ms\n", l, what,
+                     std::chrono::duration<double, std::milli>(t - t_last).count());
+        t_last = t;
+    };
     HostHierarchy H;
     H.levels.emplace_back();
     H.levels.back().A = std::move(A0);
@@ -419,23 +445,31 @@ HostHierarchy build_hierarchy(Csr A0, const SetupParams& prm) {
         HostLevel& L = H.levels.back();
         const int64_t n = L.A.nrows;
         if (!(n > prm.coarse_enough && static_cast<int>(H.levels.size()) < prm.max_levels)) break;
+        const size_t lv = H.levels.size() - 1;
         std::vector<uint8_t> S;
         strength(L.A, eps, S);
+        lap("strength", lv);
         std::vector<int32_t> id;
         std::vector<int64_t> root;
         const int64_t cnt = aggregate(L.A, S, id, &root);
+        lap("aggregate", lv);
         const bool slow = static_cast<double>(cnt) > 0.95 * static_cast<double>(n);
         if (cnt == n || (slow && prev_slow)) break;
         prev_slow = slow;
         L.P = prolongation(L.A, S, id, cnt, prm.smoothed, prm.p_omega);
+        lap("P", lv);
         L.R = transpose(L.P);
+        lap("R=P^T", lv);
         L.agg = std::move(id);
         L.root = std::move(root);
         L.n_agg = cnt;
         Csr AP = multiply(L.A, L.P);
+        lap("AP", lv);
         Csr Ac = multiply(L.R, AP);
+        lap("R(AP)", lv);
         AP = Csr();
         setup_smoother(L, prm);
+        lap("smoother", lv);
         H.levels.emplace_back();
         H.levels.back().A = std::move(Ac);
         eps *= prm.eps_decay;
@@ -446,6 +480,7 @@ HostHierarchy build_hierarchy(Csr A0, const SetupParams& prm) {
     // positive diagonal is required on the coarsest level too (strength() checks
     // the others)
     H.coarse_inv = dense_inverse(C.A);
+    lap("coarse inv", H.levels.size() - 1);
     return H;
 }
 

@@ -16,3 +16,8 @@ ncu --set full --clock-control none --import-source on --kernel-name-base demang
     -k "regex:OpCgDir|OpRelax<\(int\)1|sell_tma<\(int\)1, \(bool\)1, amgb::OpRes0>|sell_tma<\(int\)1, \(bool\)1, amgb::OpProl0>|VCgUpdate" \
     -s 25 -c 5 -o $OUT/prof_a0 $PCMD > $OUT/ncu_full.log 2>&1
 echo "ncu full rc=$?"
+if [ -f $OUT/prof_a0.ncu-rep ]; then
+  ncu -i $OUT/prof_a0.ncu-rep --page raw --csv > $OUT/prof_a0_raw.csv 2>/dev/null
+  ncu -i $OUT/prof_a0.ncu-rep --page details --csv > $OUT/prof_a0_details.csv 2>/dev/null
+  [ -n "$KEEP_REP" ] || rm -f $OUT/prof_a0.ncu-rep
+fi
