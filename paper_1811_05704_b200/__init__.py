@@ -60,6 +60,7 @@ class AmgParams(C.Structure):
         ("use_graph", C.c_int32),
         ("precision", C.c_int32),
         ("gmres_m", C.c_int32),
+        ("setup_device", C.c_int32),
     ]
 
 
@@ -162,9 +163,12 @@ PARAM_KEYS = {
     "use_graph": "use_graph",
     "precision": "precision",
     "solver.M": "gmres_m",
+    "setup.device": "setup_device",
 }
 PRECISION = {"double": 0, "mixed": 1}
-_ENUMS = {"relax": RELAX, "coarsening": COARSENING, "solver": SOLVER, "precision": PRECISION}
+SETUP_DEVICE = {"host": 0, "gpu": 1}
+_ENUMS = {"relax": RELAX, "coarsening": COARSENING, "solver": SOLVER, "precision": PRECISION,
+          "setup_device": SETUP_DEVICE}
 
 
 class AmgError(RuntimeError):

@@ -2074,18 +2074,22 @@ void amg_params_default(amg_params* p) {
     p->use_graph = 1;
     p->precision = 0;
     p->gmres_m = 30;
+    p->setup_device = 0;
 }
 
 const char* amg_last_error(void) { return amgb::g_err.c_str(); }
 
 const char* amg_version(void) {
-    return "amgb 0.2 (sm_100a; TMA-staged SELL / SELL-32 / row-block CSR fp64 solve phase; host SA setup; "
+    return "amgb 0.3 (sm_100a; TMA-staged SELL / SELL-32 / row-block CSR fp64 solve phase; host or GPU SA setup; "
            "NCCL row partition)";
 }
 
 static amg_status check_params(const amg_params& p) {
     if (p.struct_size != sizeof(amg_params)) return set_error(AMG_E_INVALID_ARG, "amg_params: struct_size mismatch");
     if (p.coarsening < 0 || p.coarsening > 1) return set_error(AMG_E_INVALID_ARG, "coarsening must be 0 or 1");
+    if (p.setup_device < 0 || p.setup_device > 1) return set_error(AMG_E_INVALID_ARG, "setup_device must be 0 or 1");
+    if (p.setup_device == 1 && p.device < 0)
+        return set_error(AMG_E_INVALID_ARG, "setup_device = 1 needs a CUDA device (device >= 0)");
     if (p.relax < 0 || p.relax > 2) return set_error(AMG_E_INVALID_ARG, "relax must be 0, 1 or 2");
     if (p.solver < 0 || p.solver > 2) return set_error(AMG_E_INVALID_ARG, "solver must be 0 (cg), 1 (bicgstab) or 2 (gmres)");
     if (p.solver == 2 && (p.gmres_m < 1 || p.gmres_m > amgb::kGmresMaxM))
@@ -2146,7 +2150,8 @@ static amg_status setup_impl(int64_t n, const int64_t* ptr, const int32_t* col, 
         sp.max_levels = prm.max_levels;
         sp.dense_max = prm.dense_max;
         const auto t0 = std::chrono::steady_clock::now();
-        H->host = build_hierarchy(std::move(A0), sp);
+        H->host = prm.setup_device == 1 ? build_hierarchy_gpu(std::move(A0), sp, prm.device)
+                                        : build_hierarchy(std::move(A0), sp);
         const auto t1 = std::chrono::steady_clock::now();
         H->lg = first_replicated_level(H->host, nranks, gather_below);
         H->starts = level_starts(H->host, nranks, H->lg);

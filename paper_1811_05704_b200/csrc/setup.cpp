@@ -474,14 +474,19 @@ HostHierarchy build_hierarchy(Csr A0, const SetupParams& prm) {
         H.levels.back().A = std::move(Ac);
         eps *= prm.eps_decay;
     }
+    finish_hierarchy(H, prm);
+    lap("coarse inv", H.levels.size() - 1);
+    return H;
+}
+
+// The coarsest level: size check and dense inverse (shared by the GPU setup).
+void finish_hierarchy(HostHierarchy& H, const SetupParams& prm) {
     HostLevel& C = H.levels.back();
     if (C.A.nrows > prm.dense_max)
         fail(-5, "coarsest level has " + std::to_string(C.A.nrows) + " rows > dense_max");
     // positive diagonal is required on the coarsest level too (strength() checks
     // the others)
     H.coarse_inv = dense_inverse(C.A);
-    lap("coarse inv", H.levels.size() - 1);
-    return H;
 }
 
 }  // namespace amgb

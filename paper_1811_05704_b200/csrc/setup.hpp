@@ -64,4 +64,12 @@ Csr multiply(const Csr& A, const Csr& B);
 
 HostHierarchy build_hierarchy(Csr A0, const SetupParams& prm);
 
+// The same hierarchy with the numeric steps on CUDA device `device` (gsetup.cu;
+// aggregation and the coarse inverse on the host).  Bitwise equal to
+// build_hierarchy.
+HostHierarchy build_hierarchy_gpu(Csr A0, const SetupParams& prm, int device);
+
+// Coarsest-level check and dense inverse (the tail of both builders).
+void finish_hierarchy(HostHierarchy& H, const SetupParams& prm);
+
 }  // namespace amgb
