@@ -287,6 +287,8 @@ def main():
     ptr, col, val, f = problem_arrays(args.problem, args.n)
     n, nnz = len(f), int(ptr[-1])
     prm = {"precond.relax.type": cfg["relax"], "solver.type": cfg["solver"], "precision": args.precision}
+    torch.empty(1, device=f"cuda:{local}")  # CUDA context creation stays outside setup_s
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
     if world == 1:
         h = amgb.setup(ptr, col, val, prm, device=local, use_graph=0 if args.no_graph else 1)
@@ -441,6 +443,8 @@ def main():
                 "dict_slice_frac_A0": round(infos[0]["dict_slices_A"] / max(1, (infos[0]["rows"] + 31) // 32), 4),
                 "iters_per_solve": iters_all[-1], "rel_resid": rels[-1], "status": statuses[-1],
                 "solve_ms": t_max_ms / args.steps, "setup_s": setup_s,
+                "setup": "numeric steps on the GPU (strength, P, R, RAP, smoother), aggregation + coarse inverse on "
+                         "the host; CUDA context created before the timer" if cfg.get("setup_device", 1) else "host",
                 "l2": "inputs larger than L2 (level-0 matrix %.2f GB + hierarchy vs 126 MB L2); no flush"
                       % (12e-9 * nnz),
                 "solve_alg_GBps": solve_gbs, "solve_roofline_frac": solve_gbs / peak,

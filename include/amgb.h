@@ -80,11 +80,11 @@ typedef struct {
                                method and its A stay fp64).  SURVEY §8f rank 2; value types
                                "double or float", PAPER.md:186-191 */
     int32_t gmres_m;        /* GMRES restart length m in [1, 64] [30] ("solver.M") */
-    int32_t setup_device;   /* 0: hierarchy built on the host [0]; 1: its numeric steps (strength,
-                               smoothed P, R = P^T, A P, R(AP), smoother data) on the CUDA device,
-                               aggregation and the coarse inverse on the host -- bitwise the same
-                               hierarchy (Algorithm 1).
-                               Needs device >= 0. */
+    int32_t setup_device;   /* 1: the hierarchy's numeric steps (strength, smoothed P, R = P^T, A P,
+                               R(AP), smoother data) run on the CUDA device, aggregation and the
+                               coarse inverse on the host [1]; 0: everything on the host.  Bitwise
+                               the same hierarchy either way (Algorithm 1,
+                               PAPER.md:95-107).  Host-only handles (device = -1) use the host. */
 } amg_params;
 
 /* Per-level statistics (amg_level_info). */

@@ -348,9 +348,13 @@ struct Handle {
         void* p = nullptr;
         ck(cudaMalloc(&p, std::max<size_t>(v.size(), 1) * sizeof(T)), "cudaMalloc");
         allocs.push_back(p);
+        const auto t0 = std::chrono::steady_clock::now();
         if (!v.empty()) ck(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+        upload_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        upload_bytes += (double)v.size() * sizeof(T);
         return static_cast<T*>(p);
     }
+    double upload_ms = 0, upload_bytes = 0;  // setup statistics (AMGB_SETUP_TIMING)
     ~Handle() {
         free_batch();
         free_gmres();
@@ -2074,7 +2078,7 @@ void amg_params_default(amg_params* p) {
     p->use_graph = 1;
     p->precision = 0;
     p->gmres_m = 30;
-    p->setup_device = 0;
+    p->setup_device = 1;
 }
 
 const char* amg_last_error(void) { return amgb::g_err.c_str(); }
@@ -2088,8 +2092,6 @@ static amg_status check_params(const amg_params& p) {
     if (p.struct_size != sizeof(amg_params)) return set_error(AMG_E_INVALID_ARG, "amg_params: struct_size mismatch");
     if (p.coarsening < 0 || p.coarsening > 1) return set_error(AMG_E_INVALID_ARG, "coarsening must be 0 or 1");
     if (p.setup_device < 0 || p.setup_device > 1) return set_error(AMG_E_INVALID_ARG, "setup_device must be 0 or 1");
-    if (p.setup_device == 1 && p.device < 0)
-        return set_error(AMG_E_INVALID_ARG, "setup_device = 1 needs a CUDA device (device >= 0)");
     if (p.relax < 0 || p.relax > 2) return set_error(AMG_E_INVALID_ARG, "relax must be 0, 1 or 2");
     if (p.solver < 0 || p.solver > 2) return set_error(AMG_E_INVALID_ARG, "solver must be 0 (cg), 1 (bicgstab) or 2 (gmres)");
     if (p.solver == 2 && (p.gmres_m < 1 || p.gmres_m > amgb::kGmresMaxM))
@@ -2150,7 +2152,7 @@ static amg_status setup_impl(int64_t n, const int64_t* ptr, const int32_t* col, 
         sp.max_levels = prm.max_levels;
         sp.dense_max = prm.dense_max;
         const auto t0 = std::chrono::steady_clock::now();
-        H->host = prm.setup_device == 1 ? build_hierarchy_gpu(std::move(A0), sp, prm.device)
+        H->host = prm.setup_device == 1 && prm.device >= 0 ? build_hierarchy_gpu(std::move(A0), sp, prm.device)
                                         : build_hierarchy(std::move(A0), sp);
         const auto t1 = std::chrono::steady_clock::now();
         H->lg = first_replicated_level(H->host, nranks, gather_below);
@@ -2179,7 +2181,12 @@ static amg_status setup_impl(int64_t n, const int64_t* ptr, const int32_t* col, 
         return AMG_OK;
     }
     try {
+        const auto tc = std::chrono::steady_clock::now();
         ck(cudaSetDevice(prm.device), "cudaSetDevice");
+        ck(cudaFree(nullptr), "context");
+        if (std::getenv("AMGB_SETUP_TIMING"))
+            std::fprintf(stderr, "[setup] CUDA context %.1f ms\n",
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tc).count());
         H->device = prm.device;
         ck(cudaDeviceGetAttribute(&H->num_sms, cudaDevAttrMultiProcessorCount, prm.device), "attr");
         ck(cudaEventCreate(&H->ev0), "event");
@@ -2192,7 +2199,12 @@ static amg_status setup_impl(int64_t n, const int64_t* ptr, const int32_t* col, 
             ckn(nccl_comm_init(&H->nccl, nranks, nccl_id, rank), "ncclCommInitRank");
         }
         H->parts.resize(H->host_parts.size());
+        const auto tu = std::chrono::steady_clock::now();
         for (size_t i = 0; i < H->parts.size(); ++i) upload_part(*H, H->host_parts[i], H->parts[i]);
+        if (std::getenv("AMGB_SETUP_TIMING"))
+            std::fprintf(stderr, "[setup] device store %.1f ms (H2D %.2f GB in %.1f ms)\n",
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tu).count(),
+                         H->upload_bytes / 1e9, H->upload_ms);
         if (H->virt) {
             std::vector<double*> ptrs;
             for (auto& p : H->parts) ptrs.push_back(p.red.defer);
