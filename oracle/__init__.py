@@ -123,6 +123,10 @@ def lib():
             L.or_gmres.argtypes = [_P, C.c_int64, _I64P, _I32P, _F64P, C.c_int, C.c_int32, _F64P, _F64P,
                                    C.c_double, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_double),
                                    C.POINTER(C.c_int32), C.c_void_p]
+            L.or_idrs_shadow.argtypes = [C.c_int64, C.c_int32, _F64P]
+            L.or_idrs.argtypes = [_P, C.c_int64, _I64P, _I32P, _F64P, C.c_int, C.c_int32, C.c_double, C.c_void_p,
+                                  _F64P, _F64P, C.c_double, C.c_int32, C.POINTER(C.c_int32),
+                                  C.POINTER(C.c_double), C.POINTER(C.c_int32), C.c_void_p]
             _lib = L
     return _lib
 
@@ -369,6 +373,33 @@ def bicgstab(A: Csr, f, x0=None, tol=1e-8, maxiter=100, hier: Hierarchy | None =
                                   1 if hier else 0, f, x, tol, maxiter, C.byref(it),
                                   C.byref(rel), C.byref(vc)))
     return dict(x=x, iters=it.value, rel_resid=rel.value, status=rc, vcycles=vc.value)
+
+
+def idrs_shadow(n, s):
+    """The IDR(s) shadow space P (s x n, row j = column j of the n x s matrix)."""
+    P = np.zeros(n * s)
+    lib().or_idrs_shadow(n, s, P)
+    return P.reshape(s, n)
+
+
+def idrs(A: Csr, f, x0=None, tol=1e-8, maxiter=100, s=4, kappa=0.7, P=None, hier: Hierarchy | None = None,
+         history=False):
+    """Right-preconditioned IDR(s) with bi-orthogonalisation (PAPER.md:212);
+    hier=None means M = I.  P: shadow space (s x n) or None (idrs_shadow)."""
+    n = A.nrows
+    f = np.ascontiguousarray(f, np.float64)
+    x = np.zeros(n) if x0 is None else np.array(x0, np.float64, copy=True)
+    it, rel, vc = C.c_int32(), C.c_double(), C.c_int32()
+    hist = np.zeros(maxiter + 1) if history else None
+    Pa = None if P is None else np.ascontiguousarray(P, np.float64).reshape(-1)
+    rc = _check(lib().or_idrs(hier._h if hier else None, n, A.ptr, A.col, A.val, 1 if hier else 0, s, kappa,
+                              Pa.ctypes.data_as(C.c_void_p) if Pa is not None else None, f, x, tol, maxiter,
+                              C.byref(it), C.byref(rel), C.byref(vc),
+                              hist.ctypes.data_as(C.c_void_p) if history else None))
+    out = dict(x=x, iters=it.value, rel_resid=rel.value, status=rc, vcycles=vc.value)
+    if history:
+        out["history"] = hist[:it.value + 1]
+    return out
 
 
 def gmres(A: Csr, f, x0=None, tol=1e-8, maxiter=100, m=30, hier: Hierarchy | None = None, history=False):

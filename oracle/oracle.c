@@ -1078,3 +1078,199 @@ int or_gmres(const or_hier *h, int64_t n, const int64_t *ptr, const int32_t *col
     free(u);
     return status;
 }
+
+/* IDR(s) shadow space: P (column-major, P[j*n + i]) from a counter-based
+ * generator -- entry (i, j) = 2 u - 1, u = the top 53 bits of
+ * splitmix64(0x181105704 + j*n + i) / 2^53 -- then orthonormalised by modified
+ * Gram-Schmidt over the columns j = 0..s-1 (the library implements the same
+ * generator on its own: DESIGN.md §8f). */
+static uint64_t splitmix64(uint64_t z) {
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+void or_idrs_shadow(int64_t n, int32_t s, double *P) {
+    for (int32_t j = 0; j < s; j++)
+        for (int64_t i = 0; i < n; i++) {
+            uint64_t z = splitmix64(0x181105704ull + (uint64_t)j * (uint64_t)n + (uint64_t)i);
+            P[(int64_t)j * n + i] = 2.0 * ((double)(z >> 11) * 0x1.0p-53) - 1.0;
+        }
+    for (int32_t j = 0; j < s; j++) {
+        double *pj = P + (int64_t)j * n;
+        for (int32_t q = 0; q < j; q++) {
+            const double *pq = P + (int64_t)q * n;
+            double h = dot(n, pq, pj);
+            for (int64_t i = 0; i < n; i++) pj[i] = pj[i] - h * pq[i];
+        }
+        double nrm = sqrt(dot(n, pj, pj));
+        for (int64_t i = 0; i < n; i++) pj[i] = pj[i] / nrm;
+    }
+}
+
+/* Right-preconditioned IDR(s) with bi-orthogonalisation (PAPER.md:212 lists
+ * IDR(s), citing Sonneveld & van Gijzen 2008; the variant is van Gijzen &
+ * Sonneveld, ACM TOMS 38(1) 2011, "Algorithm 913", with the preconditioner B = M
+ * applied as in their right-preconditioned form):
+ *   r = f - A x;  G = U = 0 (n x s);  M = I (s x s);  om = 1
+ *   while |r| > tol |f|:
+ *     phi = P^T r
+ *     for k = 0 .. s-1:
+ *        solve M[k:s, k:s] c = phi[k:s]                    (lower triangular)
+ *        v = r - G[:, k:s] c;   v = B v
+ *        U[:, k] = U[:, k:s] c + om v;   G[:, k] = A U[:, k]
+ *        for i = 0 .. k-1:  a = (P[:, i], G[:, k]) / M[i, i]
+ *                           G[:, k] -= a G[:, i];  U[:, k] -= a U[:, i]
+ *        M[k:s, k] = P[:, k:s]^T G[:, k];  breakdown if M[k, k] = 0
+ *        beta = phi[k] / M[k, k];  r -= beta G[:, k];  x += beta U[:, k]
+ *        stop if |r| <= tol |f|;   phi[k+1:s] -= beta M[k+1:s, k]
+ *     v = B r;  t = A v
+ *     om = (t, r) / (t, t);  rho = |(t, r)| / (|t| |r|);  if rho < kappa: om *= kappa / rho
+ *     breakdown if om = 0;  x += om v;  r -= om t
+ * kappa = 0.7 ("angle" strategy, the authors' default; 0 = minimal residual).
+ * iters counts preconditioned matrix-vector products (s per cycle + 1);
+ * vcycles = iters when precond.  P: shadow space (column-major n x s) or NULL
+ * for or_idrs_shadow's.  resid_hist (maxiter + 1 or NULL): |r| after each. */
+int or_idrs(const or_hier *h, int64_t n, const int64_t *ptr, const int32_t *col, const double *val,
+            int precond, int32_t s, double kappa, const double *Pin, const double *f, double *x, double tol,
+            int32_t maxiter, int32_t *iters, double *rel_resid, int32_t *vcycles, double *resid_hist) {
+    or_csr A = {n, n, ptr[n], (int64_t *)ptr, (int32_t *)col, (double *)val};
+    *iters = 0;
+    *vcycles = 0;
+    *rel_resid = 0.0;
+    if (s < 1 || s > 64) {
+        set_err("IDR(s): s must be in [1, 64]");
+        return OR_E_INVALID;
+    }
+    double nf = sqrt(dot(n, f, f));
+    if (nf == 0.0) {
+        for (int64_t i = 0; i < n; i++) x[i] = 0.0;
+        if (resid_hist) resid_hist[0] = 0.0;
+        return OR_OK;
+    }
+    size_t bytes = (size_t)n * sizeof(double);
+    double *P = (double *)malloc(bytes * s), *G = (double *)calloc((size_t)n * s, sizeof(double));
+    double *U = (double *)calloc((size_t)n * s, sizeof(double));
+    double *r = (double *)malloc(bytes), *v = (double *)malloc(bytes), *z = (double *)malloc(bytes);
+    double *t = (double *)malloc(bytes), *uk = (double *)malloc(bytes);
+    double *M = (double *)calloc((size_t)s * s, sizeof(double)), *phi = (double *)malloc(sizeof(double) * s);
+    double *c = (double *)malloc(sizeof(double) * s);
+    if (Pin)
+        memcpy(P, Pin, bytes * s);
+    else
+        or_idrs_shadow(n, s, P);
+    for (int32_t i = 0; i < s; i++) M[i * s + i] = 1.0; /* M[row * s + col] */
+    residual(&A, f, x, r);
+    double res = sqrt(dot(n, r, r));
+    if (resid_hist) resid_hist[0] = res;
+    double om = 1.0;
+    int32_t it = 0, vc = 0;
+    int status = OR_OK;
+    int stop = !(res > tol * nf);
+    while (!stop && it < maxiter) {
+        for (int32_t i = 0; i < s; i++) phi[i] = dot(n, P + (int64_t)i * n, r);
+        for (int32_t k = 0; k < s && !stop && it < maxiter; k++) {
+            /* M[k:s, k:s] c = phi[k:s], forward substitution */
+            for (int32_t i = k; i < s; i++) {
+                double sum = phi[i];
+                for (int32_t j = k; j < i; j++) sum -= M[i * s + j] * c[j - k];
+                c[i - k] = sum / M[i * s + i];
+            }
+            for (int64_t q = 0; q < n; q++) {
+                double sum = r[q];
+                for (int32_t j = k; j < s; j++) sum -= c[j - k] * G[(int64_t)j * n + q];
+                v[q] = sum;
+            }
+            if (precond) {
+                or_precond(h, v, z);
+                vc++;
+            } else {
+                memcpy(z, v, bytes);
+            }
+            for (int64_t q = 0; q < n; q++) {
+                double sum = om * z[q];
+                for (int32_t j = k; j < s; j++) sum += c[j - k] * U[(int64_t)j * n + q];
+                uk[q] = sum;
+            }
+            memcpy(U + (int64_t)k * n, uk, bytes);
+            double *gk = G + (int64_t)k * n, *ukp = U + (int64_t)k * n;
+            spmv_csr(&A, ukp, gk);
+            for (int32_t i = 0; i < k; i++) {
+                double a = dot(n, P + (int64_t)i * n, gk) / M[i * s + i];
+                for (int64_t q = 0; q < n; q++) {
+                    gk[q] = gk[q] - a * G[(int64_t)i * n + q];
+                    ukp[q] = ukp[q] - a * U[(int64_t)i * n + q];
+                }
+            }
+            for (int32_t i = k; i < s; i++) M[i * s + k] = dot(n, P + (int64_t)i * n, gk);
+            it++;
+            if (M[k * s + k] == 0.0) {
+                set_err("IDR(s) breakdown: M[%d][%d] = 0", k, k);
+                status = OR_BREAKDOWN;
+                stop = 1;
+                break;
+            }
+            double beta = phi[k] / M[k * s + k];
+            for (int64_t q = 0; q < n; q++) {
+                r[q] = r[q] - beta * gk[q];
+                x[q] = x[q] + beta * ukp[q];
+            }
+            res = sqrt(dot(n, r, r));
+            if (resid_hist) resid_hist[it] = res;
+            if (!(res > tol * nf)) {
+                stop = 1;
+                break;
+            }
+            for (int32_t i = k + 1; i < s; i++) phi[i] = phi[i] - beta * M[i * s + k];
+        }
+        if (stop || it >= maxiter) break;
+        /* dimension reduction step */
+        if (precond) {
+            or_precond(h, r, z);
+            vc++;
+        } else {
+            memcpy(z, r, bytes);
+        }
+        spmv_csr(&A, z, t);
+        double tt = sqrt(dot(n, t, t)), tr = dot(n, t, r);
+        it++;
+        if (tt == 0.0) {
+            set_err("IDR(s) breakdown: A B r = 0");
+            status = OR_BREAKDOWN;
+            break;
+        }
+        om = tr / (tt * tt);
+        double rho = fabs(tr) / (tt * res);
+        if (rho < kappa) om = om * kappa / rho;
+        if (om == 0.0) {
+            set_err("IDR(s) breakdown: omega = 0");
+            status = OR_BREAKDOWN;
+            break;
+        }
+        for (int64_t q = 0; q < n; q++) {
+            x[q] = x[q] + om * z[q];
+            r[q] = r[q] - om * t[q];
+        }
+        res = sqrt(dot(n, r, r));
+        if (resid_hist) resid_hist[it] = res;
+        if (!(res > tol * nf)) stop = 1;
+    }
+    if (status == OR_OK && res > tol * nf) status = OR_NOT_CONVERGED;
+    residual(&A, f, x, r);
+    *iters = it;
+    *vcycles = vc;
+    *rel_resid = sqrt(dot(n, r, r)) / nf;
+    free(P);
+    free(G);
+    free(U);
+    free(r);
+    free(v);
+    free(z);
+    free(t);
+    free(uk);
+    free(M);
+    free(phi);
+    free(c);
+    return status;
+}

@@ -117,4 +117,15 @@ int or_gmres(const or_hier *h, int64_t n, const int64_t *ptr, const int32_t *col
              int precond, int32_t m, const double *f, double *x, double tol, int32_t maxiter,
              int32_t *iters, double *rel_resid, int32_t *vcycles, double *resid_hist);
 
+/* IDR(s) shadow space (column-major n x s): counter-based splitmix64 entries in
+ * [-1, 1), orthonormalised by modified Gram-Schmidt. */
+void or_idrs_shadow(int64_t n, int32_t s, double *P);
+/* Right-preconditioned IDR(s) with bi-orthogonalisation (van Gijzen &
+ * Sonneveld 2011, Alg. 913).  kappa: "angle" omega strategy (0.7; 0 = minimal
+ * residual).  P: shadow space or NULL (or_idrs_shadow).  iters = preconditioned
+ * matrix-vector products; resid_hist (maxiter+1 or NULL): |r| after each. */
+int or_idrs(const or_hier *h, int64_t n, const int64_t *ptr, const int32_t *col, const double *val,
+            int precond, int32_t s, double kappa, const double *P, const double *f, double *x, double tol,
+            int32_t maxiter, int32_t *iters, double *rel_resid, int32_t *vcycles, double *resid_hist);
+
 #endif
