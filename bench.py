@@ -150,7 +150,7 @@ def workload_name(args, cfg):
 
 def oracle_solver(cfg):
     import oracle
-    return {"cg": oracle.cg, "bicgstab": oracle.bicgstab, "gmres": oracle.gmres}[cfg["solver"]]
+    return {"cg": oracle.cg, "bicgstab": oracle.bicgstab, "gmres": oracle.gmres, "idrs": oracle.idrs}[cfg["solver"]]
 
 
 def cpu_baseline_full_solve(ptr, col, val, f, cfg, tol, maxiter):

@@ -72,7 +72,8 @@ typedef struct {
     int64_t coarse_enough;  /* stop coarsening at <= this many rows [3000] */
     int32_t max_levels;     /* [30] */
     int64_t dense_max;      /* error if the coarsest level is larger [20000] */
-    int32_t solver;         /* "solver.type": 0 cg [0], 1 bicgstab, 2 gmres (restarted, right-preconditioned) */
+    int32_t solver;         /* "solver.type": 0 cg [0], 1 bicgstab, 2 gmres (restarted, right-preconditioned),
+                               3 idrs (IDR(s) with bi-orthogonalisation, right-preconditioned; single GPU) */
     int32_t device;         /* CUDA device ordinal [0]; -1 = host-only handle (setup + export) */
     int32_t use_graph;      /* 1: replay Krylov iterations as a CUDA graph [1] */
     int32_t precision;      /* 0: fp64 throughout [0]; 1: mixed -- the V-cycle reads fp32 copies of
@@ -85,6 +86,7 @@ typedef struct {
                                coarse inverse on the host [1]; 0: everything on the host.  Bitwise
                                the same hierarchy either way (Algorithm 1,
                                PAPER.md:95-107).  Host-only handles (device = -1) use the host. */
+    int32_t idrs_s;         /* IDR(s) shadow-space dimension s in {1, 2, 4, 8} [4] ("solver.s") */
 } amg_params;
 
 /* Per-level statistics (amg_level_info). */

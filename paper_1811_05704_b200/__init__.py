@@ -61,6 +61,7 @@ class AmgParams(C.Structure):
         ("precision", C.c_int32),
         ("gmres_m", C.c_int32),
         ("setup_device", C.c_int32),
+        ("idrs_s", C.c_int32),
     ]
 
 
@@ -140,7 +141,7 @@ SYMBOLS = ("amg_params_default", "amg_setup", "amg_solve", "amg_solve_host", "am
 
 RELAX = {"spai0": 0, "damped_jacobi": 1, "chebyshev": 2}
 COARSENING = {"smoothed_aggregation": 0, "aggregation": 1}
-SOLVER = {"cg": 0, "bicgstab": 1, "gmres": 2}
+SOLVER = {"cg": 0, "bicgstab": 1, "gmres": 2, "idrs": 3}
 
 # dotted keys (Listing 2 style) -> amg_params field
 PARAM_KEYS = {
@@ -164,6 +165,7 @@ PARAM_KEYS = {
     "precision": "precision",
     "solver.M": "gmres_m",
     "setup.device": "setup_device",
+    "solver.s": "idrs_s",
 }
 PRECISION = {"double": 0, "mixed": 1}
 SETUP_DEVICE = {"host": 0, "gpu": 1}

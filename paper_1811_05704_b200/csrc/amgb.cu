@@ -32,6 +32,7 @@
 #include "comm.hpp"
 #include "dist.hpp"
 #include "gmres.cuh"
+#include "idrs.cuh"
 #include "kernels.cuh"
 #include "ops.cuh"
 #include "setup.hpp"
@@ -358,6 +359,7 @@ struct Handle {
     ~Handle() {
         free_batch();
         free_gmres();
+        free_idr();
         if (graph) cudaGraphExecDestroy(graph);
         for (cudaEvent_t e : ev_all) cudaEventDestroy(e);
         for (void* p : allocs) cudaFree(p);
@@ -450,6 +452,25 @@ struct Handle {
         for (void* p : gm.mem) cudaFree(p);
         if (gm.ks_host) cudaFreeHost(gm.ks_host);
         gm = Gmres{};
+    }
+    // ---- IDR(s) buffers (single part)
+    struct Idr {
+        int s = 0;
+        double *P = nullptr, *G = nullptr, *U = nullptr, *v = nullptr, *z = nullptr, *t = nullptr, *r = nullptr;
+        KStateI* ks = nullptr;
+        KStateI* ks_host = nullptr;
+        std::vector<void*> mem;
+        cudaGraphExec_t graph = nullptr;
+        const double* graph_x = nullptr;
+        const double* graph_f = nullptr;
+        std::vector<Rec> rec;
+        int64_t graph_kernels = 0;
+    } idr;
+    void free_idr() {
+        if (idr.graph) cudaGraphExecDestroy(idr.graph);
+        for (void* p : idr.mem) cudaFree(p);
+        if (idr.ks_host) cudaFreeHost(idr.ks_host);
+        idr = Idr{};
     }
     void free_batch() {
         if (batch.graph) cudaGraphExecDestroy(batch.graph);
@@ -755,6 +776,11 @@ struct Handle {
     void gmres_step(int j);
     void gmres_cycle_end(const double* f, double* x);
     amg_status solve_gmres(const double* f, double* x, double tol, int32_t maxiter, int32_t* iters, double* rel);
+    template <int S>
+    void idr_cycle(double* x);
+    template <int S>
+    amg_status solve_idrs_t(const double* f, double* x, double tol, int32_t maxiter, int32_t* iters, double* rel);
+    amg_status solve_idrs(const double* f, double* x, double tol, int32_t maxiter, int32_t* iters, double* rel);
     void bicgstab_iteration();
     amg_status solve(const double* f, double* x, double tol, int32_t maxiter, int32_t* iters, double* rel);
     void precond(const double* r, double* z);
@@ -1744,6 +1770,227 @@ amg_status Handle::solve_gmres(const double* f, double* x, double tol, int32_t m
     return st;
 }
 
+// IDR(s) shadow space P (s x n, row m = column m): the counter-based generator
+// of oracle/oracle.c or_idrs_shadow, written independently -- entry (i, m) =
+// 2 u - 1, u = top 53 bits of splitmix64(0x181105704 + m n + i) / 2^53 -- then
+// modified Gram-Schmidt in the same order (host, no FP contraction).
+static uint64_t idr_splitmix64(uint64_t z) {
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+static std::vector<double> idr_shadow(int64_t n, int s) {
+    std::vector<double> P((size_t)n * s);
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < n * s; ++e) {
+        const uint64_t z = idr_splitmix64(0x181105704ull + (uint64_t)e);
+        P[e] = 2.0 * ((double)(z >> 11) * 0x1.0p-53) - 1.0;
+    }
+    for (int j = 0; j < s; ++j) {
+        double* pj = P.data() + (int64_t)j * n;
+        for (int q = 0; q < j; ++q) {
+            const double* pq = P.data() + (int64_t)q * n;
+            double h = 0.0;
+            for (int64_t i = 0; i < n; ++i) h += pq[i] * pj[i];
+            for (int64_t i = 0; i < n; ++i) pj[i] = pj[i] - h * pq[i];
+        }
+        double nn = 0.0;
+        for (int64_t i = 0; i < n; ++i) nn += pj[i] * pj[i];
+        const double nrm = std::sqrt(nn);
+        for (int64_t i = 0; i < n; ++i) pj[i] = pj[i] / nrm;
+    }
+    return P;
+}
+
+// One IDR(s) cycle: s inner steps (tags 0..s-1) and the dimension reduction
+// (tag s); every kernel is gated by the done flag.
+template <int S>
+void Handle::idr_cycle(double* x) {
+    Part& p = parts[0];
+    const int64_t n = p.lv[0].n;
+    const int32_t* gate = &idr.ks->done;
+    GSel g = [gate](Part&) { return gate; };
+    for (int k = 0; k < S; ++k) {
+        cur_iter = k;
+        launch(AMG_PROF_VECTOR, 0, "idr c", [&] { idr_solve_c<<<1, 1, 0, stream>>>(idr.ks, k); });
+        launch(AMG_PROF_VECTOR, 8.0 * (S - k + 2) * n, "idr v = r - G c", [&] {
+            vec_kernel<VIdrV<S>><<<grid_for(n), kBlock, 0, stream>>>(
+                n, VIdrV<S>{idr.v, idr.r, idr.G, n, k, idr.ks, {}, {}}, gate, p.red);
+        });
+        vcycle(0, [this](Part&) { return (const double*)idr.v; }, [this](Part&) { return idr.z; }, g, false);
+        launch(AMG_PROF_VECTOR, 8.0 * (S - k + 2) * n, "idr U_k", [&] {
+            vec_kernel<VIdrU<S>><<<grid_for(n), kBlock, 0, stream>>>(
+                n, VIdrU<S>{idr.U, idr.z, n, k, idr.ks, {}, {}, 0.0}, gate, p.red);
+        });
+        rows(p, p.lv[0].A,
+             OpIdrG<S>{idr.U + (int64_t)k * n, idr.G + (int64_t)k * n, idr.P, n, FinIdrOrth{idr.ks, k}}, gate,
+             "idr G_k = A U_k + P^T G_k");
+        launch(AMG_PROF_VECTOR, 8.0 * (4 * k + 6) * n, "idr update", [&] {
+            vec_kernel<VIdrUpd<S>><<<grid_for(n), kBlock, 0, stream>>>(
+                n, VIdrUpd<S>{idr.G, idr.U, idr.r, x, n, k, idr.ks, FinIdrRes{idr.ks}, {}, 0.0}, gate, p.red);
+        });
+    }
+    cur_iter = S;
+    vcycle(0, [this](Part&) { return (const double*)idr.r; }, [this](Part&) { return idr.z; }, g, false);
+    rows(p, p.lv[0].A, OpIdrT{idr.z, idr.t, idr.r, FinIdrOmega{idr.ks}}, gate, "idr t = A z");
+    launch(AMG_PROF_VECTOR, 8.0 * (6 + S) * n, "idr reduction update", [&] {
+        vec_kernel<VIdrRed<S>><<<grid_for(n), kBlock, 0, stream>>>(
+            n, VIdrRed<S>{x, idr.r, idr.z, idr.t, idr.P, n, idr.ks, FinIdrCycle<S>{idr.ks}, 0.0}, gate, p.red);
+    });
+    cur_iter = -1;
+}
+
+template <int S>
+amg_status Handle::solve_idrs_t(const double* f, double* x, double tol, int32_t maxiter, int32_t* iters,
+                                double* rel) {
+    Part& p = parts[0];
+    const int64_t n = p.lv[0].n;
+    if (idr.s != S) {
+        free_idr();
+        idr.s = S;
+        auto alloc = [&](int64_t cnt) {
+            void* q = nullptr;
+            ck(cudaMalloc(&q, std::max<int64_t>(cnt, 1) * sizeof(double)), "cudaMalloc (idrs)");
+            idr.mem.push_back(q);
+            return static_cast<double*>(q);
+        };
+        idr.P = alloc((int64_t)S * n);
+        idr.G = alloc((int64_t)S * n);
+        idr.U = alloc((int64_t)S * n);
+        idr.v = alloc(n);
+        idr.z = alloc(n);
+        idr.t = alloc(n);
+        idr.r = alloc(n);
+        const std::vector<double> P = idr_shadow(n, S);
+        ck(cudaMemcpy(idr.P, P.data(), P.size() * sizeof(double), cudaMemcpyHostToDevice), "upload P");
+        void* q = nullptr;
+        ck(cudaMalloc(&q, sizeof(KStateI)), "cudaMalloc");
+        idr.mem.push_back(q);
+        idr.ks = static_cast<KStateI*>(q);
+        ck(cudaMallocHost(&idr.ks_host, sizeof(KStateI)), "cudaMallocHost");
+    }
+    const int64_t launches0 = launches;
+    collect(rec_direct, 0, true);
+    alg_bytes = 0;
+    std::fill(acc_ms, acc_ms + 8, 0.0);
+    std::fill(acc_bytes, acc_bytes + 8, 0.0);
+    std::fill(acc_launches, acc_launches + 8, 0);
+    cur_iter = -1;
+    ck(cudaEventRecord(ev0, stream), "event");
+    KStateI* kh = idr.ks_host;
+    std::memset(kh, 0, sizeof(KStateI));
+    kh->s = S;
+    kh->maxiter = maxiter;
+    kh->om = 1.0;
+    kh->kappa = 0.7;
+    for (int i = 0; i < S; ++i) kh->M[i * S + i] = 1.0;
+    ck(cudaMemcpyAsync(idr.ks, kh, sizeof(KStateI), cudaMemcpyHostToDevice, stream), "ks init");
+    ck(cudaMemsetAsync(idr.G, 0, (size_t)S * n * sizeof(double), stream), "memset");
+    ck(cudaMemsetAsync(idr.U, 0, (size_t)S * n * sizeof(double), stream), "memset");
+    vec(p, n, VNorm2T<FinIdrNorm>{f, FinIdrNorm{idr.ks, tol}}, nullptr, "norm f");
+    rows(p, p.lv[0].A, OpResidual<1, FinIdrRes0>{x, f, idr.r, FinIdrRes0{idr.ks}}, nullptr, "idr r0");
+    launch(AMG_PROF_VECTOR, 8.0 * (1 + S) * n, "idr phi", [&] {
+        vec_kernel<VIdrPhi<S>><<<grid_for(n), kBlock, 0, stream>>>(n, VIdrPhi<S>{idr.r, idr.P, n, {idr.ks}}, nullptr,
+                                                                   p.red);
+    });
+    ck(cudaMemcpyAsync(kh, idr.ks, sizeof(KStateI), cudaMemcpyDeviceToHost, stream), "ks read");
+    ck(cudaStreamSynchronize(stream), "sync");
+    collect(rec_direct, 0, true);
+    if (kh->nf == 0.0) {  // zero right-hand side: x = 0
+        ck(cudaMemsetAsync(x, 0, n * sizeof(double), stream), "memset");
+        ck(cudaStreamSynchronize(stream), "sync");
+        *iters = 0;
+        *rel = 0.0;
+        stats = amg_solve_stats{};
+        stats.kernel_launches = launches - launches0;
+        return AMG_OK;
+    }
+    const bool use_graph = prm.use_graph && !sync_debug;
+    while (!kh->done) {
+        const int it_before = kh->it;
+        if (use_graph) {  // one cycle (s gated steps + the reduction) per graph launch
+            if (!idr.graph || idr.graph_x != x || idr.graph_f != f) {
+                if (idr.graph) cudaGraphExecDestroy(idr.graph);
+                idr.graph = nullptr;
+                cudaGraph_t g;
+                const int64_t before = launches;
+                const int saved_mask = prof_mask;
+                prof_mask = 0;
+                std::vector<Rec> saved;
+                saved.swap(rec_graph);
+                ck(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "capture");
+                capturing = true;
+                try {
+                    idr_cycle<S>(x);
+                } catch (...) {
+                    cur_iter = -1;
+                    capturing = false;
+                    prof_mask = saved_mask;
+                    cudaStreamEndCapture(stream, &g);
+                    rec_graph.swap(saved);
+                    throw;
+                }
+                capturing = false;
+                prof_mask = saved_mask;
+                ck(cudaStreamEndCapture(stream, &g), "end capture");
+                idr.rec.swap(rec_graph);
+                rec_graph.swap(saved);
+                idr.graph_kernels = launches - before;
+                launches = before;
+                ck(cudaGraphInstantiate(&idr.graph, g, 0), "instantiate");
+                cudaGraphDestroy(g);
+                idr.graph_x = x;
+                idr.graph_f = f;
+            }
+            ck(cudaGraphLaunch(idr.graph, stream), "graph launch");
+            launches += idr.graph_kernels;
+            ck(cudaMemcpyAsync(kh, idr.ks, sizeof(KStateI), cudaMemcpyDeviceToHost, stream), "ks read");
+            ck(cudaStreamSynchronize(stream), "sync");
+            collect(idr.rec, kh->it - it_before, false);  // the steps that ran
+        } else {
+            idr_cycle<S>(x);
+            ck(cudaMemcpyAsync(kh, idr.ks, sizeof(KStateI), cudaMemcpyDeviceToHost, stream), "ks read");
+            ck(cudaStreamSynchronize(stream), "sync");
+            collect(rec_direct, 0, true);
+        }
+    }
+    rows(p, p.lv[0].A, OpResidual<1, FinTrueResI>{x, f, idr.r, FinTrueResI{idr.ks}}, nullptr, "true res");
+    ck(cudaEventRecord(ev1, stream), "event");
+    ck(cudaMemcpyAsync(kh, idr.ks, sizeof(KStateI), cudaMemcpyDeviceToHost, stream), "ks read");
+    ck(cudaStreamSynchronize(stream), "sync");
+    collect(rec_direct, 0, true);
+    *iters = kh->it;
+    *rel = kh->res / kh->nf;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev0, ev1);
+    stats = amg_solve_stats{};
+    stats.iters = kh->it;
+    stats.vcycles = kh->it;
+    stats.kernel_launches = launches - launches0;
+    stats.solve_ms = ms;
+    stats.rel_resid = *rel;
+    stats.alg_bytes = alg_bytes;
+    if (kh->status == AMG_BREAKDOWN) {
+        g_err = "IDR(s) breakdown: M[k][k] = 0 or omega = 0";
+        stats.status = AMG_BREAKDOWN;
+        return AMG_BREAKDOWN;
+    }
+    const amg_status st = *rel <= tol ? AMG_OK : AMG_NOT_CONVERGED;
+    stats.status = st;
+    return st;
+}
+
+amg_status Handle::solve_idrs(const double* f, double* x, double tol, int32_t maxiter, int32_t* iters, double* rel) {
+    switch (prm.idrs_s) {
+        case 1: return solve_idrs_t<1>(f, x, tol, maxiter, iters, rel);
+        case 2: return solve_idrs_t<2>(f, x, tol, maxiter, iters, rel);
+        case 4: return solve_idrs_t<4>(f, x, tol, maxiter, iters, rel);
+        default: return solve_idrs_t<8>(f, x, tol, maxiter, iters, rel);
+    }
+}
+
 // z = M r for every part (r, z: device; global vectors in virtual mode).
 void Handle::precond(const double* r, double* z) {
     GSel nogate = [](Part&) { return (const int32_t*)nullptr; };
@@ -2006,7 +2253,7 @@ void upload_part(Handle& H, const RankPart& RP, Part& P) {
     ck(cudaMalloc(&pp, sizeof(KState)), "cudaMalloc");
     H.allocs.push_back(pp);
     P.ks = static_cast<KState*>(pp);
-    ck(cudaMalloc(&pp, (size_t)H.num_sms * 8 * kMaxK * sizeof(double)), "cudaMalloc");
+    ck(cudaMalloc(&pp, (size_t)H.num_sms * 8 * 16 * sizeof(double)), "cudaMalloc");  // <= 16 dots per reduction
     H.allocs.push_back(pp);
     P.red.partial = static_cast<double*>(pp);
     ck(cudaMalloc(&pp, 64), "cudaMalloc");
@@ -2079,6 +2326,7 @@ void amg_params_default(amg_params* p) {
     p->precision = 0;
     p->gmres_m = 30;
     p->setup_device = 1;
+    p->idrs_s = 4;
 }
 
 const char* amg_last_error(void) { return amgb::g_err.c_str(); }
@@ -2093,7 +2341,10 @@ static amg_status check_params(const amg_params& p) {
     if (p.coarsening < 0 || p.coarsening > 1) return set_error(AMG_E_INVALID_ARG, "coarsening must be 0 or 1");
     if (p.setup_device < 0 || p.setup_device > 1) return set_error(AMG_E_INVALID_ARG, "setup_device must be 0 or 1");
     if (p.relax < 0 || p.relax > 2) return set_error(AMG_E_INVALID_ARG, "relax must be 0, 1 or 2");
-    if (p.solver < 0 || p.solver > 2) return set_error(AMG_E_INVALID_ARG, "solver must be 0 (cg), 1 (bicgstab) or 2 (gmres)");
+    if (p.solver < 0 || p.solver > 3)
+        return set_error(AMG_E_INVALID_ARG, "solver must be 0 (cg), 1 (bicgstab), 2 (gmres) or 3 (idrs)");
+    if (p.solver == 3 && p.idrs_s != 1 && p.idrs_s != 2 && p.idrs_s != 4 && p.idrs_s != 8)
+        return set_error(AMG_E_INVALID_ARG, "IDR(s): s must be 1, 2, 4 or 8");
     if (p.solver == 2 && (p.gmres_m < 1 || p.gmres_m > amgb::kGmresMaxM))
         return set_error(AMG_E_INVALID_ARG, "gmres_m in [1, 64]");
     if (p.npre < 0 || p.npost < 0 || p.npre + p.npost < 1)
@@ -2269,6 +2520,10 @@ amg_status amg_solve(amg_handle h, const double* f, double* x, double tol, int32
             if (h->h->distributed()) return set_error(AMG_E_INVALID_ARG, "GMRES: single-GPU handles only");
             return h->h->solve_gmres(f, x, tol, maxiter, iters, rel);
         }
+        if (h->h->prm.solver == 3) {
+            if (h->h->distributed()) return set_error(AMG_E_INVALID_ARG, "IDR(s): single-GPU handles only");
+            return h->h->solve_idrs(f, x, tol, maxiter, iters, rel);
+        }
         return h->h->solve(f, x, tol, maxiter, iters, rel);
     } catch (const amgb::CudaError& e) {
         cudaGetLastError();
@@ -2293,8 +2548,9 @@ amg_status amg_solve_host(amg_handle h, const double* f, const double* x0, doubl
             ck(cudaMemcpyAsync(H.hx, x0, n * sizeof(double), cudaMemcpyHostToDevice, H.stream), "H2D x0");
         else
             ck(cudaMemsetAsync(H.hx, 0, n * sizeof(double), H.stream), "zero x0");
-        amg_status st = H.prm.solver == 2 && !H.distributed() ? H.solve_gmres(H.hf, H.hx, tol, maxiter, iters, rel)
-                                                               : H.solve(H.hf, H.hx, tol, maxiter, iters, rel);
+        amg_status st = H.prm.solver == 2 && !H.distributed()   ? H.solve_gmres(H.hf, H.hx, tol, maxiter, iters, rel)
+                        : H.prm.solver == 3 && !H.distributed() ? H.solve_idrs(H.hf, H.hx, tol, maxiter, iters, rel)
+                                                                : H.solve(H.hf, H.hx, tol, maxiter, iters, rel);
         ck(cudaMemcpyAsync(x, H.hx, n * sizeof(double), cudaMemcpyDeviceToHost, H.stream), "D2H x");
         ck(cudaStreamSynchronize(H.stream), "sync");
         return st;
