@@ -2052,7 +2052,22 @@ std::vector<int32_t> row_blocks(const Csr& A, int G) {
     return b;
 }
 
+DMat upload_mat_impl(Handle& H, const Csr& A, int64_t* bytes, bool f32);
+
+// upload_mat with AMGB_SETUP_TIMING: per-matrix conversion + copy time
 DMat upload_mat(Handle& H, const Csr& A, int64_t* bytes, bool f32 = false) {
+    const auto t0 = std::chrono::steady_clock::now();
+    const double up0 = H.upload_ms;
+    DMat d = upload_mat_impl(H, A, bytes, f32);
+    if (std::getenv("AMGB_SETUP_TIMING"))
+        std::fprintf(stderr, "[setup]   matrix %lld x %lld, %lld nnz, fmt %d: %.1f ms (H2D %.1f ms)\n",
+                     (long long)A.nrows, (long long)A.ncols, (long long)A.nnz(), (int)d.fmt,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(),
+                     H.upload_ms - up0);
+    return d;
+}
+
+DMat upload_mat_impl(Handle& H, const Csr& A, int64_t* bytes, bool f32) {
     DMat d;
     d.nrows = A.nrows;
     d.ncols = A.ncols;
