@@ -102,11 +102,34 @@ inline void ckn(int r, const char* what) {
     }
 }
 
+// Host staging vectors for the device store: default-initialised (no zero fill),
+// so the parallel loops that write every element also do the first touch.
+template <class T>
+struct UninitAlloc : std::allocator<T> {
+    template <class U>
+    struct rebind {
+        using other = UninitAlloc<U>;
+    };
+    UninitAlloc() = default;
+    template <class U>
+    UninitAlloc(const UninitAlloc<U>&) {}
+    template <class U, class... Args>
+    void construct(U* p, Args&&... args) {
+        ::new ((void*)p) U(std::forward<Args>(args)...);
+    }
+    template <class U>
+    void construct(U* p) {
+        ::new ((void*)p) U;
+    }
+};
+template <class T>
+using hvec = std::vector<T, UninitAlloc<T>>;
+
 struct HostSell {
     int64_t nrows = 0, ncols = 0, nslices = 0;
     std::vector<int64_t> sptr;
-    std::vector<int32_t> col;
-    std::vector<double> val;
+    hvec<int32_t> col;
+    hvec<double> val;
 };
 
 // CSR -> SELL-C, slice height C (see kernels.cuh): entry k of row s*C + r at
@@ -123,8 +146,8 @@ HostSell to_sell(const Csr& A, int C = 32) {
             w = std::max<int64_t>(w, A.ptr[r + 1] - A.ptr[r]);
         S.sptr[s + 1] = S.sptr[s] + C * w;
     }
-    S.col.assign(S.sptr[S.nslices], 0);
-    S.val.assign(S.sptr[S.nslices], 0.0);
+    S.col.resize(S.sptr[S.nslices]);  // every element written below (entries + padding)
+    S.val.resize(S.sptr[S.nslices]);
 #pragma omp parallel for schedule(static)
     for (int64_t s = 0; s < S.nslices; ++s) {
         const int64_t w = (S.sptr[s + 1] - S.sptr[s]) / C;
@@ -160,51 +183,58 @@ HostSell to_sell(const Csr& A, int C = 32) {
 // cptr[s+1] - cptr[s] < 32 w.
 struct HostTmaCols {
     std::vector<int64_t> cptr;
-    std::vector<int32_t> col;
+    hvec<int32_t> col;
     int64_t idx_bytes = 0;  // index bytes the format needs (excl. alignment/padding)
     int64_t ndict = 0;      // dictionary slices
 };
 
 HostTmaCols tma_cols(const Csr& A, HostSell& S, bool allow_dict) {
     constexpr int C = 32;
+    constexpr int kW = 16;  // dictionary slices have at most kW offsets
     const int64_t ns = S.nslices;
-    std::vector<std::vector<int32_t>> U(ns);
-    std::vector<int64_t> true_nnz(ns, 0);
-#pragma omp parallel for schedule(dynamic, 1024)
-    for (int64_t s = 0; s < ns; ++s) {
-        const int64_t w = (S.sptr[s + 1] - S.sptr[s]) / C;
-        const int64_t r0 = s * C, r1 = std::min<int64_t>(A.nrows, r0 + C);
-        true_nnz[s] = A.ptr[r1] - A.ptr[r0];
-        if (!allow_dict || w == 0 || r1 - r0 < C) continue;
-        std::vector<int64_t> offs;
-        offs.reserve((size_t)true_nnz[s]);
-        for (int64_t r = r0; r < r1; ++r)
-            for (int64_t e = A.ptr[r]; e < A.ptr[r + 1]; ++e) offs.push_back((int64_t)A.col[e] - r);
-        std::sort(offs.begin(), offs.end());
-        offs.erase(std::unique(offs.begin(), offs.end()), offs.end());
-        if ((int64_t)offs.size() != w) continue;
-        bool ok = true;
-        for (int64_t r = r0; r < r1 && ok; ++r)
-            ok = r + offs.front() >= 0 && r + offs.back() < A.ncols;
-        if (!ok) continue;
-        U[s].assign(offs.begin(), offs.end());
-        // values at U's positions (the row's entries are ascending, so are U's)
-        for (int lane = 0; lane < C; ++lane) {
-            const int64_t r = r0 + lane;
-            int64_t k = 0;
-            for (int64_t e = A.ptr[r]; e < A.ptr[r + 1]; ++e) {
-                const int64_t u = (int64_t)A.col[e] - r;
-                for (; U[s][k] != u; ++k) {
-                    S.val[S.sptr[s] + C * k + lane] = 0.0;
-                    S.col[S.sptr[s] + C * k + lane] = (int32_t)(r + U[s][k]);
+    hvec<int32_t> U((size_t)ns * kW);
+    hvec<int32_t> ulen(ns);  // offsets in the slice's dictionary (0: explicit slice)
+    hvec<int64_t> true_nnz(ns);
+#pragma omp parallel
+    {
+        std::vector<int64_t> offs(C * kW);
+#pragma omp for schedule(dynamic, 1024)
+        for (int64_t s = 0; s < ns; ++s) {
+            ulen[s] = 0;
+            const int64_t w = (S.sptr[s + 1] - S.sptr[s]) / C;
+            const int64_t r0 = s * C, r1 = std::min<int64_t>(A.nrows, r0 + C);
+            true_nnz[s] = A.ptr[r1] - A.ptr[r0];
+            if (!allow_dict || w == 0 || w > kW || r1 - r0 < C) continue;
+            size_t no = 0;
+            for (int64_t r = r0; r < r1; ++r)
+                for (int64_t e = A.ptr[r]; e < A.ptr[r + 1]; ++e) offs[no++] = (int64_t)A.col[e] - r;
+            std::sort(offs.begin(), offs.begin() + no);
+            no = std::unique(offs.begin(), offs.begin() + no) - offs.begin();
+            if ((int64_t)no != w) continue;
+            bool ok = true;
+            for (int64_t r = r0; r < r1 && ok; ++r) ok = r + offs[0] >= 0 && r + offs[no - 1] < A.ncols;
+            if (!ok) continue;
+            int32_t* u = U.data() + (size_t)s * kW;
+            for (size_t k = 0; k < no; ++k) u[k] = (int32_t)offs[k];
+            ulen[s] = (int32_t)no;
+            // values at U's positions (the row's entries are ascending, so are U's)
+            for (int lane = 0; lane < C; ++lane) {
+                const int64_t r = r0 + lane;
+                int64_t k = 0;
+                for (int64_t e = A.ptr[r]; e < A.ptr[r + 1]; ++e) {
+                    const int64_t off = (int64_t)A.col[e] - r;
+                    for (; u[k] != off; ++k) {
+                        S.val[S.sptr[s] + C * k + lane] = 0.0;
+                        S.col[S.sptr[s] + C * k + lane] = (int32_t)(r + u[k]);
+                    }
+                    S.val[S.sptr[s] + C * k + lane] = A.val[e];
+                    S.col[S.sptr[s] + C * k + lane] = A.col[e];
+                    ++k;
                 }
-                S.val[S.sptr[s] + C * k + lane] = A.val[e];
-                S.col[S.sptr[s] + C * k + lane] = A.col[e];
-                ++k;
-            }
-            for (; k < w; ++k) {
-                S.val[S.sptr[s] + C * k + lane] = 0.0;
-                S.col[S.sptr[s] + C * k + lane] = (int32_t)(r + U[s][k]);
+                for (; k < w; ++k) {
+                    S.val[S.sptr[s] + C * k + lane] = 0.0;
+                    S.col[S.sptr[s] + C * k + lane] = (int32_t)(r + u[k]);
+                }
             }
         }
     }
@@ -215,7 +245,7 @@ HostTmaCols tma_cols(const Csr& A, HostSell& S, bool allow_dict) {
         if (s % 8 == 0) cur = (cur + 3) & ~int64_t(3);
         T.cptr[s] = cur;
         const int64_t w = (S.sptr[s + 1] - S.sptr[s]) / C;
-        if (!U[s].empty()) {
+        if (ulen[s]) {
             cur += w;
             T.idx_bytes += 4 * w;
             ++T.ndict;
@@ -225,13 +255,16 @@ HostTmaCols tma_cols(const Csr& A, HostSell& S, bool allow_dict) {
         }
     }
     T.cptr[ns] = (cur + 3) & ~int64_t(3);
-    T.col.assign(T.cptr[ns], 0);
+    T.col.resize(T.cptr[ns]);
 #pragma omp parallel for schedule(static)
     for (int64_t s = 0; s < ns; ++s) {
-        if (!U[s].empty())
-            std::copy(U[s].begin(), U[s].end(), T.col.begin() + T.cptr[s]);
+        int32_t* out = T.col.data() + T.cptr[s];
+        if (ulen[s])
+            std::copy(U.data() + (size_t)s * kW, U.data() + (size_t)s * kW + ulen[s], out);
         else
-            std::copy(S.col.begin() + S.sptr[s], S.col.begin() + S.sptr[s + 1], T.col.begin() + T.cptr[s]);
+            std::copy(S.col.begin() + S.sptr[s], S.col.begin() + S.sptr[s + 1], out);
+        const int64_t len = ulen[s] ? ulen[s] : S.sptr[s + 1] - S.sptr[s];
+        for (int64_t q = T.cptr[s] + len; q < T.cptr[s + 1]; ++q) T.col[q] = 0;  // alignment padding
     }
     return T;
 }
@@ -344,8 +377,8 @@ struct Handle {
         allocs.push_back(p);
         return static_cast<double*>(p);
     }
-    template <class T>
-    T* upload(const std::vector<T>& v) {
+    template <class T, class Al>
+    T* upload(const std::vector<T, Al>& v) {
         void* p = nullptr;
         ck(cudaMalloc(&p, std::max<size_t>(v.size(), 1) * sizeof(T)), "cudaMalloc");
         allocs.push_back(p);
