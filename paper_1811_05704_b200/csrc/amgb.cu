@@ -102,28 +102,6 @@ inline void ckn(int r, const char* what) {
     }
 }
 
-// Host staging vectors for the device store: default-initialised (no zero fill),
-// so the parallel loops that write every element also do the first touch.
-template <class T>
-struct UninitAlloc : std::allocator<T> {
-    template <class U>
-    struct rebind {
-        using other = UninitAlloc<U>;
-    };
-    UninitAlloc() = default;
-    template <class U>
-    UninitAlloc(const UninitAlloc<U>&) {}
-    template <class U, class... Args>
-    void construct(U* p, Args&&... args) {
-        ::new ((void*)p) U(std::forward<Args>(args)...);
-    }
-    template <class U>
-    void construct(U* p) {
-        ::new ((void*)p) U;
-    }
-};
-template <class T>
-using hvec = std::vector<T, UninitAlloc<T>>;
 
 struct HostSell {
     int64_t nrows = 0, ncols = 0, nslices = 0;

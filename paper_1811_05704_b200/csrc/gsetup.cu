@@ -76,6 +76,18 @@ struct DVec {
         if (n) gck(cudaMemcpy(h.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost), "D2H");
         return h;
     }
+    // into an uninitialised host vector: pages first touched by all threads,
+    // then one copy
+    void to_host(hvec<T>& h) const {
+        h.resize(n);
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < n; i += 512) h[i] = T{};
+        if (n) gck(cudaMemcpy(h.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost), "D2H");
+    }
+    void from(const hvec<T>& h) {
+        resize((int64_t)h.size());
+        if (n) gck(cudaMemcpy(p, h.data(), n * sizeof(T), cudaMemcpyHostToDevice), "H2D");
+    }
 };
 
 struct DCsr {
@@ -100,9 +112,9 @@ Csr download(const DCsr& D) {
     Csr A;
     A.nrows = D.nrows;
     A.ncols = D.ncols;
-    A.ptr = D.ptr.to_host();
-    A.col = D.col.to_host();
-    A.val = D.val.to_host();
+    D.ptr.to_host(A.ptr);
+    D.col.to_host(A.col);
+    D.val.to_host(A.val);
     if (A.ptr.empty()) A.ptr.assign(1, 0);
     return A;
 }

@@ -3,16 +3,42 @@
 // (PAPER.md:163-167); the result is uploaded by hierarchy.cu.
 #pragma once
 #include <cstdint>
+#include <memory>
+#include <utility>
 #include <string>
 #include <vector>
 
 namespace amgb {
 
+// Vectors whose elements are default-initialised (no zero fill): every CSR
+// array is completely written by its producer, so the first touch of its pages
+// happens in that (often parallel) loop instead of in a serial memset.
+template <class T>
+struct UninitAlloc : std::allocator<T> {
+    template <class U>
+    struct rebind {
+        using other = UninitAlloc<U>;
+    };
+    UninitAlloc() = default;
+    template <class U>
+    UninitAlloc(const UninitAlloc<U>&) {}
+    template <class U, class... Args>
+    void construct(U* p, Args&&... args) {
+        ::new ((void*)p) U(std::forward<Args>(args)...);
+    }
+    template <class U>
+    void construct(U* p) {
+        ::new ((void*)p) U;
+    }
+};
+template <class T>
+using hvec = std::vector<T, UninitAlloc<T>>;
+
 struct Csr {
     int64_t nrows = 0, ncols = 0;
-    std::vector<int64_t> ptr;  // nrows + 1
-    std::vector<int32_t> col;
-    std::vector<double> val;
+    hvec<int64_t> ptr;  // nrows + 1
+    hvec<int32_t> col;
+    hvec<double> val;
     int64_t nnz() const { return ptr.empty() ? 0 : ptr.back(); }
 };
 
