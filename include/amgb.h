@@ -247,8 +247,11 @@ amg_status amg_setup_dist(int64_t n, const int64_t *ptr, const int32_t *col, con
 /* nranks, first replicated level and the level-0 row starts (nranks+1 entries, may be NULL). */
 amg_status amg_dist_info(amg_handle h, int32_t *nranks, int32_t *first_replicated, int64_t *row_starts);
 /* out[0..11] = row0, row1, ghosts, nnz(A), nnz(P), nnz(R), crow0, crow1, replicated,
- *              send entries, recv peers, send peers of (rank, level). */
-amg_status amg_dist_level_info(amg_handle h, int32_t rank, int32_t level, int64_t out[12]);
+ *              send entries, recv peers, send peers of (rank, level);
+ * out[12..17] = interior row range [ib0, ib1) of the split A, P and R passes (rows
+ *              without ghost columns, overlapped with the halo exchange),
+ *              -1 where the pass is not split (host-only handles, replicated levels). */
+amg_status amg_dist_level_info(amg_handle h, int32_t rank, int32_t level, int64_t out[18]);
 amg_status amg_dist_export(amg_handle h, int32_t rank, int32_t level, const amg_dist_level_export *out);
 /* Self-test of the NCCL transport on a 1-rank communicator of `device`: grouped
  * send/recv to self, all-reduce and broadcast, directly and replayed from a

@@ -296,10 +296,10 @@ class Hierarchy:
         return {"nranks": nr.value, "first_replicated": lg.value, "row_starts": starts}
 
     def dist_level_info(self, rank: int, l: int) -> dict:
-        out = np.zeros(12, np.int64)
+        out = np.zeros(18, np.int64)
         _check(_lib.amg_dist_level_info(self._h, rank, l, out.ctypes.data), "amg_dist_level_info")
         keys = ("row0", "row1", "ghosts", "nnz_A", "nnz_P", "nnz_R", "crow0", "crow1", "replicated",
-                "send_total", "recv_peers", "send_peers")
+                "send_total", "recv_peers", "send_peers", "A_ib0", "A_ib1", "P_ib0", "P_ib1", "R_ib0", "R_ib1")
         return dict(zip(keys, (int(v) for v in out)))
 
     def dist_export(self, rank: int, l: int) -> dict:

@@ -56,6 +56,19 @@ __global__ void fin_kernel(Fin fin, const double* tot, const int32_t* gate) {
 }
 
 // virtual-mode all-reduce: every part's totals <- sum over parts in rank order
+// Split pass (interior + boundary launches): fold the deferred totals of the
+// launches that ran (slot k at defer + k * kSlot) into slot 0, fixed order.
+constexpr int kSlot = 8;
+__global__ void sum_slots_kernel(double* defer, int nv, unsigned mask) {
+    if (threadIdx.x != 0) return;
+    for (int k = 0; k < nv; ++k) {
+        double s = 0.0;
+        for (int q = 0; q < 3; ++q)
+            if (mask >> q & 1) s += defer[q * kSlot + k];
+        defer[k] = s;
+    }
+}
+
 __global__ void sum_parts_kernel(double* const* parts, int nparts, int nv) {
     const int k = threadIdx.x;
     if (k >= nv) return;
@@ -262,7 +275,75 @@ struct DMat {
     double mat_bytes(bool f32) const {
         return (f32 ? 4.0 : 8.0) * nnz + (idx_bytes < 0 ? 4.0 * nnz : (double)idx_bytes);
     }
+    // Multi-GPU split pass: rows [ib0, ib1) have no ghost column
+    // and run while the halo exchange is in flight, the rest after it.
+    bool split = false;
+    int64_t ib0 = 0, ib1 = 0;
+    std::vector<int32_t> hblocks;  // row-block starts of the CSR format (host copy)
+    double bytes_scale = 1.0;      // views: share of the pass's algorithmic bytes
+    const DMat* origin = nullptr;  // views: the matrix they cut
+    DMat view(int64_t r0, int64_t r1, double scale) const {
+        DMat v;
+        v.fmt = fmt;
+        v.nrows = r1 - r0;
+        v.ncols = ncols;
+        v.nnz = nnz;
+        v.idx_bytes = idx_bytes;
+        v.bytes_scale = scale;
+        v.origin = origin ? origin : this;
+        if (fmt == Fmt::TMA) {
+            v.tma = tma;
+            v.tma.row0 = tma.row0 + r0;
+            v.tma.nrows = r1 - r0;
+            v.tma.sptr = tma.sptr + r0 / 32;
+            v.tma.cptr = tma.cptr + r0 / 32;
+            v.tma.nslices = (r1 - r0 + 31) / 32;
+            v.tma.ntiles = (v.tma.nslices + 7) / 8;
+        } else if (fmt == Fmt::SELL) {
+            v.sell = sell;
+            v.sell.row0 = sell.row0 + r0;
+            v.sell.nrows = r1 - r0;
+            v.sell.sptr = sell.sptr + r0 / 32;
+            v.sell.nslices = (r1 - r0 + 31) / 32;
+        } else {
+            const int64_t b0 = std::lower_bound(hblocks.begin(), hblocks.end(), (int32_t)r0) - hblocks.begin();
+            const int64_t b1 = std::lower_bound(hblocks.begin(), hblocks.end(), (int32_t)r1) - hblocks.begin();
+            v.csr = csr;
+            v.csr.brow = csr.brow + b0;
+            v.csr.nblocks = b1 - b0;
+        }
+        return v;
+    }
 };
+
+// Interior rows of a distributed matrix: the longest run of rows whose columns
+// are all local (< nloc), cut to the format's granularity (256-row tiles, 32-row
+// slices, CSR row blocks).  {0, 0}: no split.
+std::pair<int64_t, int64_t> interior_range(const Csr& M, int64_t nloc, Fmt fmt, const std::vector<int32_t>& blocks) {
+    int64_t best0 = 0, best1 = 0, run0 = 0;
+    for (int64_t i = 0; i <= M.nrows; ++i) {
+        bool ghost = i == M.nrows;
+        for (int64_t k = ghost ? 0 : M.ptr[i]; !ghost && k < M.ptr[i + 1]; ++k) ghost = M.col[k] >= nloc;
+        if (ghost) {
+            if (i - run0 > best1 - best0) best0 = run0, best1 = i;
+            run0 = i + 1;
+        }
+    }
+    int64_t a = best0, b = best1;
+    if (fmt == Fmt::CSR) {
+        auto lo = std::lower_bound(blocks.begin(), blocks.end(), (int32_t)a);
+        auto hi = std::upper_bound(blocks.begin(), blocks.end(), (int32_t)b);
+        if (lo == blocks.end() || hi == blocks.begin()) return {0, 0};
+        a = *lo;
+        b = *(hi - 1);
+    } else {
+        const int64_t g = fmt == Fmt::TMA ? 256 : 32;
+        a = (a + g - 1) / g * g;
+        b = b == M.nrows ? b : b / g * g;
+    }
+    if (b <= a) return {0, 0};
+    return {a, b};
+}
 
 // One level of one part.  Vectors that are gathered by a matrix pass have a
 // ghost region after the n local entries.
@@ -378,6 +459,9 @@ struct Handle {
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         if (own_stream) cudaStreamDestroy(own_stream);
+        if (comm_stream) cudaStreamDestroy(comm_stream);
+        if (ev_pack) cudaEventDestroy(ev_pack);
+        if (ev_halo) cudaEventDestroy(ev_halo);
         if (nccl && Nccl::get().commDestroy) Nccl::get().commDestroy(nccl);
     }
 
@@ -510,6 +594,7 @@ struct Handle {
     bool trace = std::getenv("AMGB_TRACE") != nullptr;
     template <class F>
     void launch(int cls, double bytes, const char* what, F&& fn) {
+        if (!in_interior) halo_wait();  // only interior rows may overlap an exchange
         if (trace) {
             std::fprintf(stderr, "[amgb] launch %s\n", what);
             std::fflush(stderr);
@@ -568,7 +653,8 @@ struct Handle {
     }
 
     // ---------------------------------------------------------------- launches
-    int mat_class(const Part& p, const DMat& M) const {
+    int mat_class(const Part& p, const DMat& M0) const {
+        const DMat& M = M0.origin ? *M0.origin : M0;
         if (&M == &p.lv[0].A) return AMG_PROF_A0_PASS;
         for (const auto& L : p.lv)
             if (&M == &L.A) return AMG_PROF_A_COARSE;
@@ -612,22 +698,26 @@ struct Handle {
             rows_tma_impl<T, false, F32>(M, op, gate, red);
     }
     // a part with no rows contributes zeros to an all-reduce
-    void zero_defer(Part& p) {
-        if (p.red.defer) ck(cudaMemsetAsync(p.red.defer, 0, 4 * sizeof(double), stream), "memset");
+    void zero_defer(Part& p, const Red* r = nullptr) {
+        const Red& red = r ? *r : p.red;
+        if (red.defer) ck(cudaMemsetAsync(red.defer, 0, 4 * sizeof(double), stream), "memset");
     }
     // One pass over matrix M of part p with the fused epilogue op; F32: read the
     // fp32 copy of the matrix values (mixed-precision V-cycle).
     template <bool F32, class Op>
-    void rows_impl(Part& p, const DMat& M, const Op& op, const int32_t* gate, const char* what) {
+    void rows_impl(Part& p, const DMat& M, const Op& op, const int32_t* gate, const char* what,
+                   const Red* red_slot = nullptr) {
         if (M.nrows == 0) {
-            if constexpr (Op::NDOT > 0) zero_defer(p);
+            if constexpr (Op::NDOT > 0) zero_defer(p, red_slot);
             return;
         }
         // matrices too big for L2 stream their entries (evict-first); the rest
         // keep them cached so coarse levels stay L2-resident across cycles
         const bool big = M.nnz * 12 > (int64_t)48 << 20;
-        const double bytes = M.mat_bytes(F32) + 4.0 * M.nrows + 8.0 * M.ncols * Op::GATHER + 8.0 * M.nrows * Op::ROWV;
-        const Red& red = p.red;
+        const DMat& Mo = M.origin ? *M.origin : M;  // a view accounts a share of its matrix's pass
+        const double bytes = M.bytes_scale * (Mo.mat_bytes(F32) + 4.0 * Mo.nrows + 8.0 * Mo.ncols * Op::GATHER +
+                                              8.0 * Mo.nrows * Op::ROWV);
+        const Red& red = red_slot ? *red_slot : p.red;
         launch(mat_class(p, M), bytes, what, [&] {
             if (M.fmt == Fmt::TMA) {  // T = 1 lane per row (narrow rows only, pick_format)
                 rows_tma<1, F32>(M.tma, op, gate, red, big);
@@ -644,17 +734,68 @@ struct Handle {
             }
         });
     }
+    // A distributed pass split around the halo exchange: the
+    // interior rows run while the exchange started by exchange() is in flight
+    // on comm_stream, the boundary rows after it; fused dots of the (up to 3)
+    // launches are folded in a fixed order before the all-reduce.
+    template <bool F32, class Op>
+    void rows_split(Part& p, const DMat& M, const Op& op, const int32_t* gate, const char* what) {
+        Red slot[3] = {p.red, p.red, p.red};
+        for (int q = 0; q < 3; ++q)
+            if (p.red.defer) slot[q].defer = p.red.defer + q * kSlot;
+        unsigned mask = 0;
+        bool acct = false;  // the first launch carries the pass's bytes
+        if (M.ib1 > M.ib0) {
+            in_interior = true;
+            rows_impl<F32>(p, M.view(M.ib0, M.ib1, 1.0), op, gate, what, &slot[0]);
+            in_interior = false;
+            mask |= 1;
+            acct = true;
+        }
+        halo_wait();
+        if (M.ib0 > 0) {
+            rows_impl<F32>(p, M.view(0, M.ib0, acct ? 0.0 : 1.0), op, gate, what, &slot[1]);
+            mask |= 2;
+            acct = true;
+        }
+        if (M.ib1 < M.nrows) {
+            rows_impl<F32>(p, M.view(M.ib1, M.nrows, acct ? 0.0 : 1.0), op, gate, what, &slot[2]);
+            mask |= 4;
+        }
+        if constexpr (Op::NDOT > 0)
+            launch(AMG_PROF_VECTOR, 0, "fold split dots",
+                   [&] { sum_slots_kernel<<<1, 32, 0, stream>>>(p.red.defer, Op::NDOT, mask); });
+    }
+    template <bool F32, class Op>
+    void rows_any(Part& p, const DMat& M, const Op& op, const int32_t* gate, const char* what) {
+        if (M.split && distributed() && M.nrows > 0) {
+            rows_split<F32>(p, M, op, gate, what);
+        } else {
+            halo_wait();
+            rows_impl<F32>(p, M, op, gate, what);
+        }
+    }
     template <class Op>
     void rows(Part& p, const DMat& M, const Op& op, const int32_t* gate, const char* what) {
-        rows_impl<false>(p, M, op, gate, what);
+        rows_any<false>(p, M, op, gate, what);
     }
     // V-cycle passes: fp32 hierarchy values when prm.precision == 1
     template <class Op>
     void vrows(Part& p, const DMat& M, const Op& op, const int32_t* gate, const char* what) {
         if (prm.precision == 1)
-            rows_impl<true>(p, M, op, gate, what);
+            rows_any<true>(p, M, op, gate, what);
         else
-            rows_impl<false>(p, M, op, gate, what);
+            rows_any<false>(p, M, op, gate, what);
+    }
+    // ---- halo exchange in flight on comm_stream (distributed handles)
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
+    bool halo_pending = false;
+    bool in_interior = false;
+    void halo_wait() {
+        if (!halo_pending) return;
+        ck(cudaStreamWaitEvent(stream, ev_halo, 0), "wait halo");
+        halo_pending = false;
     }
     template <class Op>
     void vec(Part& p, int64_t n, const Op& op, const int32_t* gate, const char* what) {
@@ -687,6 +828,11 @@ struct Handle {
                 pack_kernel<<<grid_for(L.nsend), kBlock, 0, stream>>>(L.send_idx, v, L.sendbuf, L.nsend);
             });
         }
+        halo_wait();
+        // the transfers run on comm_stream, after everything issued so far on
+        // the work stream; the next split pass overlaps its interior rows
+        ck(cudaEventRecord(ev_pack, stream), "record pack");
+        ck(cudaStreamWaitEvent(comm_stream, ev_pack, 0), "wait pack");
         if (virt) {
             for (Part& p : parts) {
                 DevLevel& L = p.lv[l];
@@ -699,7 +845,7 @@ struct Handle {
                         if (Q.plan.send_peer[j] == p.rank) soff = Q.plan.send_off[j];
                     if (soff < 0) throw CudaError{"halo plan mismatch"};
                     ck(cudaMemcpyAsync(dst + L.plan.recv_off[k], Q.sendbuf + soff, L.plan.recv_cnt[k] * sizeof(double),
-                                       cudaMemcpyDeviceToDevice, stream),
+                                       cudaMemcpyDeviceToDevice, comm_stream),
                        "halo copy");
                 }
             }
@@ -711,20 +857,23 @@ struct Handle {
             ckn(nc.groupStart(), "ncclGroupStart");
             for (size_t j = 0; j < L.plan.send_peer.size(); ++j)
                 ckn(nc.send(L.sendbuf + L.plan.send_off[j], L.plan.send_cnt[j], kNcclDouble, L.plan.send_peer[j], nccl,
-                            stream),
+                            comm_stream),
                     "ncclSend");
             for (size_t k = 0; k < L.plan.recv_peer.size(); ++k)
                 ckn(nc.recv(dst + L.plan.recv_off[k], L.plan.recv_cnt[k], kNcclDouble, L.plan.recv_peer[k], nccl,
-                            stream),
+                            comm_stream),
                     "ncclRecv");
             ckn(nc.groupEnd(), "ncclGroupEnd");
         }
+        ck(cudaEventRecord(ev_halo, comm_stream), "record halo");
+        halo_pending = true;
     }
     // After a fused dot on a distributed handle: all-reduce the deferred
     // totals, then finalize on every part.
     template <class MakeFin>
     void allreduce_fin(int nv, const MakeFin& make_fin, const GSel& gate) {
         if (!distributed()) return;
+        halo_wait();
         if (virt) {
             launch(AMG_PROF_VECTOR, 0, "allreduce (virtual)",
                    [&] { sum_parts_kernel<<<1, 32, 0, stream>>>(d_defer_ptrs, (int)parts.size(), nv); });
@@ -743,6 +892,7 @@ struct Handle {
     // full vector sel(part); gather the other ranks' slices.
     void allgather_slices(int l_rep, const Sel& sel) {
         if (!distributed()) return;
+        halo_wait();
         if (l_rep >= (int)starts.size()) throw CudaError{"allgather_slices: level without a partition"};
         const std::vector<int64_t>& st = starts[l_rep];
         if (virt) {
@@ -1229,6 +1379,7 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
                     throw;
                 }
                 capturing = false;
+                halo_wait();  // the comm stream rejoins before the capture ends
                 ck(cudaStreamEndCapture(stream, &g), "end capture");
                 graph_kernels = launches - before;
                 launches = before;
@@ -1730,6 +1881,7 @@ amg_status Handle::solve_gmres(const double* f, double* x, double tol, int32_t m
                 }
                 capturing = false;
                 prof_mask = saved_mask;
+                halo_wait();  // the comm stream rejoins before the capture ends
                 ck(cudaStreamEndCapture(stream, &g), "end capture");
                 gm.rec.swap(rec_graph);
                 rec_graph.swap(saved);
@@ -1945,6 +2097,7 @@ amg_status Handle::solve_idrs_t(const double* f, double* x, double tol, int32_t 
                 }
                 capturing = false;
                 prof_mask = saved_mask;
+                halo_wait();  // the comm stream rejoins before the capture ends
                 ck(cudaStreamEndCapture(stream, &g), "end capture");
                 idr.rec.swap(rec_graph);
                 rec_graph.swap(saved);
@@ -2104,6 +2257,7 @@ DMat upload_mat_impl(Handle& H, const Csr& A, int64_t* bytes, bool f32) {
         d.csr.col = H.upload(A.col);
         d.csr.val = H.upload(A.val);
         d.csr.brow = H.upload(blocks);
+        d.hblocks = blocks;
         if (f32) d.csr.valf = H.upload(std::vector<float>(A.val.begin(), A.val.end()));
         d.stored = d.nnz;
         *bytes += (int64_t)(ptr32.size() * 4 + A.col.size() * 12 + blocks.size() * 4);
@@ -2241,6 +2395,23 @@ void upload_part(Handle& H, const RankPart& RP, Part& P) {
         if (!coarsest) {
             L.P = upload_mat(H, lp.mp(), &L.dev_bytes, f32);
             L.R = upload_mat(H, lp.mr(), &L.dev_bytes, f32);
+        }
+        // multi-GPU: interior rows (no ghost column) of each pass that follows a
+        // halo exchange -- A and R gather this level's vectors, P the next level's
+        if (H.distributed() && !lp.replicated && std::getenv("AMGB_NO_SPLIT") == nullptr) {
+            auto mark = [](DMat& M, const Csr& host, int64_t nloc) {
+                const auto r = interior_range(host, nloc, M.fmt, M.hblocks);
+                M.split = true;  // boundary-only when the range is empty
+                M.ib0 = r.first;
+                M.ib1 = r.second;
+            };
+            mark(L.A, lp.ma(), L.n);
+            if (!coarsest) {
+                mark(L.R, lp.mr(), L.n);
+                if (!lp.next_replicated) mark(L.P, lp.mp(), lp.crow1 - lp.crow0);
+            }
+        }
+        if (!coarsest) {
             if (prm.relax != 2) L.m = H.upload(lp.m);
             if (prm.relax == 2) L.diag = H.upload(lp.diag);  // Chebyshev D^-1 scaling
             L.x = H.dalloc(nv);
@@ -2286,7 +2457,7 @@ void upload_part(Handle& H, const RankPart& RP, Part& P) {
     H.allocs.push_back(pp);
     ck(cudaMemset(pp, 0, 64), "memset");
     P.red.ticket = static_cast<unsigned int*>(pp);
-    if (H.distributed()) P.red.defer = H.dalloc(4);
+    if (H.distributed()) P.red.defer = H.dalloc(3 * kSlot);  // 3 slots: split passes
     P.r = H.dalloc(nv0);
     P.r2 = H.dalloc(nv0);  // fused CG: ping-pong r
     P.z = H.dalloc(nv0);
@@ -2470,6 +2641,11 @@ static amg_status setup_impl(int64_t n, const int64_t* ptr, const int32_t* col, 
         ck(cudaEventCreate(&H->ev1), "event");
         ck(cudaStreamCreate(&H->own_stream), "stream");  // capture needs a non-legacy stream
         H->stream = H->own_stream;
+        if (nranks > 1) {  // halo transfers overlap interior rows
+            ck(cudaStreamCreateWithFlags(&H->comm_stream, cudaStreamNonBlocking), "comm stream");
+            ck(cudaEventCreateWithFlags(&H->ev_pack, cudaEventDisableTiming), "event");
+            ck(cudaEventCreateWithFlags(&H->ev_halo, cudaEventDisableTiming), "event");
+        }
         if (nranks > 1 && rank >= 0) {
             Nccl& nc = Nccl::get();
             if (!nc.ok) return set_error(AMG_E_CUDA, "NCCL unavailable: " + nc.error);
@@ -2719,7 +2895,7 @@ static const amgb::LevelPart* find_part(const Handle& H, int32_t rank, int32_t l
     return nullptr;
 }
 
-amg_status amg_dist_level_info(amg_handle h, int32_t rank, int32_t l, int64_t out[12]) {
+amg_status amg_dist_level_info(amg_handle h, int32_t rank, int32_t l, int64_t out[18]) {
     if (!h || !h->h || !out) return set_error(AMG_E_INVALID_ARG, "NULL argument");
     const amgb::LevelPart* lp = find_part(*h->h, rank, l);
     if (!lp) return set_error(AMG_E_INVALID_ARG, "rank/level not held by this handle");
@@ -2735,6 +2911,18 @@ amg_status amg_dist_level_info(amg_handle h, int32_t rank, int32_t l, int64_t ou
     out[9] = (int64_t)lp->halo.send_idx.size();
     out[10] = (int64_t)lp->halo.recv_peer.size();
     out[11] = (int64_t)lp->halo.send_peer.size();
+    for (int q = 12; q < 18; ++q) out[q] = -1;  // split passes: device handles only
+    const amgb::Handle& H = *h->h;
+    for (const auto& p : H.parts)
+        if (p.rank == rank && l < (int)p.lv.size()) {
+            const amgb::DevLevel& L = p.lv[l];
+            const amgb::DMat* m[3] = {&L.A, &L.P, &L.R};
+            for (int q = 0; q < 3; ++q)
+                if (m[q]->split) {
+                    out[12 + 2 * q] = m[q]->ib0;
+                    out[13 + 2 * q] = m[q]->ib1;
+                }
+        }
     return AMG_OK;
 }
 

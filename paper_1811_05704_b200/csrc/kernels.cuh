@@ -26,6 +26,7 @@ constexpr int kWarp = 32;
 
 struct Sell {
     int64_t nrows = 0, ncols = 0, nslices = 0;
+    int64_t row0 = 0;  // first row of this (sub-)matrix view: row = row0 + local row
     const int64_t* sptr = nullptr;
     const int32_t* col = nullptr;
     const double* val = nullptr;
@@ -223,7 +224,8 @@ __global__ void __launch_bounds__(kBlock, minb_of<Op>(PIPE ? 4 : 6)) sell_rows(S
         // row-local epilogue operands are requested first, so their latency
         // overlaps the matrix stream (single column; K-column rows load later)
         typename Op::Row rr{};
-        if constexpr (cols_of<Op>() == 1) rr = op.load(row);
+        const int64_t grow = A.row0 + row;  // global row (views of a split pass)
+        if constexpr (cols_of<Op>() == 1) rr = op.load(grow);
         const int64_t s = row >> 5;
         const int lane = (int)(row & 31);
         const int64_t beg = A.sptr[s];
@@ -269,8 +271,8 @@ __global__ void __launch_bounds__(kBlock, minb_of<Op>(PIPE ? 4 : 6)) sell_rows(S
                 v[u] = vn[u];
             }
         }
-        if constexpr (cols_of<Op>() > 1) rr = op.load(row);
-        op.row(row, sum, rr, dots);
+        if constexpr (cols_of<Op>() > 1) rr = op.load(grow);
+        op.row(grow, sum, rr, dots);
     }
     pdl_trigger();
     if constexpr (Op::NDOT > 0) grid_reduce<Op::NDOT>(dots, red, op.fin);
@@ -293,6 +295,7 @@ constexpr int kTmaThreads = kBlock + 32;  // 8 consumer warps + 1 producer warp
 
 struct SellTma {
     int64_t nrows = 0, ncols = 0, nslices = 0, ntiles = 0;
+    int64_t row0 = 0;  // first row of this (sub-)matrix view (a multiple of 256)
     const int64_t* sptr = nullptr;  // nslices + 1 element offsets (multiples of C)
     const int64_t* cptr = nullptr;  // nslices + 1 offsets into col (offset dictionary, amgb.cu tma_cols)
     const int32_t* col = nullptr;
@@ -401,8 +404,9 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sel
         for (int64_t t = blockIdx.x; t < A.ntiles; t += gridDim.x, ++i) {
             const int s = i % kTmaStages;
             const int64_t slice = t * NS + warp;
-            const int64_t row = slice * C + r;
-            const bool has_row = slice < A.nslices && row < A.nrows;
+            const int64_t lrow = slice * C + r;
+            const bool has_row = slice < A.nslices && lrow < A.nrows;
+            const int64_t row = A.row0 + lrow;  // global row (views of a split pass)
             typename Op::Row rr{};
             if constexpr (cols_of<Op>() == 1)
                 if (pt == 0 && has_row) rr = op.load(row);  // in flight during the wait
