@@ -47,7 +47,7 @@ def main():
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--rounds", type=int, default=6)
     ap.add_argument("--solves", type=int, default=3)
-    ap.add_argument("--variants", required=True, help="name:setup_env|solve_env;...")
+    ap.add_argument("--variants", required=True, help="name:setup_env|solve_env[|setup kwargs k=v,...];...")
     a = ap.parse_args()
     p, c, v, f = synth.problem(a.problem, a.n)
     fd = torch.from_numpy(f).cuda()
@@ -55,11 +55,11 @@ def main():
     handles = {}
     for spec in a.variants.split(";"):
         name, envs = spec.split(":", 1)
-        se, _, so = envs.partition("|")
-        se, so = parse_env(se), parse_env(so)
-        key = tuple(sorted(se.items()))
+        fields = envs.split("|") + ["", ""]
+        se, so, kw = parse_env(fields[0]), parse_env(fields[1]), parse_env(fields[2])
+        key = (tuple(sorted(se.items())), tuple(sorted(kw.items())))
         if key not in handles:
-            handles[key] = with_env(se, lambda: amgb.setup(p, c, v))
+            handles[key] = with_env(se, lambda: amgb.setup(p, c, v, **kw))
         variants.append((name, handles[key], so))
     times = {n: [] for n, _, _ in variants}
     iters = {}
