@@ -16,6 +16,8 @@
 // distributed matrix pass and an all-reduce after each fused dot.
 #include <cuda_runtime.h>
 
+#include <cub/cub.cuh>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -33,6 +35,7 @@
 #include "dist.hpp"
 #include "gmres.cuh"
 #include "idrs.cuh"
+#include "convert.cuh"
 #include "kernels.cuh"
 #include "ops.cuh"
 #include "setup.hpp"
@@ -429,6 +432,13 @@ struct Handle {
     bool distributed() const { return nranks > 1; }
 
 
+    template <class T>
+    T* talloc(int64_t n) {  // uninitialised device array owned by the handle
+        void* p = nullptr;
+        ck(cudaMalloc(&p, std::max<int64_t>(n, 1) * sizeof(T)), "cudaMalloc");
+        allocs.push_back(p);
+        return static_cast<T*>(p);
+    }
     double* dalloc(int64_t n) {
         void* p = nullptr;
         ck(cudaMalloc(&p, std::max<int64_t>(n, 1) * sizeof(double)), "cudaMalloc");
@@ -2231,6 +2241,123 @@ DMat upload_mat(Handle& H, const Csr& A, int64_t* bytes, bool f32 = false) {
     return d;
 }
 
+// Device-side format construction (convert.cuh): the CSR goes to the device
+// once and the SELL / TMA arrays are built there -- the same arrays as the
+// host converters below (AMGB_HOST_CONVERT=1 selects those).
+struct DevTmp {  // scratch freed at scope exit
+    std::vector<void*> p;
+    template <class T>
+    T* get(int64_t n) {
+        void* q = nullptr;
+        ck(cudaMalloc(&q, std::max<int64_t>(n, 1) * sizeof(T)), "cudaMalloc (convert)");
+        p.push_back(q);
+        return static_cast<T*>(q);
+    }
+    ~DevTmp() {
+        for (void* q : p) cudaFree(q);
+    }
+};
+
+static void dev_scan_ptr(int64_t* v, int64_t n) {  // inclusive sum of v[1..n] in place (v[0] = 0)
+    if (n <= 0) return;
+    size_t tmp = 0;
+    ck(cub::DeviceScan::InclusiveSum(nullptr, tmp, v + 1, v + 1, (int)n), "scan");
+    void* t = nullptr;
+    ck(cudaMalloc(&t, std::max<size_t>(tmp, 1)), "cudaMalloc (scan)");
+    const cudaError_t e = cub::DeviceScan::InclusiveSum(t, tmp, v + 1, v + 1, (int)n);
+    cudaFree(t);
+    ck(e, "scan");
+}
+
+static int cv_grid(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 1 << 20)); }
+
+bool upload_sliced_dev(Handle& H, const Csr& A, Fmt fmt, bool f32, bool allow_dict, DMat& d, int64_t* bytes) {
+    const int64_t n = A.nrows, nnz = A.nnz(), ns = (n + 31) / 32;
+    DevTmp tmp;
+    int64_t* dptr = tmp.get<int64_t>(n + 1);
+    int32_t* dcol = tmp.get<int32_t>(nnz);
+    double* dval = tmp.get<double>(nnz);
+    ck(cudaMemcpy(dptr, A.ptr.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice), "H2D ptr");
+    ck(cudaMemcpy(dcol, A.col.data(), nnz * sizeof(int32_t), cudaMemcpyHostToDevice), "H2D col");
+    ck(cudaMemcpy(dval, A.val.data(), nnz * sizeof(double), cudaMemcpyHostToDevice), "H2D val");
+    int64_t* sptr = H.talloc<int64_t>(ns + 1);
+    cv_slice_width<<<cv_grid(ns), 256>>>(n, ns, dptr, sptr);
+    dev_scan_ptr(sptr, ns);
+    int64_t stored = 0;
+    ck(cudaMemcpy(&stored, sptr + ns, sizeof(int64_t), cudaMemcpyDeviceToHost), "D2H");
+    double* sval = H.talloc<double>(stored);
+    if (fmt == Fmt::SELL) {
+        int32_t* scol = H.talloc<int32_t>(stored);
+        cv_fill<<<cv_grid(ns * 32), 256>>>(n, ns, dptr, dcol, dval, sptr, nullptr, nullptr, nullptr, scol, nullptr,
+                                           sval);
+        d.sell.nrows = n;
+        d.sell.ncols = A.ncols;
+        d.sell.nslices = ns;
+        d.sell.sptr = sptr;
+        d.sell.col = scol;
+        d.sell.val = sval;
+        if (f32) {
+            float* vf = H.talloc<float>(stored);
+            cv_to_f32<<<cv_grid(stored), 256>>>(stored, sval, vf);
+            d.sell.valf = vf;
+        }
+        d.stored = stored;
+        *bytes += (ns + 1) * 8 + stored * 12;
+    } else {
+        const int64_t nt = (ns + 7) / 8;
+        int32_t* U = tmp.get<int32_t>(ns * kDictW);
+        int32_t* ulen = tmp.get<int32_t>(ns);
+        if (allow_dict)
+            cv_dict<<<cv_grid(ns), 256>>>(n, A.ncols, ns, dptr, dcol, sptr, U, ulen);
+        else
+            ck(cudaMemset(ulen, 0, ns * sizeof(int32_t)), "memset");
+        int64_t* tc = tmp.get<int64_t>(nt + 1);
+        cv_tile_cols<<<cv_grid(nt), 256>>>(ns, nt, sptr, ulen, tc);
+        dev_scan_ptr(tc, nt);
+        int64_t ncol_total = 0;
+        ck(cudaMemcpy(&ncol_total, tc + nt, sizeof(int64_t), cudaMemcpyDeviceToHost), "D2H");
+        int64_t* cptr = H.talloc<int64_t>(ns + 1);
+        int64_t* tent = tmp.get<int64_t>(nt);
+        int64_t* tib = tmp.get<int64_t>(nt);
+        cv_cptr<<<cv_grid(nt), 256>>>(ns, nt, dptr, n, sptr, ulen, tc, cptr, tent, tib);
+        int32_t* tcol = H.talloc<int32_t>(ncol_total);
+        ck(cudaMemset(tcol, 0, std::max<int64_t>(ncol_total, 1) * sizeof(int32_t)), "memset");
+        cv_fill<<<cv_grid(ns * 32), 256>>>(n, ns, dptr, dcol, dval, sptr, ulen, U, cptr, nullptr, tcol, sval);
+        ck(cudaGetLastError(), "convert");
+        std::vector<int64_t> hent(nt), hib(nt);
+        std::vector<int32_t> hulen(ns);
+        ck(cudaMemcpy(hent.data(), tent, nt * sizeof(int64_t), cudaMemcpyDeviceToHost), "D2H");
+        ck(cudaMemcpy(hib.data(), tib, nt * sizeof(int64_t), cudaMemcpyDeviceToHost), "D2H");
+        ck(cudaMemcpy(hulen.data(), ulen, ns * sizeof(int32_t), cudaMemcpyDeviceToHost), "D2H");
+        int64_t te = 0, ib = 0, nd = 0;
+        for (int64_t t = 0; t < nt; ++t) te = std::max(te, hent[t]), ib += hib[t];
+        for (int64_t q = 0; q < ns; ++q) nd += hulen[q] > 0;
+        SellTma& t = d.tma;
+        t.nrows = n;
+        t.ncols = A.ncols;
+        t.nslices = ns;
+        t.T = 1;
+        t.ntiles = nt;
+        t.tile_ent = (int32_t)(((std::max<int64_t>(te, 32) + 31) / 32) * 32);
+        t.sptr = sptr;
+        t.cptr = cptr;
+        t.col = tcol;
+        t.val = sval;
+        if (f32) {
+            float* vf = H.talloc<float>(stored);
+            cv_to_f32<<<cv_grid(stored), 256>>>(stored, sval, vf);
+            t.valf = vf;
+        }
+        d.stored = stored;
+        d.idx_bytes = ib;
+        d.ndict = nd;
+        *bytes += (ns + 1) * 16 + stored * 8 + ncol_total * 4;
+    }
+    ck(cudaGetLastError(), "convert");
+    ck(cudaDeviceSynchronize(), "convert sync");
+    return true;
+}
+
 DMat upload_mat_impl(Handle& H, const Csr& A, int64_t* bytes, bool f32) {
     DMat d;
     d.nrows = A.nrows;
@@ -2261,6 +2388,8 @@ DMat upload_mat_impl(Handle& H, const Csr& A, int64_t* bytes, bool f32) {
         if (f32) d.csr.valf = H.upload(std::vector<float>(A.val.begin(), A.val.end()));
         d.stored = d.nnz;
         *bytes += (int64_t)(ptr32.size() * 4 + A.col.size() * 12 + blocks.size() * 4);
+    } else if (!std::getenv("AMGB_HOST_CONVERT")) {  // SELL / TMA built on the device
+        upload_sliced_dev(H, A, d.fmt, f32, !std::getenv("AMGB_NO_DICT"), d, bytes);
     } else if (d.fmt == Fmt::SELL) {
         HostSell S = to_sell(A, 32);
         d.sell.nrows = S.nrows;
@@ -2583,9 +2712,18 @@ static amg_status setup_impl(int64_t n, const int64_t* ptr, const int32_t* col, 
         validate_csr(n, ptr, col);
         Csr A0;
         A0.nrows = A0.ncols = n;
-        A0.ptr.assign(ptr, ptr + n + 1);
-        A0.col.assign(col, col + ptr[n]);
-        A0.val.assign(val, val + ptr[n]);
+        A0.ptr.resize(n + 1);  // uninitialised: first touch in the parallel copy
+        A0.col.resize(ptr[n]);
+        A0.val.resize(ptr[n]);
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < n; ++i) {
+            A0.ptr[i + 1] = ptr[i + 1];
+            for (int64_t k = ptr[i]; k < ptr[i + 1]; ++k) {
+                A0.col[k] = col[k];
+                A0.val[k] = val[k];
+            }
+        }
+        A0.ptr[0] = ptr[0];
         SetupParams sp;
         sp.smoothed = prm.coarsening == 0;
         sp.eps_strong = prm.eps_strong;

@@ -63,7 +63,17 @@ int thread_id() {
 
 void validate_csr(int64_t n, const int64_t* ptr, const int32_t* col) {
     if (ptr[0] != 0) fail(-2, "CSR: ptr[0] must be 0");
+    // parallel scan for the first bad row, then the message from a serial check of it
+    int64_t first_bad = n;
+#pragma omp parallel for schedule(static) reduction(min : first_bad)
     for (int64_t i = 0; i < n; ++i) {
+        bool bad = ptr[i + 1] < ptr[i];
+        for (int64_t k = ptr[i]; !bad && k < ptr[i + 1]; ++k)
+            bad = col[k] < 0 || col[k] >= n || (k > ptr[i] && col[k] <= col[k - 1]);
+        if (bad && i < first_bad) first_bad = i;
+    }
+    if (first_bad < n) {
+        const int64_t i = first_bad;
         if (ptr[i + 1] < ptr[i]) fail(-2, "CSR: row " + std::to_string(i) + ": ptr decreases");
         for (int64_t k = ptr[i]; k < ptr[i + 1]; ++k) {
             if (col[k] < 0 || col[k] >= n)

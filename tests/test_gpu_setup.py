@@ -122,3 +122,30 @@ def test_gpu_setup_errors():
     # a host-only handle builds on the host whatever setup_device says
     hh = amgb.setup(p, c, synth.problem("poisson", 12)[2], setup_device="gpu", device=-1, coarse_enough=50)
     assert hh.nlevels >= 2
+
+
+@pytest.mark.parametrize("gen,n,kw", [("poisson", 48, {}), ("poisson", 41, {"precision": "mixed"}),
+                                      ("poisson_perm", 40, {}), ("varcoef", 42, {"relax": "chebyshev"})])
+def test_device_format_conversion_matches_host(gen, n, kw):
+    """The SELL-32 / TMA (+ offset dictionary) arrays built on the device
+    (convert.cuh, the default) equal the host converters' (AMGB_HOST_CONVERT=1):
+    same stored sizes, dictionary slices and bitwise the same solve."""
+    import os
+    p, c, v, f = problem(gen, n)
+    hd = amgb.setup(p, c, v, **kw)
+    os.environ["AMGB_HOST_CONVERT"] = "1"
+    try:
+        hh = amgb.setup(p, c, v, **kw)
+    finally:
+        del os.environ["AMGB_HOST_CONVERT"]
+    for l in range(hh.nlevels):
+        a, b = hd.level_info(l), hh.level_info(l)
+        assert (a["padded_nnz_A"], a["dict_slices_A"], a["dev_bytes"]) == \
+            (b["padded_nnz_A"], b["dict_slices_A"], b["dev_bytes"]), l
+    r = synth.random_vector(len(f))
+    assert np.array_equal(hd.precond(dev(r)).cpu().numpy(), hh.precond(dev(r)).cpu().numpy())
+    xd, itd, reld, _ = hd.solve(dev(f), tol=1e-8)
+    xh, ith, relh, _ = hh.solve(dev(f), tol=1e-8)
+    torch.cuda.synchronize()
+    assert itd == ith and reld == relh
+    assert np.array_equal(xd.cpu().numpy(), xh.cpu().numpy())
