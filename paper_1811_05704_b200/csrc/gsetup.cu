@@ -413,6 +413,7 @@ DCsr product(const DCsr& A, const DCsr& B, const Csr* hA, const Csr* hB) {
     bool ovf = false;
     DCsr C = spgemm_dev(A, B, &ovf);
     if (!ovf) return C;
+    if (std::getenv("AMGB_SETUP_TIMING")) std::fprintf(stderr, "[gsetup] product row > %d columns: host multiply\n", kMaxC);
     Csr a = hA ? *hA : download(A), b = hB ? *hB : download(B);
     return upload(multiply(a, b));
 }
