@@ -1652,7 +1652,13 @@ amg_status Handle::solve_batched(int k, const double* F, int64_t ldf, double* X,
         kh->done = all;
         ck(cudaMemcpyAsync(batch.ks, kh, sizeof(KStateB), cudaMemcpyHostToDevice, stream), "ks update");
     }
-    if (!kh->done) {
+    if (!kh->done && std::getenv("AMGB_NO_DEVICE_LOOP")) {  // direct launches (ncu profiling)
+        while (!kh->done) {
+            for (int it = 0; it < 2; ++it) cg_iteration_b<K>(it);
+            ck(cudaMemcpyAsync(kh, batch.ks, sizeof(KStateB), cudaMemcpyDeviceToHost, stream), "ks read");
+            ck(cudaStreamSynchronize(stream), "sync");
+        }
+    } else if (!kh->done) {
         if (!batch.graph) {  // conditional WHILE node around two iterations (device-side loop)
             cudaGraph_t g;
             ck(cudaGraphCreate(&g, 0), "graph create");
