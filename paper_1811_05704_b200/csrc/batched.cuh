@@ -23,10 +23,28 @@ struct KStateB {
     int32_t k, maxiter, done, pad;
 };
 
+// K interleaved columns of row i: K = 4, 8 move 32-byte groups with one 256-bit
+// access each (LDG/STG.E.ENL2.256 on sm_100a): a warp's gather of 32 rows is
+// then full 128-byte lines instead of half-used ones (two 16-byte loads per row
+// left the level-0 batched kernels L1-bound); K = 2 one 128-bit access.
+__device__ __forceinline__ void ld256(const double* p, double* r) {  // data written by earlier kernels
+    asm("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3]) : "l"(p));
+}
+__device__ __forceinline__ void ldg256(const double* p, double* r) {
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3]) : "l"(p));
+}
+__device__ __forceinline__ void st256(double* p, const double* v) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+                 : "memory");
+}
+
 template <int K>
 __device__ __forceinline__ Vk<K> ldk(const double* p, int64_t i) {
     Vk<K> r;
-    if constexpr (K % 2 == 0) {
+    if constexpr (K % 4 == 0) {
+#pragma unroll
+        for (int j = 0; j < K / 4; ++j) ld256(p + i * K + 4 * j, r.v + 4 * j);
+    } else if constexpr (K % 2 == 0) {
         const double2* q = reinterpret_cast<const double2*>(p + i * K);
 #pragma unroll
         for (int j = 0; j < K / 2; ++j) {
@@ -43,7 +61,10 @@ __device__ __forceinline__ Vk<K> ldk(const double* p, int64_t i) {
 template <int K>
 __device__ __forceinline__ Vk<K> ldgk(const double* p, int64_t i) {  // read-only path (gathers)
     Vk<K> r;
-    if constexpr (K % 2 == 0) {
+    if constexpr (K % 4 == 0) {
+#pragma unroll
+        for (int j = 0; j < K / 4; ++j) ldg256(p + i * K + 4 * j, r.v + 4 * j);
+    } else if constexpr (K % 2 == 0) {
         const double2* q = reinterpret_cast<const double2*>(p + i * K);
 #pragma unroll
         for (int j = 0; j < K / 2; ++j) {
@@ -59,7 +80,10 @@ __device__ __forceinline__ Vk<K> ldgk(const double* p, int64_t i) {  // read-onl
 }
 template <int K>
 __device__ __forceinline__ void stk(double* p, int64_t i, const Vk<K>& v) {
-    if constexpr (K % 2 == 0) {
+    if constexpr (K % 4 == 0) {
+#pragma unroll
+        for (int j = 0; j < K / 4; ++j) st256(p + i * K + 4 * j, v.v + 4 * j);
+    } else if constexpr (K % 2 == 0) {
         double2* q = reinterpret_cast<double2*>(p + i * K);
 #pragma unroll
         for (int j = 0; j < K / 2; ++j) q[j] = make_double2(v.v[2 * j], v.v[2 * j + 1]);
