@@ -88,7 +88,7 @@ template <class Op>
 constexpr int unroll_of(int u1) { return cols_of<Op>() == 1 ? u1 : (cols_of<Op>() == 2 ? 4 : (cols_of<Op>() == 4 ? 2 : 1)); }
 // resident blocks requested per SM (launch bounds)
 template <class Op>
-constexpr int minb_of(int b1) { return cols_of<Op>() == 1 ? b1 : 2; }
+constexpr int minb_of(int b1) { return cols_of<Op>() == 1 ? b1 : (cols_of<Op>() <= 4 ? 3 : 2); }
 __device__ __forceinline__ void fma_acc(double& s, double a, double x) { s = fma(a, x, s); }
 template <int K>
 __device__ __forceinline__ void fma_acc(Vk<K>& s, double a, const Vk<K>& x) {
