@@ -200,8 +200,13 @@ HostTmaCols tma_cols(const Csr& A, HostSell& S, bool allow_dict) {
             true_nnz[s] = A.ptr[r1] - A.ptr[r0];
             if (!allow_dict || w == 0 || w > kW || r1 - r0 < C) continue;
             size_t no = 0;
+            bool sorted = true;  // the value layout below needs ascending columns in every row
             for (int64_t r = r0; r < r1; ++r)
-                for (int64_t e = A.ptr[r]; e < A.ptr[r + 1]; ++e) offs[no++] = (int64_t)A.col[e] - r;
+                for (int64_t e = A.ptr[r]; e < A.ptr[r + 1]; ++e) {
+                    offs[no++] = (int64_t)A.col[e] - r;
+                    if (e > A.ptr[r] && A.col[e] <= A.col[e - 1]) sorted = false;
+                }
+            if (!sorted) continue;
             std::sort(offs.begin(), offs.begin() + no);
             no = std::unique(offs.begin(), offs.begin() + no) - offs.begin();
             if ((int64_t)no != w) continue;

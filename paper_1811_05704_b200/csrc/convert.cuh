@@ -30,8 +30,10 @@ __global__ void cv_slice_width(int64_t nrows, int64_t nslices, const int64_t* pt
 }
 
 // dictionary of slice s (amgb.cu tma_cols): the sorted distinct offsets col - row
-// of its 32 rows if there are exactly w of them (w = slice width <= kDictW) and
-// every row + offset is a valid column; ulen[s] = w, else 0
+// of its 32 rows if there are exactly w of them (w = slice width <= kDictW),
+// every row + offset is a valid column and every row's columns are ascending
+// (the local matrices of a partition keep the global entry order, so a row whose
+// first entry is a ghost is not); ulen[s] = w, else 0
 __global__ void cv_dict(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t* ptr, const int32_t* col,
                         const int64_t* sptr, int32_t* U, int32_t* ulen) {
     CV_LOOP(s, nslices) {
@@ -44,6 +46,10 @@ __global__ void cv_dict(int64_t nrows, int64_t ncols, int64_t nslices, const int
         bool ok = true;
         for (int64_t r = r0; r < r1 && ok; ++r)
             for (int64_t e = ptr[r]; e < ptr[r + 1]; ++e) {
+                if (e > ptr[r] && col[e] <= col[e - 1]) {  // the value layout needs ascending columns
+                    ok = false;
+                    break;
+                }
                 const int64_t off = (int64_t)col[e] - r;
                 int lo = 0, hi = m;
                 while (lo < hi) {

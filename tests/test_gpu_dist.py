@@ -31,6 +31,9 @@ CASES = [
     ("varcoef", 24, 2, {"relax": "chebyshev"}),
     ("convdiff", 20, 3, {"relax": "damped_jacobi", "solver": "bicgstab"}),
     ("poisson", 25, 2, {"npre": 2, "npost": 2}),
+    # >= 65536 local rows: level 0 in the TMA format (offset dictionary, split views)
+    ("poisson", 64, 2, {}),
+    ("poisson", 72, 3, {}),
 ]
 
 
