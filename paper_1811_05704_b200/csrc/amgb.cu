@@ -463,6 +463,8 @@ struct Handle {
         return static_cast<T*>(p);
     }
     double upload_ms = 0, upload_bytes = 0;  // setup statistics (AMGB_SETUP_TIMING)
+    // matrices larger than this are read evict-first (AMGB_STREAM_MB overrides)
+    int64_t stream_bytes = (std::getenv("AMGB_STREAM_MB") ? std::atoll(std::getenv("AMGB_STREAM_MB")) : 48) << 20;
     ~Handle() {
         free_batch();
         free_gmres();
@@ -728,7 +730,7 @@ struct Handle {
         }
         // matrices too big for L2 stream their entries (evict-first); the rest
         // keep them cached so coarse levels stay L2-resident across cycles
-        const bool big = M.nnz * 12 > (int64_t)48 << 20;
+        const bool big = M.nnz * 12 > stream_bytes;
         const DMat& Mo = M.origin ? *M.origin : M;  // a view accounts a share of its matrix's pass
         const double bytes = M.bytes_scale * (Mo.mat_bytes(F32) + 4.0 * Mo.nrows + 8.0 * Mo.ncols * Op::GATHER +
                                               8.0 * Mo.nrows * Op::ROWV);
