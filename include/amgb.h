@@ -147,13 +147,15 @@ void amg_params_default(amg_params *p);
 amg_status amg_setup(int64_t n, const int64_t *ptr, const int32_t *col, const double *val,
                      const amg_params *prm, amg_handle *out);
 
-/* Solve A x = f to |f - A x| <= tol |f| (recurrence residual; R17) with
- * the handle's Krylov method, at most maxiter iterations.  f, x: DEVICE pointers;
- * x holds the initial guess on entry and the solution on return.  f = 0 gives
- * x = 0, 0 iterations.  *iters = loop trips, *rel_resid = true |f - A x|/|f|
- * recomputed at exit.  Returns AMG_OK, AMG_NOT_CONVERGED or AMG_BREAKDOWN (outputs
- * filled in all three cases) or an error.  Synchronous.  Cite: PAPER.md:141-143,
- * 209-215. */
+/* Solve A x = f to |f - A x| <= tol |f| (recurrence residual; R14) with
+ * the handle's Krylov method (params.solver: CG, BiCGStab, GMRES(m) or IDR(s)), at
+ * most maxiter iterations.  f, x: DEVICE pointers; x holds the initial guess on
+ * entry and the solution on return.  f = 0 gives x = 0, 0 iterations.  *iters =
+ * loop trips (CG, BiCGStab), Arnoldi steps (GMRES) or preconditioned products
+ * (IDR(s)); *rel_resid = true |f - A x|/|f| recomputed at exit.  Returns AMG_OK,
+ * AMG_NOT_CONVERGED or AMG_BREAKDOWN (outputs filled in all three cases) or an
+ * error.  GMRES and IDR(s) need a single-GPU handle.  Synchronous.  Cite:
+ * PAPER.md:141-143, 209-215. */
 amg_status amg_solve(amg_handle h, const double *f, double *x, double tol, int32_t maxiter,
                      int32_t *iters, double *rel_resid);
 
