@@ -39,3 +39,23 @@ def test_params_struct_size():
     assert p.struct_size == ctypes.sizeof(amgb.AmgParams)
     assert abs(p.p_omega - 2 / 3) < 1e-16 and p.eps_strong == 0.08 and p.coarse_enough == 3000
     assert "sm_100a" in amgb.version()
+
+
+def test_params_defaults_and_validation_host_only():
+    """New parameters: defaults (GPU setup on, IDR(s) s = 4) and their validation,
+    checked on host-only handles (device = -1, no GPU needed)."""
+    import numpy as np
+    import pytest
+
+    import synth
+    p = amgb.make_params()
+    assert p.setup_device == 1 and p.idrs_s == 4 and p.solver == 0
+    assert amgb.make_params(solver="idrs", **{"solver.s": 8}).idrs_s == 8
+    ptr, col, val, f = synth.problem("poisson", 10)
+    h = amgb.setup(ptr, col, val, device=-1, setup_device="gpu", coarse_enough=100)  # host build
+    assert h.nlevels >= 2
+    for bad in ({"solver": "idrs", "idrs_s": 3}, {"setup_device": 2}, {"solver": 4}):
+        with pytest.raises(amgb.AmgError) as e:
+            amgb.setup(ptr, col, val, device=-1, **bad)
+        assert e.value.code == amgb.E_INVALID_ARG
+    assert np.isfinite(h.level_info(0)["alg_bytes_vcycle"])
