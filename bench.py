@@ -61,6 +61,7 @@ def parse():
                     help="k > 1: k right-hand sides per solve (amg_solve_batched); value counts column V-cycles")
     ap.add_argument("--precision", default="double", choices=["double", "mixed"],
                     help="mixed: fp32 hierarchy values in the V-cycle (not the headline; SURVEY §8f rank 2)")
+    ap.add_argument("--reorder", action="store_true", help="locality reordering of the device store (params reorder=1)")
     ap.add_argument("--json-out", default=None)
     return ap.parse_args()
 
@@ -291,7 +292,8 @@ def main():
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     if world == 1:
-        h = amgb.setup(ptr, col, val, prm, device=local, use_graph=0 if args.no_graph else 1)
+        h = amgb.setup(ptr, col, val, prm, device=local, use_graph=0 if args.no_graph else 1,
+                       reorder=1 if args.reorder else 0)
         r0, r1 = 0, n
     else:
         # strong scaling: the global system row-partitioned over the ranks, halo

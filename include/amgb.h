@@ -87,6 +87,12 @@ typedef struct {
                                the same hierarchy either way (Algorithm 1,
                                PAPER.md:95-107).  Host-only handles (device = -1) use the host. */
     int32_t idrs_s;         /* IDR(s) shadow-space dimension s in {1, 2, 4, 8} [4] ("solver.s") */
+    int32_t reorder;        /* 1: locality reordering of the device store (single GPU): the same
+                               hierarchy stored as Q_l A_l Q_l^T, Q_l P_l Q_{l+1}^T, ... with q_0 =
+                               reverse Cuthill-McKee of A_0 and aggregates numbered by their root;
+                               amg_solve / amg_solve_host / amg_precond_apply permute f, x, r, z
+                               on entry and exit; amg_level_op and amg_solve_batched are not
+                               available [0] */
 } amg_params;
 
 /* Per-level statistics (amg_level_info). */

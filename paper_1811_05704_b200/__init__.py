@@ -62,6 +62,7 @@ class AmgParams(C.Structure):
         ("gmres_m", C.c_int32),
         ("setup_device", C.c_int32),
         ("idrs_s", C.c_int32),
+        ("reorder", C.c_int32),
     ]
 
 

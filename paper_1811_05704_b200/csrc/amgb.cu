@@ -23,6 +23,7 @@
 #include <cstdio>
 #include <chrono>
 #include <cstdlib>
+#include <numeric>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -59,6 +60,17 @@ __global__ void fin_kernel(Fin fin, const double* tot, const int32_t* gate) {
 }
 
 // virtual-mode all-reduce: every part's totals <- sum over parts in rank order
+// Locality reordering of the device store (params.reorder): natural -> stored
+// order (dst[q[i]] = src[i]) and back (dst[i] = src[q[i]]).
+__global__ void perm_to_kernel(int64_t n, const int64_t* q, const double* src, double* dst) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[q[i]] = src[i];
+}
+__global__ void perm_from_kernel(int64_t n, const int64_t* q, const double* src, double* dst) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[q[i]];
+}
+
 // Split pass (interior + boundary launches): fold the deferred totals of the
 // launches that ran (slot k at defer + k * kSlot) into slot 0, fixed order.
 constexpr int kSlot = 8;
@@ -463,6 +475,13 @@ struct Handle {
         return static_cast<T*>(p);
     }
     double upload_ms = 0, upload_bytes = 0;  // setup statistics (AMGB_SETUP_TIMING)
+    // locality reordering (params.reorder = 1, single GPU): the device store
+    // holds Q_l A_l Q_l^T etc.; API vectors are permuted on entry / exit
+    bool reordered = false;
+    std::vector<double> coarse_inv_perm;
+    int64_t* dq0 = nullptr;        // q_0 on the device
+    std::vector<int64_t> reorder_q0;
+    double *rf = nullptr, *rx = nullptr;
     // matrices larger than this are read evict-first (AMGB_STREAM_MB overrides)
     int64_t stream_bytes = (std::getenv("AMGB_STREAM_MB") ? std::atoll(std::getenv("AMGB_STREAM_MB")) : 48) << 20;
     ~Handle() {
@@ -959,6 +978,16 @@ struct Handle {
     template <int S>
     amg_status solve_idrs_t(const double* f, double* x, double tol, int32_t maxiter, int32_t* iters, double* rel);
     amg_status solve_idrs(const double* f, double* x, double tol, int32_t maxiter, int32_t* iters, double* rel);
+    amg_status solve_dispatch(const double* f, double* x, double tol, int32_t maxiter, int32_t* iters, double* rel);
+    amg_status solve_api(const double* f, double* x, double tol, int32_t maxiter, int32_t* iters, double* rel);
+    void perm_in(const double* src, double* dst) {  // natural -> stored order
+        const int64_t n = parts[0].lv[0].n;
+        perm_to_kernel<<<grid_for(n), kBlock, 0, stream>>>(n, dq0, src, dst);
+    }
+    void perm_out(const double* src, double* dst) {
+        const int64_t n = parts[0].lv[0].n;
+        perm_from_kernel<<<grid_for(n), kBlock, 0, stream>>>(n, dq0, src, dst);
+    }
     void bicgstab_iteration();
     amg_status solve(const double* f, double* x, double tol, int32_t maxiter, int32_t* iters, double* rel);
     void precond(const double* r, double* z);
@@ -2169,6 +2198,25 @@ amg_status Handle::solve_idrs_t(const double* f, double* x, double tol, int32_t 
     return st;
 }
 
+// The handle's Krylov method; with a reordered store the API vectors are
+// permuted into the stored order first and the solution back afterwards.
+amg_status Handle::solve_dispatch(const double* f, double* x, double tol, int32_t maxiter, int32_t* iters,
+                                  double* rel) {
+    if (prm.solver == 2 && !distributed()) return solve_gmres(f, x, tol, maxiter, iters, rel);
+    if (prm.solver == 3 && !distributed()) return solve_idrs(f, x, tol, maxiter, iters, rel);
+    return solve(f, x, tol, maxiter, iters, rel);
+}
+
+amg_status Handle::solve_api(const double* f, double* x, double tol, int32_t maxiter, int32_t* iters, double* rel) {
+    if (!reordered) return solve_dispatch(f, x, tol, maxiter, iters, rel);
+    perm_in(f, rf);
+    perm_in(x, rx);
+    const amg_status st = solve_dispatch(rf, rx, tol, maxiter, iters, rel);
+    perm_out(rx, x);
+    ck(cudaStreamSynchronize(stream), "sync");
+    return st;
+}
+
 amg_status Handle::solve_idrs(const double* f, double* x, double tol, int32_t maxiter, int32_t* iters, double* rel) {
     switch (prm.idrs_s) {
         case 1: return solve_idrs_t<1>(f, x, tol, maxiter, iters, rel);
@@ -2500,6 +2548,118 @@ double level_alg_bytes(int64_t n_, int64_t z_, int64_t p_, int64_t c_, const amg
 }
 
 // Upload one rank part into a device Part.
+// Reverse Cuthill-McKee order of A's row pattern (params.reorder): breadth-first
+// from a minimum-degree node of each component, neighbours by ascending degree,
+// reversed.  Returns q with q[old] = new.
+std::vector<int64_t> rcm_order(const Csr& A) {
+    const int64_t n = A.nrows;
+    std::vector<int64_t> order;
+    order.reserve(n);
+    std::vector<char> seen(n, 0);
+    std::vector<int64_t> by_deg(n);
+    std::iota(by_deg.begin(), by_deg.end(), 0);
+    auto deg = [&](int64_t i) { return A.ptr[i + 1] - A.ptr[i]; };
+    std::stable_sort(by_deg.begin(), by_deg.end(), [&](int64_t a, int64_t b) { return deg(a) < deg(b); });
+    std::vector<int64_t> nb;
+    for (int64_t start : by_deg) {
+        if (seen[start]) continue;
+        seen[start] = 1;
+        size_t head = order.size();
+        order.push_back(start);
+        while (head < order.size()) {
+            const int64_t i = order[head++];
+            nb.clear();
+            for (int64_t k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
+                const int64_t j = A.col[k];
+                if (!seen[j]) {
+                    seen[j] = 1;
+                    nb.push_back(j);
+                }
+            }
+            std::stable_sort(nb.begin(), nb.end(), [&](int64_t a, int64_t b) { return deg(a) < deg(b); });
+            order.insert(order.end(), nb.begin(), nb.end());
+        }
+    }
+    std::vector<int64_t> q(n);
+    for (int64_t k = 0; k < n; ++k) q[order[n - 1 - k]] = k;
+    return q;
+}
+
+// Rows moved to qr[i], columns renamed qc[c]; every row keeps its entries in the
+// original order, so each row sum is formed exactly as before.
+Csr permute_csr(const Csr& M, const std::vector<int64_t>& qr, const std::vector<int64_t>& qc) {
+    Csr P;
+    P.nrows = M.nrows;
+    P.ncols = M.ncols;
+    P.ptr.assign(M.nrows + 1, 0);
+    for (int64_t i = 0; i < M.nrows; ++i) P.ptr[qr[i] + 1] = M.ptr[i + 1] - M.ptr[i];
+    for (int64_t i = 0; i < M.nrows; ++i) P.ptr[i + 1] += P.ptr[i];
+    P.col.resize(M.nnz());
+    P.val.resize(M.nnz());
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < M.nrows; ++i) {
+        int64_t d = P.ptr[qr[i]];
+        for (int64_t k = M.ptr[i]; k < M.ptr[i + 1]; ++k, ++d) {
+            P.col[d] = (int32_t)qc[M.col[k]];
+            P.val[d] = M.val[k];
+        }
+    }
+    return P;
+}
+
+// The single-rank part of the reordered store: q_0 = RCM(A_0); an aggregate is
+// numbered by the new index of its root, so every level keeps the locality.
+RankPart reordered_part(const HostHierarchy& H, std::vector<std::vector<int64_t>>& q,
+                        std::vector<double>& inv_perm) {
+    const int L = (int)H.levels.size();
+    q.assign(L, {});
+    q[0] = rcm_order(H.levels[0].A);
+    for (int l = 0; l + 1 < L; ++l) {
+        const HostLevel& hl = H.levels[l];
+        const int64_t nc = hl.n_agg;
+        std::vector<int64_t> by(nc);
+        std::iota(by.begin(), by.end(), 0);
+        std::sort(by.begin(), by.end(), [&](int64_t a, int64_t b) { return q[l][hl.root[a]] < q[l][hl.root[b]]; });
+        q[l + 1].assign(nc, 0);
+        for (int64_t k = 0; k < nc; ++k) q[l + 1][by[k]] = k;
+    }
+    RankPart RP;
+    RP.rank = 0;
+    RP.nranks = 1;
+    RP.lg = L;
+    RP.lv.resize(L);
+    for (int l = 0; l < L; ++l) {
+        const HostLevel& hl = H.levels[l];
+        LevelPart& lp = RP.lv[l];
+        const bool coarsest = l == L - 1;
+        const int64_t n = hl.A.nrows;
+        lp.replicated = true;
+        lp.row0 = 0;
+        lp.row1 = n;
+        lp.A = permute_csr(hl.A, q[l], q[l]);
+        if (!coarsest) {
+            lp.P = permute_csr(hl.P, q[l], q[l + 1]);
+            lp.R = permute_csr(hl.R, q[l + 1], q[l]);
+            lp.crow0 = 0;
+            lp.crow1 = hl.P.ncols;
+            lp.next_replicated = true;
+        }
+        auto perm_vec = [&](const std::vector<double>& v, std::vector<double>& out) {
+            out.assign(v.size(), 0.0);
+            for (size_t i = 0; i < v.size(); ++i) out[q[l][i]] = v[i];
+        };
+        perm_vec(hl.m, lp.m);
+        perm_vec(hl.diag, lp.diag);
+        lp.halo.nloc = n;
+    }
+    const int64_t nL = H.levels.back().A.nrows;
+    inv_perm.assign(H.coarse_inv.size(), 0.0);
+    const auto& qL = q[L - 1];
+    for (int64_t a = 0; a < nL; ++a)
+        for (int64_t b = 0; b < nL; ++b) inv_perm[qL[a] * nL + qL[b]] = H.coarse_inv[a * nL + b];
+    return RP;
+}
+
 void upload_part(Handle& H, const RankPart& RP, Part& P) {
     const amg_params& prm = H.prm;
     const int nlev = (int)RP.lv.size();
@@ -2585,7 +2745,7 @@ void upload_part(Handle& H, const RankPart& RP, Part& P) {
         }
     }
     P.nL = RP.lv.back().ma().nrows;
-    P.coarse_inv = H.upload(H.host.coarse_inv);
+    P.coarse_inv = H.upload(H.reordered ? H.coarse_inv_perm : H.host.coarse_inv);
     P.lv.back().dev_bytes += 8 * P.nL * P.nL;
     const int64_t nv0 = P.lv[0].n + P.lv[0].ng;
     void* pp = nullptr;
@@ -2666,6 +2826,7 @@ void amg_params_default(amg_params* p) {
     p->gmres_m = 30;
     p->setup_device = 1;
     p->idrs_s = 4;
+    p->reorder = 0;
 }
 
 const char* amg_last_error(void) { return amgb::g_err.c_str(); }
@@ -2679,6 +2840,7 @@ static amg_status check_params(const amg_params& p) {
     if (p.struct_size != sizeof(amg_params)) return set_error(AMG_E_INVALID_ARG, "amg_params: struct_size mismatch");
     if (p.coarsening < 0 || p.coarsening > 1) return set_error(AMG_E_INVALID_ARG, "coarsening must be 0 or 1");
     if (p.setup_device < 0 || p.setup_device > 1) return set_error(AMG_E_INVALID_ARG, "setup_device must be 0 or 1");
+    if (p.reorder < 0 || p.reorder > 1) return set_error(AMG_E_INVALID_ARG, "reorder must be 0 or 1");
     if (p.relax < 0 || p.relax > 2) return set_error(AMG_E_INVALID_ARG, "relax must be 0, 1 or 2");
     if (p.solver < 0 || p.solver > 3)
         return set_error(AMG_E_INVALID_ARG, "solver must be 0 (cg), 1 (bicgstab), 2 (gmres) or 3 (idrs)");
@@ -2757,7 +2919,14 @@ static amg_status setup_impl(int64_t n, const int64_t* ptr, const int32_t* col, 
         H->lg = first_replicated_level(H->host, nranks, gather_below);
         H->starts = level_starts(H->host, nranks, H->lg);
         if (nranks == 1) {
-            H->host_parts.push_back(build_rank_part(H->host, 1, 0, H->lg, H->starts));
+            if (prm.reorder == 1 && prm.device >= 0) {  // locality reordering of the device store
+                std::vector<std::vector<int64_t>> q;
+                H->host_parts.push_back(reordered_part(H->host, q, H->coarse_inv_perm));
+                H->reordered = true;
+                H->reorder_q0 = std::move(q[0]);
+            } else {
+                H->host_parts.push_back(build_rank_part(H->host, 1, 0, H->lg, H->starts));
+            }
         } else if (rank < 0) {
             for (int r = 0; r < nranks; ++r)
                 H->host_parts.push_back(build_rank_part(H->host, nranks, r, H->lg, H->starts));
@@ -2816,6 +2985,12 @@ static amg_status setup_impl(int64_t n, const int64_t* ptr, const int32_t* col, 
         }
         ck(cudaMallocHost(&H->ks_host, sizeof(KState)), "cudaMallocHost");
         ck(cudaDeviceSynchronize(), "setup sync");
+        if (H->reordered) {
+            const int64_t n0 = H->parts[0].lv[0].n;
+            H->dq0 = H->upload(H->reorder_q0);
+            H->rf = H->dalloc(n0);
+            H->rx = H->dalloc(n0);
+        }
         H->on_device = true;
     } catch (const amgb::CudaError& e) {
         cudaGetLastError();
@@ -2869,15 +3044,11 @@ amg_status amg_solve(amg_handle h, const double* f, double* x, double tol, int32
     if (!(tol >= 0) || maxiter < 0) return set_error(AMG_E_INVALID_ARG, "tol >= 0, maxiter >= 0");
     try {
         ck(cudaSetDevice(h->h->device), "cudaSetDevice");
-        if (h->h->prm.solver == 2) {
-            if (h->h->distributed()) return set_error(AMG_E_INVALID_ARG, "GMRES: single-GPU handles only");
-            return h->h->solve_gmres(f, x, tol, maxiter, iters, rel);
-        }
-        if (h->h->prm.solver == 3) {
-            if (h->h->distributed()) return set_error(AMG_E_INVALID_ARG, "IDR(s): single-GPU handles only");
-            return h->h->solve_idrs(f, x, tol, maxiter, iters, rel);
-        }
-        return h->h->solve(f, x, tol, maxiter, iters, rel);
+        if (h->h->prm.solver == 2 && h->h->distributed())
+            return set_error(AMG_E_INVALID_ARG, "GMRES: single-GPU handles only");
+        if (h->h->prm.solver == 3 && h->h->distributed())
+            return set_error(AMG_E_INVALID_ARG, "IDR(s): single-GPU handles only");
+        return h->h->solve_api(f, x, tol, maxiter, iters, rel);
     } catch (const amgb::CudaError& e) {
         cudaGetLastError();
         return set_error(AMG_E_CUDA, e.msg);
@@ -2901,9 +3072,7 @@ amg_status amg_solve_host(amg_handle h, const double* f, const double* x0, doubl
             ck(cudaMemcpyAsync(H.hx, x0, n * sizeof(double), cudaMemcpyHostToDevice, H.stream), "H2D x0");
         else
             ck(cudaMemsetAsync(H.hx, 0, n * sizeof(double), H.stream), "zero x0");
-        amg_status st = H.prm.solver == 2 && !H.distributed()   ? H.solve_gmres(H.hf, H.hx, tol, maxiter, iters, rel)
-                        : H.prm.solver == 3 && !H.distributed() ? H.solve_idrs(H.hf, H.hx, tol, maxiter, iters, rel)
-                                                                : H.solve(H.hf, H.hx, tol, maxiter, iters, rel);
+        amg_status st = H.solve_api(H.hf, H.hx, tol, maxiter, iters, rel);
         ck(cudaMemcpyAsync(x, H.hx, n * sizeof(double), cudaMemcpyDeviceToHost, H.stream), "D2H x");
         ck(cudaStreamSynchronize(H.stream), "sync");
         return st;
@@ -2919,6 +3088,7 @@ amg_status amg_solve_batched(amg_handle h, int32_t k, const double* F, int64_t l
     Handle& H = *h->h;
     if (H.distributed()) return set_error(AMG_E_INVALID_ARG, "amg_solve_batched: single-GPU handles only");
     if (H.prm.solver != 0) return set_error(AMG_E_INVALID_ARG, "amg_solve_batched: CG only");
+    if (H.reordered) return set_error(AMG_E_INVALID_ARG, "amg_solve_batched: not available with params.reorder = 1");
     const int64_t n = H.parts[0].lv[0].n;
     if (k < 1 || k > amgb::kMaxK || !F || !X || !iters || !rel || ldf < n || ldx < n)
         return set_error(AMG_E_INVALID_ARG, "k in [1, 8], F/X/iters/rel non-NULL, ld >= n");
@@ -2939,7 +3109,14 @@ amg_status amg_precond_apply(amg_handle h, const double* r, double* z) {
     if (!r || !z || r == z) return set_error(AMG_E_INVALID_ARG, "r, z");
     try {
         ck(cudaSetDevice(h->h->device), "cudaSetDevice");
-        h->h->precond(r, z);
+        amgb::Handle& H = *h->h;
+        if (H.reordered) {
+            H.perm_in(r, H.rf);
+            H.precond(H.rf, H.rx);
+            H.perm_out(H.rx, z);
+        } else {
+            H.precond(r, z);
+        }
         ck(cudaGetLastError(), "launch");
     } catch (const amgb::CudaError& e) {
         return set_error(AMG_E_CUDA, e.msg);
@@ -3175,6 +3352,7 @@ amg_status amg_level_op(amg_handle h, int32_t l, int32_t op, const double* x, co
     if (amg_status st = need_device(h)) return st;
     Handle& H = *h->h;
     if (H.distributed()) return set_error(AMG_E_INVALID_ARG, "amg_level_op: single-GPU handles only");
+    if (H.reordered) return set_error(AMG_E_INVALID_ARG, "amg_level_op: not available with params.reorder = 1");
     Part& p = H.parts[0];
     const int nlev = (int)p.lv.size();
     if (l < 0 || l >= nlev) return set_error(AMG_E_INVALID_ARG, "level out of range");
