@@ -28,11 +28,21 @@ def main(path, marker="VCgUpdate"):
     for n, v in zip(names, t):
         tot[short(n)] += v
         cnt[short(n)] += 1
-    T = sum(tot.values())
-    print(f"# {len(t)} launches, {T / 1e6:.3f} ms total (ncu: serialised, cold-cache)")
-    print("# share  total_ms  launches  kernel")
+    # setup-phase kernels (GPU setup k_*, format conversion cv_*, CUB, torch) are
+    # listed apart: the shares are of the solve kernels
+    setup = {k for k in tot if re.match(r"(<unnamed>::)?(k_|cv_)|cub::|void cub|at::|void at::", k)}
+    T = sum(v for k, v in tot.items() if k not in setup)
+    S = sum(tot[k] for k in setup)
+    print(f"# {len(t)} launches; solve kernels {T / 1e6:.3f} ms, setup/other kernels {S / 1e6:.3f} ms "
+          "(ncu: serialised, cold-cache)")
+    print("# share of solve  total_ms  launches  kernel")
     for k, v in sorted(tot.items(), key=lambda x: -x[1]):
-        print(f"{100 * v / T:6.2f}% {v / 1e6:9.3f} {cnt[k]:6d}  {k}")
+        if k not in setup:
+            print(f"{100 * v / T:6.2f}% {v / 1e6:9.3f} {cnt[k]:6d}  {k}")
+    print("# setup / other kernels")
+    for k, v in sorted(tot.items(), key=lambda x: -x[1]):
+        if k in setup:
+            print(f"   --  {v / 1e6:9.3f} {cnt[k]:6d}  {k}")
     idx = [i for i, n in enumerate(names) if marker in n]
     if len(idx) > 2:
         per = collections.Counter(b - a for a, b in zip(idx, idx[1:])).most_common(1)[0][0]
