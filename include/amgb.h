@@ -87,12 +87,12 @@ typedef struct {
                                the same hierarchy either way (Algorithm 1,
                                PAPER.md:95-107).  Host-only handles (device = -1) use the host. */
     int32_t idrs_s;         /* IDR(s) shadow-space dimension s in {1, 2, 4, 8} [4] ("solver.s") */
-    int32_t reorder;        /* 1: locality reordering of the device store (single GPU): the same
-                               hierarchy stored as Q_l A_l Q_l^T, Q_l P_l Q_{l+1}^T, ... with q_0 =
-                               reverse Cuthill-McKee of A_0 and aggregates numbered by their root;
-                               amg_solve / amg_solve_host / amg_precond_apply permute f, x, r, z
-                               on entry and exit; amg_level_op and amg_solve_batched are not
-                               available [0] */
+    int32_t reorder;        /* locality reordering of the device store (single GPU):
+                               the same hierarchy stored as Q_l A_l Q_l^T, Q_l P_l Q_{l+1}^T, ...
+                               with q_0 = reverse Cuthill-McKee of A_0 and aggregates numbered by
+                               their root; every API call permutes its vectors on entry and exit.
+                               0 off, 1 on, 2 automatic: on when A_0's gathers are non-local (a
+                               256-row tile touches > 0.5 distinct 32-byte sectors per entry) [2] */
 } amg_params;
 
 /* Per-level statistics (amg_level_info). */
@@ -123,7 +123,7 @@ typedef struct {
     int32_t iters;          /* Krylov iterations (loop trips, DESIGN.md §3 R19) */
     int32_t vcycles;        /* preconditioner applications */
     int32_t status;
-    int32_t flags;          /* bit 0: the fused CG iteration ran */
+    int32_t flags;          /* bit 0: the fused CG iteration ran; bit 1: reordered store */
     int64_t kernel_launches;/* kernels this library launched during the solve */
     double solve_ms;        /* device time of the solve (events on the handle stream) */
     double rel_resid;       /* true |f - A x| / |f| */

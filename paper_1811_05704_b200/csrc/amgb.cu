@@ -480,7 +480,8 @@ struct Handle {
     bool reordered = false;
     std::vector<double> coarse_inv_perm;
     int64_t* dq0 = nullptr;        // q_0 on the device
-    std::vector<int64_t> reorder_q0;
+    std::vector<int64_t*> dq;      // q_l on the device, every level
+    std::vector<std::vector<int64_t>> reorder_q;
     double *rf = nullptr, *rx = nullptr;
     // matrices larger than this are read evict-first (AMGB_STREAM_MB overrides)
     int64_t stream_bytes = (std::getenv("AMGB_STREAM_MB") ? std::atoll(std::getenv("AMGB_STREAM_MB")) : 48) << 20;
@@ -980,13 +981,13 @@ struct Handle {
     amg_status solve_idrs(const double* f, double* x, double tol, int32_t maxiter, int32_t* iters, double* rel);
     amg_status solve_dispatch(const double* f, double* x, double tol, int32_t maxiter, int32_t* iters, double* rel);
     amg_status solve_api(const double* f, double* x, double tol, int32_t maxiter, int32_t* iters, double* rel);
-    void perm_in(const double* src, double* dst) {  // natural -> stored order
-        const int64_t n = parts[0].lv[0].n;
-        perm_to_kernel<<<grid_for(n), kBlock, 0, stream>>>(n, dq0, src, dst);
+    void perm_in(const double* src, double* dst, int l = 0) {  // natural -> stored order (level l)
+        const int64_t n = parts[0].lv[l].n;
+        perm_to_kernel<<<grid_for(n), kBlock, 0, stream>>>(n, dq[l], src, dst);
     }
-    void perm_out(const double* src, double* dst) {
-        const int64_t n = parts[0].lv[0].n;
-        perm_from_kernel<<<grid_for(n), kBlock, 0, stream>>>(n, dq0, src, dst);
+    void perm_out(const double* src, double* dst, int l = 0) {
+        const int64_t n = parts[0].lv[l].n;
+        perm_from_kernel<<<grid_for(n), kBlock, 0, stream>>>(n, dq[l], src, dst);
     }
     void bicgstab_iteration();
     amg_status solve(const double* f, double* x, double tol, int32_t maxiter, int32_t* iters, double* rel);
@@ -2214,6 +2215,7 @@ amg_status Handle::solve_api(const double* f, double* x, double tol, int32_t max
     const amg_status st = solve_dispatch(rf, rx, tol, maxiter, iters, rel);
     perm_out(rx, x);
     ck(cudaStreamSynchronize(stream), "sync");
+    stats.flags |= 2;  // bit 1: reordered store
     return st;
 }
 
@@ -2548,6 +2550,27 @@ double level_alg_bytes(int64_t n_, int64_t z_, int64_t p_, int64_t c_, const amg
 }
 
 // Upload one rank part into a device Part.
+// Gather locality of a matrix (params.reorder = 2, automatic): distinct 32-byte
+// sectors of the gathered vector touched by a 256-row tile, per entry, over a
+// sample of tiles -- about 0.2 for a stencil in natural order (neighbouring rows
+// share sectors), about 1 for a randomly permuted matrix.
+double gather_sectors_per_entry(const Csr& A) {
+    const int64_t tiles = (A.nrows + 255) / 256;
+    if (tiles == 0) return 0.0;
+    const int64_t step = std::max<int64_t>(1, tiles / 1024);
+    int64_t distinct = 0, ents = 0;
+    std::vector<int32_t> sec;
+    for (int64_t t = 0; t < tiles; t += step) {
+        const int64_t r0 = t * 256, r1 = std::min<int64_t>(A.nrows, r0 + 256);
+        sec.clear();
+        for (int64_t e = A.ptr[r0]; e < A.ptr[r1]; ++e) sec.push_back(A.col[e] >> 2);
+        std::sort(sec.begin(), sec.end());
+        distinct += std::unique(sec.begin(), sec.end()) - sec.begin();
+        ents += (int64_t)sec.size();
+    }
+    return ents ? (double)distinct / (double)ents : 0.0;
+}
+
 // Reverse Cuthill-McKee order of A's row pattern (params.reorder): breadth-first
 // from a minimum-degree node of each component, neighbours by ascending degree,
 // reversed.  Returns q with q[old] = new.
@@ -2826,7 +2849,7 @@ void amg_params_default(amg_params* p) {
     p->gmres_m = 30;
     p->setup_device = 1;
     p->idrs_s = 4;
-    p->reorder = 0;
+    p->reorder = 2;
 }
 
 const char* amg_last_error(void) { return amgb::g_err.c_str(); }
@@ -2840,7 +2863,7 @@ static amg_status check_params(const amg_params& p) {
     if (p.struct_size != sizeof(amg_params)) return set_error(AMG_E_INVALID_ARG, "amg_params: struct_size mismatch");
     if (p.coarsening < 0 || p.coarsening > 1) return set_error(AMG_E_INVALID_ARG, "coarsening must be 0 or 1");
     if (p.setup_device < 0 || p.setup_device > 1) return set_error(AMG_E_INVALID_ARG, "setup_device must be 0 or 1");
-    if (p.reorder < 0 || p.reorder > 1) return set_error(AMG_E_INVALID_ARG, "reorder must be 0 or 1");
+    if (p.reorder < 0 || p.reorder > 2) return set_error(AMG_E_INVALID_ARG, "reorder must be 0, 1 or 2");
     if (p.relax < 0 || p.relax > 2) return set_error(AMG_E_INVALID_ARG, "relax must be 0, 1 or 2");
     if (p.solver < 0 || p.solver > 3)
         return set_error(AMG_E_INVALID_ARG, "solver must be 0 (cg), 1 (bicgstab), 2 (gmres) or 3 (idrs)");
@@ -2919,11 +2942,14 @@ static amg_status setup_impl(int64_t n, const int64_t* ptr, const int32_t* col, 
         H->lg = first_replicated_level(H->host, nranks, gather_below);
         H->starts = level_starts(H->host, nranks, H->lg);
         if (nranks == 1) {
-            if (prm.reorder == 1 && prm.device >= 0) {  // locality reordering of the device store
+            const bool reorder = prm.device >= 0 && H->host.levels.size() > 1 &&
+                                 (prm.reorder == 1 ||
+                                  (prm.reorder == 2 && gather_sectors_per_entry(H->host.levels[0].A) > 0.5));
+            if (reorder) {  // locality reordering of the device store
                 std::vector<std::vector<int64_t>> q;
                 H->host_parts.push_back(reordered_part(H->host, q, H->coarse_inv_perm));
                 H->reordered = true;
-                H->reorder_q0 = std::move(q[0]);
+                H->reorder_q = std::move(q);
             } else {
                 H->host_parts.push_back(build_rank_part(H->host, 1, 0, H->lg, H->starts));
             }
@@ -2987,7 +3013,8 @@ static amg_status setup_impl(int64_t n, const int64_t* ptr, const int32_t* col, 
         ck(cudaDeviceSynchronize(), "setup sync");
         if (H->reordered) {
             const int64_t n0 = H->parts[0].lv[0].n;
-            H->dq0 = H->upload(H->reorder_q0);
+            for (const auto& q : H->reorder_q) H->dq.push_back(H->upload(q));
+            H->dq0 = H->dq[0];
             H->rf = H->dalloc(n0);
             H->rx = H->dalloc(n0);
         }
@@ -3088,13 +3115,28 @@ amg_status amg_solve_batched(amg_handle h, int32_t k, const double* F, int64_t l
     Handle& H = *h->h;
     if (H.distributed()) return set_error(AMG_E_INVALID_ARG, "amg_solve_batched: single-GPU handles only");
     if (H.prm.solver != 0) return set_error(AMG_E_INVALID_ARG, "amg_solve_batched: CG only");
-    if (H.reordered) return set_error(AMG_E_INVALID_ARG, "amg_solve_batched: not available with params.reorder = 1");
     const int64_t n = H.parts[0].lv[0].n;
     if (k < 1 || k > amgb::kMaxK || !F || !X || !iters || !rel || ldf < n || ldx < n)
         return set_error(AMG_E_INVALID_ARG, "k in [1, 8], F/X/iters/rel non-NULL, ld >= n");
     if (!(tol >= 0) || maxiter < 0) return set_error(AMG_E_INVALID_ARG, "tol >= 0, maxiter >= 0");
     try {
         ck(cudaSetDevice(H.device), "cudaSetDevice");
+        if (H.reordered) {  // columns permuted into the stored order and back
+            amgb::DevTmp tmp;
+            double* Fs = tmp.get<double>(k * n);
+            double* Xs = tmp.get<double>(k * n);
+            for (int j = 0; j < k; ++j) {
+                H.perm_in(F + j * ldf, Fs + j * n);
+                H.perm_in(X + j * ldx, Xs + j * n);
+            }
+            amg_status st;
+            if (k <= 2) st = H.solve_batched<2>(k, Fs, n, Xs, n, tol, maxiter, iters, rel);
+            else if (k <= 4) st = H.solve_batched<4>(k, Fs, n, Xs, n, tol, maxiter, iters, rel);
+            else st = H.solve_batched<8>(k, Fs, n, Xs, n, tol, maxiter, iters, rel);
+            for (int j = 0; j < k; ++j) H.perm_out(Xs + j * n, X + j * ldx);
+            ck(cudaStreamSynchronize(H.stream), "sync");
+            return st;
+        }
         if (k <= 2) return H.solve_batched<2>(k, F, ldf, X, ldx, tol, maxiter, iters, rel);
         if (k <= 4) return H.solve_batched<4>(k, F, ldf, X, ldx, tol, maxiter, iters, rel);
         return H.solve_batched<8>(k, F, ldf, X, ldx, tol, maxiter, iters, rel);
@@ -3347,12 +3389,39 @@ amg_status amg_nccl_selftest(int32_t device) {
     return st;
 }
 
+static amg_status level_op_impl(amgb::Handle& H, int32_t l, int32_t op, const double* x, const double* f, double* y);
+
 amg_status amg_level_op(amg_handle h, int32_t l, int32_t op, const double* x, const double* f, double* y) {
     using namespace amgb;
     if (amg_status st = need_device(h)) return st;
     Handle& H = *h->h;
     if (H.distributed()) return set_error(AMG_E_INVALID_ARG, "amg_level_op: single-GPU handles only");
-    if (H.reordered) return set_error(AMG_E_INVALID_ARG, "amg_level_op: not available with params.reorder = 1");
+    const int nlev = (int)H.parts[0].lv.size();
+    if (l < 0 || l >= nlev) return set_error(AMG_E_INVALID_ARG, "level out of range");
+    if (!H.reordered) return level_op_impl(H, l, op, x, f, y);
+    // reordered store: the operands' levels (x, f, y) per op, permuted in and out
+    int lx = l, ly = l;
+    if (op == AMG_OP_SPMV_P) lx = std::min(l + 1, nlev - 1);
+    if (op == AMG_OP_SPMV_R) ly = std::min(l + 1, nlev - 1);
+    try {
+        ck(cudaSetDevice(H.device), "cudaSetDevice");
+        DevTmp tmp;
+        double* xs = x ? tmp.get<double>(H.parts[0].lv[lx].n) : nullptr;
+        double* fs = f ? tmp.get<double>(H.parts[0].lv[l].n) : nullptr;
+        double* ys = tmp.get<double>(H.parts[0].lv[ly].n);
+        if (x) H.perm_in(x, xs, lx);
+        if (f) H.perm_in(f, fs, l);
+        const amg_status st = level_op_impl(H, l, op, xs, fs, ys);
+        if (st == AMG_OK) H.perm_out(ys, y, ly);
+        ck(cudaStreamSynchronize(H.stream), "sync");
+        return st;
+    } catch (const amgb::CudaError& e) {
+        return set_error(AMG_E_CUDA, e.msg);
+    }
+}
+
+static amg_status level_op_impl(amgb::Handle& H, int32_t l, int32_t op, const double* x, const double* f, double* y) {
+    using namespace amgb;
     Part& p = H.parts[0];
     const int nlev = (int)p.lv.size();
     if (l < 0 || l >= nlev) return set_error(AMG_E_INVALID_ARG, "level out of range");

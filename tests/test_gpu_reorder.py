@@ -30,7 +30,7 @@ def host(t):
 def test_reordered_store_matches(gen, n, kw):
     p, c, v, f = synth.problem(gen, n)
     kw = dict(kw, coarse_enough=200)
-    hp = amgb.setup(p, c, v, **kw)
+    hp = amgb.setup(p, c, v, reorder=0, **kw)
     hr = amgb.setup(p, c, v, reorder=1, **kw)
     r = synth.random_vector(len(f))
     zp, zr = host(hp.precond(dev(r))), host(hr.precond(dev(r)))
@@ -47,13 +47,43 @@ def test_reordered_store_matches(gen, n, kw):
     assert ith == itr and np.array_equal(xh, host(xr))
 
 
-def test_reordered_store_limits():
+def test_reordered_level_ops_and_batched():
+    """amg_level_op permutes each operand with its level's order; the row sums
+    are formed exactly as on the plain store, so SpMV / residual / smoother /
+    transfer results are bitwise equal; the batched solve matches per column."""
+    p, c, v, f = synth.problem("poisson_perm", 30)
+    hp = amgb.setup(p, c, v, reorder=0, coarse_enough=200)
+    hr = amgb.setup(p, c, v, reorder=1, coarse_enough=200)
+    for l in range(hp.nlevels - 1):
+        n = hp.level_info(l)["rows"]
+        nc = hp.level_info(l + 1)["rows"]
+        x, fl, xc = synth.random_vector(n), synth.random_vector(n)[::-1].copy(), synth.random_vector(nc)
+        for op, xin, fin, ny in ((amgb.OP_SPMV_A, x, None, n), (amgb.OP_RESIDUAL, x, fl, n),
+                                 (amgb.OP_RELAX, x, fl, n), (amgb.OP_SPMV_P, xc, None, n),
+                                 (amgb.OP_SPMV_R, x, None, nc)):
+            ya = host(hp.level_op(l, op, x=dev(xin), f=dev(fin) if fin is not None else None, ny=ny))
+            yb = host(hr.level_op(l, op, x=dev(xin), f=dev(fin) if fin is not None else None, ny=ny))
+            assert np.array_equal(ya, yb), (l, op)
+    F = torch.stack([dev(f), dev(f[::-1].copy()), dev(f * 0.5)])
+    Xp, itp, _, stp = hp.solve_batched(F, tol=1e-8)
+    Xr, itr, _, str_ = hr.solve_batched(F, tol=1e-8)
+    assert stp == str_ == amgb.OK and np.max(np.abs(np.array(itp) - np.array(itr))) <= 1
+    assert np.linalg.norm(host(Xr) - host(Xp)) <= 1e-7 * np.linalg.norm(host(Xp))
+
+
+def test_automatic_reordering():
+    """reorder = 2 (default): on for a randomly permuted matrix, off for a
+    stencil in natural order (stats flags bit 1)."""
+    for gen, expect in (("poisson_perm", 2), ("poisson", 0)):
+        p, c, v, f = synth.problem(gen, 36)
+        h = amgb.setup(p, c, v, coarse_enough=200)
+        x, it, rel, st = h.solve(dev(f), tol=1e-8)
+        assert st == amgb.OK and h.stats()["flags"] & 2 == expect, gen
+
+
+def test_reordered_nonzero_initial_guess():
     p, c, v, f = synth.problem("poisson_perm", 20)
     hr = amgb.setup(p, c, v, reorder=1, coarse_enough=200)
-    with pytest.raises(amgb.AmgError):
-        hr.level_op(0, amgb.OP_SPMV_A, x=dev(f), ny=len(f))
-    with pytest.raises(amgb.AmgError):
-        hr.solve_batched(torch.stack([dev(f)] * 2))
     x0 = synth.random_vector(len(f))
-    x, it, rel, st = hr.solve(dev(f), x=dev(x0), tol=1e-8)  # non-zero initial guess is permuted too
+    x, it, rel, st = hr.solve(dev(f), x=dev(x0), tol=1e-8)  # the initial guess is permuted too
     assert st == amgb.OK and rel <= 1.01e-8
