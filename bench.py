@@ -61,7 +61,8 @@ def parse():
                     help="k > 1: k right-hand sides per solve (amg_solve_batched); value counts column V-cycles")
     ap.add_argument("--precision", default="double", choices=["double", "mixed"],
                     help="mixed: fp32 hierarchy values in the V-cycle (not the headline; SURVEY §8f rank 2)")
-    ap.add_argument("--reorder", action="store_true", help="locality reordering of the device store (params reorder=1)")
+    ap.add_argument("--reorder", default="auto", choices=["auto", "on", "off"],
+                    help="locality reordering of the device store (params reorder 2 / 1 / 0)")
     ap.add_argument("--json-out", default=None)
     return ap.parse_args()
 
@@ -293,7 +294,7 @@ def main():
     t0 = time.perf_counter()
     if world == 1:
         h = amgb.setup(ptr, col, val, prm, device=local, use_graph=0 if args.no_graph else 1,
-                       reorder=1 if args.reorder else 0)
+                       reorder={"auto": 2, "on": 1, "off": 0}[args.reorder])
         r0, r1 = 0, n
     else:
         # strong scaling: the global system row-partitioned over the ranks, halo
