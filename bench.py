@@ -345,6 +345,7 @@ def main():
                 acc["alg_bytes"] += s["alg_bytes"]
                 acc["status"].append(st)
                 acc["rel"].append(rel)
+                acc["flags"] = s["flags"]
             ev1.record(stream)
             torch.cuda.synchronize()
         acc["ms"] = ev0.elapsed_time(ev1)
@@ -443,6 +444,7 @@ def main():
                 f"{h.dist_info()['first_replicated']} distributed, coarser replicated)",
                 "levels": len(infos), "rows_per_level": [i["rows"] for i in infos],
                 "nnz_per_level": [i["nnz_A"] for i in infos],
+                "reordered_store": bool(A.get("flags", 0) & 2),
                 "dict_slice_frac_A0": round(infos[0]["dict_slices_A"] / max(1, (infos[0]["rows"] + 31) // 32), 4),
                 "iters_per_solve": iters_all[-1], "rel_resid": rels[-1], "status": statuses[-1],
                 "solve_ms": t_max_ms / args.steps, "setup_s": setup_s,
