@@ -457,7 +457,7 @@ def main():
             "roofline": {
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "kernel": "level-0 A-pass kernels (sell_rows on A0: res0 / relax+dot / cg-dir+dot / r0)",
+                "kernel": "level-0 A-pass kernels (one kernel template on A0 in the format pick_format chose: sell_tma at 256^3; res0 / relax+rho / cg-dir+sigma / initial and true residual)",
                 "launches_timed": prof_launch, "bytes_per_launch": prof_bytes / max(prof_launch, 1),
                 "ms_per_launch": prof_ms / max(prof_launch, 1), "peak_source": peak_src,
                 "timed_in": "a second timed region of the same K solves with CUDA-event record nodes "
