@@ -105,6 +105,10 @@ typedef struct {
     int64_t dev_bytes;                  /* device bytes of this level's store */
     int64_t padded_nnz_A;               /* stored (sliced-ELL) entries of A incl. padding */
     double alg_bytes_vcycle;            /* algorithmic HBM bytes of this level per V-cycle */
+    int64_t padded_nnz_P, padded_nnz_R; /* stored entries of P and R incl. padding */
+    int32_t sigma_mask;                 /* bit 0/1/2: A/P/R stored SELL-C-sigma (rows sorted by
+                                           length inside 256-row windows) */
+    int32_t reserved_;
 } amg_level_info;
 
 /* Test/export hook (amg_export_level): caller-owned HOST buffers, sized from

@@ -71,6 +71,8 @@ class LevelInfo(C.Structure):
         ("rows", C.c_int64), ("nnz_A", C.c_int64), ("nnz_P", C.c_int64), ("cols_P", C.c_int64),
         ("aggregates", C.c_int64), ("is_coarsest", C.c_int32), ("dict_slices_A", C.c_int32),
         ("dev_bytes", C.c_int64), ("padded_nnz_A", C.c_int64), ("alg_bytes_vcycle", C.c_double),
+        ("padded_nnz_P", C.c_int64), ("padded_nnz_R", C.c_int64), ("sigma_mask", C.c_int32),
+        ("reserved_", C.c_int32),
     ]
 
 

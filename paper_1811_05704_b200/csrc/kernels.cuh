@@ -31,7 +31,16 @@ struct Sell {
     const int32_t* col = nullptr;
     const double* val = nullptr;
     const float* valf = nullptr;  // fp32 copy of val (mixed-precision V-cycle)
+    // SELL-C-sigma (amgb.cu sigma_sort): slot s holds row (s & ~255) + rperm[s];
+    // nullptr = slots are rows
+    const uint8_t* rperm = nullptr;
 };
+
+// stored slot -> matrix row of a SELL-C-sigma matrix (rows sorted by length
+// inside aligned 256-row windows); the identity without a permutation
+__device__ __forceinline__ int64_t slot_row(const uint8_t* rperm, int64_t slot) {
+    return rperm ? (slot & ~(int64_t)255) + (int64_t)__ldg(rperm + slot) : slot;
+}
 
 // Krylov scalars kept on the device between kernels.
 struct KState {
@@ -224,7 +233,7 @@ __global__ void __launch_bounds__(kBlock, minb_of<Op>(PIPE ? 4 : 6)) sell_rows(S
         // row-local epilogue operands are requested first, so their latency
         // overlaps the matrix stream (single column; K-column rows load later)
         typename Op::Row rr{};
-        const int64_t grow = A.row0 + row;  // global row (views of a split pass)
+        const int64_t grow = A.row0 + slot_row(A.rperm, row);  // global row (views of a split pass)
         if constexpr (cols_of<Op>() == 1) rr = op.load(grow);
         const int64_t s = row >> 5;
         const int lane = (int)(row & 31);
@@ -303,6 +312,7 @@ struct SellTma {
     const float* valf = nullptr;    // fp32 copy of val (mixed-precision V-cycle)
     int32_t T = 1;          // lanes per row; slice height C = 32 / T
     int32_t tile_ent = 0;   // capacity of one stage in entries (max over tiles)
+    const uint8_t* rperm = nullptr;  // SELL-C-sigma slot -> row (T = 1: window = tile); see Sell
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -406,7 +416,9 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sel
             const int64_t slice = t * NS + warp;
             const int64_t lrow = slice * C + r;
             const bool has_row = slice < A.nslices && lrow < A.nrows;
-            const int64_t row = A.row0 + lrow;  // global row (views of a split pass)
+            // global row (views of a split pass); a sorted matrix has no
+            // dictionary slices, so `row` is only the epilogue's index there
+            const int64_t row = A.row0 + (has_row ? slot_row(A.rperm, lrow) : lrow);
             typename Op::Row rr{};
             if constexpr (cols_of<Op>() == 1)
                 if (pt == 0 && has_row) rr = op.load(row);  // in flight during the wait
