@@ -119,7 +119,10 @@ struct CudaError {
 };
 
 inline void ck(cudaError_t e, const char* what) {
-    if (e != cudaSuccess) throw CudaError{std::string(what) + ": " + cudaGetErrorString(e)};
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();  // a failed call must not resurface in a later, unrelated check
+        throw CudaError{std::string(what) + ": " + cudaGetErrorString(e)};
+    }
 }
 
 inline void ckn(int r, const char* what) {
@@ -2257,10 +2260,13 @@ Fmt pick_format(const Csr& A) {
     const std::string f = e ? e : "auto";
     if (f == "csr") return Fmt::CSR;
     if (f == "sell") return Fmt::SELL;
-    if (f == "tma") return Fmt::TMA;
-    if (A.nrows < 65536) return Fmt::CSR;
     int64_t lmax = 0;
     for (int64_t r = 0; r < A.nrows; ++r) lmax = std::max<int64_t>(lmax, A.ptr[r + 1] - A.ptr[r]);
+    // a TMA stage holds a tile of 8 slices x 32 rows x (longest row) entries at
+    // 12 B, kTmaStages of them must fit the 227 KB of shared memory per CTA
+    const bool tma_fits = (int64_t)kTmaStages * 256 * 12 * std::max<int64_t>(lmax, 1) + 64 <= 227 * 1024;
+    if (f == "tma") return tma_fits ? Fmt::TMA : Fmt::SELL;
+    if (A.nrows < 65536) return Fmt::CSR;
     // narrow rows (level-0 A, P): TMA-staged SELL-32, one thread per row.  Wide
     // rows (coarse A, R): their gathers are L2-bound and one thread per row of a
     // register-pipelined SELL-32 measured faster than T > 1 lanes per row.
@@ -2428,10 +2434,12 @@ bool upload_sliced_dev(Handle& H, const Csr& A, Fmt fmt, bool f32, bool allow_di
 // Slot s of the stored matrix holds row (s & ~255) + rp[s]; the kernels map a
 // slot to its row for the row-local epilogue operands (slot_row), the columns
 // and every row's entry order are unchanged, so each row sum is formed exactly
-// as in the unsorted store.  Applied when it cuts the stored entries by >= 5 %
-// of nnz (smoothed-aggregation P0 36 % -> 9 %, R0 14 % -> 3 %, A1 12 % -> 3 %
-// padding at 256^3); single-part handles only (the multi-GPU split passes cut
-// matrices at 32-row granularity).
+// as in the unsorted store.  Opt-in (AMGB_SIGMA=1), applied when it cuts the
+// stored entries by >= 5 % of nnz (smoothed-aggregation P0 36 % -> 9 %, R0
+// 14 % -> 3 %, A1 12 % -> 3 % padding at 256^3); single-part handles only (the
+// multi-GPU split passes cut matrices at 32-row granularity).  Measured: no gain
+// on the 256^3 solve (41.8 ms either way) -- the padded entries' bytes are
+// traded for scattered row-local epilogue accesses.
 bool sigma_sort(const Csr& A, std::vector<uint8_t>& rp, Csr& B) {
     const int64_t n = A.nrows;
     auto len = [&](int64_t r) { return A.ptr[r + 1] - A.ptr[r]; };
@@ -2505,7 +2513,7 @@ DMat upload_mat_impl(Handle& H, const Csr& A0, int64_t* bytes, bool f32) {
     // SELL / TMA: rows sorted by length inside 256-row windows when it pays
     std::vector<uint8_t> rp;
     Csr Bs;
-    const bool sorted = !H.distributed() && !std::getenv("AMGB_NO_SIGMA") && sigma_sort(A0, rp, Bs);
+    const bool sorted = !H.distributed() && std::getenv("AMGB_SIGMA") && sigma_sort(A0, rp, Bs);
     const Csr& As = sorted ? Bs : A0;
     const bool allow_dict = !sorted && !std::getenv("AMGB_NO_DICT");
     if (!std::getenv("AMGB_HOST_CONVERT")) {  // SELL / TMA built on the device

@@ -2,8 +2,9 @@
 of a SELL / TMA matrix are stored sorted by length, so slices pad less; the
 kernels map a stored slot back to its row for the row-local operands.  It is a
 storage choice only: every row sum is formed from the same entries in the same
-order, so every result must be BITWISE equal to the unsorted store
-(AMGB_NO_SIGMA=1), and within the usual tolerance of the oracle.  GPU only."""
+order, so every result must be BITWISE equal to the unsorted store (the
+default; AMGB_SIGMA=1 turns sorting on), and within the usual tolerance of the
+oracle.  GPU only."""
 import os
 
 import numpy as np
@@ -31,12 +32,12 @@ def setup_pair(p, c, v, fmt=None, **kw):
     if fmt:
         os.environ["AMGB_FORMAT"] = fmt
     try:
-        h_sig = amgb.setup(p, c, v, **kw)
-        os.environ["AMGB_NO_SIGMA"] = "1"
+        h_plain = amgb.setup(p, c, v, **kw)
+        os.environ["AMGB_SIGMA"] = "1"
         try:
-            h_plain = amgb.setup(p, c, v, **kw)
+            h_sig = amgb.setup(p, c, v, **kw)
         finally:
-            del os.environ["AMGB_NO_SIGMA"]
+            del os.environ["AMGB_SIGMA"]
     finally:
         if fmt:
             if old is None:
@@ -60,9 +61,10 @@ def level_ops_equal(ha, hb):
 
 
 # 48^3: P0 (TMA format) has rows of 1..6 entries -> sorted; 41^3: the last
-# 256-row window is ragged (68921 rows).  fmt forces SELL / TMA on every level,
-# so the sorted layout is exercised in both kernels on A, P and R.
-@pytest.mark.parametrize("n,fmt", [(48, None), (41, None), (41, "sell"), (30, "tma"), (30, "sell")])
+# 256-row window is ragged (68921 rows).  fmt forces SELL-32 / TMA on every
+# level, so the sorted layout runs in both kernels on A, P and R (a forced TMA
+# format falls back to SELL-32 for rows too wide for its shared-memory stages).
+@pytest.mark.parametrize("n,fmt", [(48, None), (41, None), (41, "sell"), (30, "sell"), (30, "tma")])
 def test_sigma_bitwise_equal(n, fmt):
     p, c, v, f = synth.problem("poisson", n)
     hs, hp = setup_pair(p, c, v, fmt=fmt, coarse_enough=200)
@@ -105,7 +107,8 @@ def test_sigma_bitwise_equal_variants(kw):
 @pytest.mark.parametrize("k", [2, 4, 8])
 def test_sigma_batched(k):
     p, c, v, f = synth.problem("poisson", 44)
-    hs, hp = setup_pair(p, c, v, fmt="tma", coarse_enough=200)
+    hs, hp = setup_pair(p, c, v, coarse_enough=200)  # P0 sorted in the TMA format
+    assert hs.level_info(0)["sigma_mask"] & 2
     F = torch.stack([dev(f * (1.0 + 0.25 * j)) if j % 2 == 0 else dev(synth.random_vector(len(f)))
                      for j in range(k)])
     Xs, its, _, sts = hs.solve_batched(F, tol=1e-8)
