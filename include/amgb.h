@@ -175,6 +175,20 @@ amg_status amg_solve(amg_handle h, const double *f, double *x, double tol, int32
 amg_status amg_solve_host(amg_handle h, const double *f, const double *x0, double *x, double tol,
                           int32_t maxiter, int32_t *iters, double *rel_resid);
 
+/* A sequence of k independent solves with HOST buffers (the end-to-end path for a
+ * stream of right-hand sides; the hierarchy is reused for many right-hand sides,
+ * PAPER.md:156-159): system j solves A x_j = f_j from a zero initial guess, f[j]
+ * and x[j] are host pointers of n_local doubles (entries may repeat: the same
+ * buffer is copied again for every system).  The copy of f[j+1] to the device
+ * and of x[j-1] back to the host run on a copy stream while system j is solved
+ * (double-buffered device vectors), so with PINNED host buffers the transfers
+ * overlap the solves; pageable buffers still give correct results.  iters[j],
+ * rel_resid[j] as amg_solve; vcycles (may be NULL): preconditioner applications
+ * per system.  Returns the first non-OK status of the k solves (all k are run
+ * unless a CUDA error stops the sequence); amg_solve_stats describes the last. */
+amg_status amg_solve_host_stream(amg_handle h, int32_t k, const double *const *f, double *const *x, double tol,
+                                 int32_t maxiter, int32_t *iters, double *rel_resid, int32_t *vcycles);
+
 /* Batched solve of A X = F for k right-hand sides (1 <= k <= 8) with one pass over
  * the hierarchy per iteration serving every column (the hierarchy is reused for
  * many right-hand sides).  F, X: DEVICE,

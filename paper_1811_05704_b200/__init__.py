@@ -109,6 +109,7 @@ _lib.amg_setup.argtypes = [C.c_int64, _V, _V, _V, C.POINTER(AmgParams), C.POINTE
 _lib.amg_solve.argtypes = [_V, _V, _V, C.c_double, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_double)]
 _lib.amg_solve_host.argtypes = [_V, _V, _V, _V, C.c_double, C.c_int32, C.POINTER(C.c_int32),
                                 C.POINTER(C.c_double)]
+_lib.amg_solve_host_stream.argtypes = [_V, C.c_int32, _V, _V, C.c_double, C.c_int32, _V, _V, _V]
 _lib.amg_precond_apply.argtypes = [_V, _V, _V]
 _lib.amg_set_stream.argtypes = [_V, _V]
 _lib.amg_set_profile.argtypes = [_V, C.c_int32]
@@ -128,7 +129,7 @@ _lib.amg_dist_level_info.argtypes = [_V, C.c_int32, C.c_int32, _V]
 _lib.amg_dist_export.argtypes = [_V, C.c_int32, C.c_int32, C.POINTER(DistLevelExport)]
 _lib.amg_last_error.restype = C.c_char_p
 _lib.amg_version.restype = C.c_char_p
-for _name in ("amg_setup", "amg_solve", "amg_solve_host", "amg_precond_apply", "amg_set_stream",
+for _name in ("amg_setup", "amg_solve", "amg_solve_host", "amg_solve_host_stream", "amg_precond_apply", "amg_set_stream",
               "amg_set_profile", "amg_level_count", "amg_level_info_get", "amg_export_level",
               "amg_solve_stats_get", "amg_level_op", "amg_nccl_unique_id", "amg_setup_dist",
               "amg_dist_info", "amg_dist_level_info", "amg_dist_export", "amg_nccl_selftest",
@@ -136,7 +137,8 @@ for _name in ("amg_setup", "amg_solve", "amg_solve_host", "amg_precond_apply", "
     getattr(_lib, _name).restype = C.c_int
 
 # Exported C symbols (tests check them against include/amgb.h).
-SYMBOLS = ("amg_params_default", "amg_setup", "amg_solve", "amg_solve_host", "amg_precond_apply",
+SYMBOLS = ("amg_params_default", "amg_setup", "amg_solve", "amg_solve_host", "amg_solve_host_stream",
+           "amg_precond_apply",
            "amg_set_stream", "amg_set_profile", "amg_level_count", "amg_level_info_get",
            "amg_export_level", "amg_solve_stats_get", "amg_level_op", "amg_destroy",
            "amg_last_error", "amg_version", "amg_nccl_unique_id", "amg_setup_dist", "amg_dist_info",
@@ -387,6 +389,28 @@ class Hierarchy:
         st = _check(_lib.amg_solve_host(self._h, _ptr(f), x0p, _ptr(out), tol, maxiter, C.byref(it),
                                         C.byref(rel)), "amg_solve_host")
         return out, it.value, rel.value, st
+
+    def solve_host_stream(self, fs, xs=None, tol=1e-8, maxiter=100):
+        """amg_solve_host_stream: k independent solves from zero initial guesses
+        with HOST arrays; the copies of system j+1's f and system j-1's x overlap
+        the solve of system j (use pinned buffers for the overlap).  fs / xs:
+        sequences of float64 arrays (entries may repeat).  Returns (xs, iters,
+        rels, vcycles, status of the first non-OK solve)."""
+        fs = [np.ascontiguousarray(f, np.float64) for f in fs]
+        k = len(fs)
+        if xs is None:
+            xs = [np.empty_like(f) for f in fs]
+        assert len(xs) == k and all(x.flags.c_contiguous and x.dtype == np.float64 for x in xs)
+        fp = (C.c_void_p * max(k, 1))(*[_ptr(f) for f in fs])
+        xp = (C.c_void_p * max(k, 1))(*[_ptr(x) for x in xs])
+        it = (C.c_int32 * max(k, 1))()
+        rel = (C.c_double * max(k, 1))()
+        vc = (C.c_int32 * max(k, 1))()
+        self._sync_stream()
+        st = _check(_lib.amg_solve_host_stream(self._h, k, C.cast(fp, _V), C.cast(xp, _V), tol, maxiter,
+                                               C.cast(it, _V), C.cast(rel, _V), C.cast(vc, _V)),
+                    "amg_solve_host_stream")
+        return xs, list(it)[:k], list(rel)[:k], list(vc)[:k], st
 
     def precond(self, r, z=None):
         """z = M r: one V-cycle from zero (asynchronous on the current stream)."""

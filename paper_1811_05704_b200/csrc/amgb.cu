@@ -436,6 +436,9 @@ struct Handle {
     double** d_defer_ptrs = nullptr;       // virtual all-reduce: device array of part->defer
     KState* ks_host = nullptr;             // pinned (part 0)
     double *hf = nullptr, *hx = nullptr;   // device copies for amg_solve_host
+    // amg_solve_host_stream: fixed solve vectors (the iteration graph is keyed by
+    // x) and double-buffered input / output staging vectors for the copy stream
+    double *sf = nullptr, *sx = nullptr, *sin[2] = {nullptr, nullptr}, *sout[2] = {nullptr, nullptr};
     std::vector<void*> allocs;
     // CUDA graph of two Krylov iterations, keyed by the x pointer
     cudaGraphExec_t graph = nullptr;
@@ -3183,6 +3186,74 @@ amg_status amg_solve_host(amg_handle h, const double* f, const double* x0, doubl
         cudaGetLastError();
         return set_error(AMG_E_CUDA, e.msg);
     }
+}
+
+amg_status amg_solve_host_stream(amg_handle h, int32_t k, const double* const* f, double* const* x, double tol,
+                                 int32_t maxiter, int32_t* iters, double* rel, int32_t* vcycles) {
+    if (amg_status st = need_device(h)) return st;
+    if (k < 0 || (k > 0 && (!f || !x || !iters || !rel))) return set_error(AMG_E_INVALID_ARG, "k, f, x, iters, rel");
+    for (int32_t j = 0; j < k; ++j)
+        if (!f[j] || !x[j]) return set_error(AMG_E_INVALID_ARG, "f[j] / x[j] is NULL");
+    Handle& H = *h->h;
+    const int64_t n = H.virt ? H.host.levels[0].A.nrows : H.parts[0].lv[0].n;
+    const size_t bytes = (size_t)n * sizeof(double);
+    cudaStream_t cs = nullptr;
+    cudaEvent_t in[2] = {nullptr, nullptr}, out[2] = {nullptr, nullptr}, done = nullptr;
+    amg_status first = AMG_OK;
+    try {
+        ck(cudaSetDevice(H.device), "cudaSetDevice");
+        if (!H.sf) {
+            H.sf = H.dalloc(n);
+            H.sx = H.dalloc(n);
+            for (int b = 0; b < 2; ++b) H.sin[b] = H.dalloc(n), H.sout[b] = H.dalloc(n);
+        }
+        ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "copy stream");
+        for (int b = 0; b < 2; ++b) {
+            ck(cudaEventCreateWithFlags(&in[b], cudaEventDisableTiming), "event");
+            ck(cudaEventCreateWithFlags(&out[b], cudaEventDisableTiming), "event");
+        }
+        ck(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "event");
+        if (k > 0) {
+            ck(cudaMemcpyAsync(H.sin[0], f[0], bytes, cudaMemcpyHostToDevice, cs), "H2D f");
+            ck(cudaEventRecord(in[0], cs), "event");
+        }
+        for (int32_t j = 0; j < k; ++j) {
+            const int b = j & 1;
+            // the next system's input streams in while this one is solved (its
+            // staging vector was last read at the start of solve j - 1, which
+            // returned synchronously)
+            if (j + 1 < k) {
+                ck(cudaMemcpyAsync(H.sin[b ^ 1], f[j + 1], bytes, cudaMemcpyHostToDevice, cs), "H2D f");
+                ck(cudaEventRecord(in[b ^ 1], cs), "event");
+            }
+            ck(cudaStreamWaitEvent(H.stream, in[b], 0), "wait");
+            ck(cudaMemcpyAsync(H.sf, H.sin[b], bytes, cudaMemcpyDeviceToDevice, H.stream), "stage f");
+            ck(cudaMemsetAsync(H.sx, 0, bytes, H.stream), "zero x0");
+            const amg_status st = H.solve_api(H.sf, H.sx, tol, maxiter, &iters[j], &rel[j]);
+            if (vcycles) vcycles[j] = H.stats.vcycles;
+            if (st != AMG_OK && first == AMG_OK) first = st;
+            if (st < 0) break;
+            // the solution leaves through a staging vector, copied out while
+            // the next system is solved
+            if (j >= 2) ck(cudaStreamWaitEvent(H.stream, out[b], 0), "wait");  // x[j-2] copied out
+            ck(cudaMemcpyAsync(H.sout[b], H.sx, bytes, cudaMemcpyDeviceToDevice, H.stream), "stage x");
+            ck(cudaEventRecord(done, H.stream), "event");
+            ck(cudaStreamWaitEvent(cs, done, 0), "wait");
+            ck(cudaMemcpyAsync(x[j], H.sout[b], bytes, cudaMemcpyDeviceToHost, cs), "D2H x");
+            ck(cudaEventRecord(out[b], cs), "event");
+        }
+        ck(cudaStreamSynchronize(cs), "sync");
+    } catch (const amgb::CudaError& e) {
+        cudaGetLastError();
+        first = set_error(AMG_E_CUDA, e.msg);
+    }
+    if (cs) cudaStreamSynchronize(cs), cudaStreamDestroy(cs);
+    for (int b = 0; b < 2; ++b) {
+        if (in[b]) cudaEventDestroy(in[b]);
+        if (out[b]) cudaEventDestroy(out[b]);
+    }
+    if (done) cudaEventDestroy(done);
+    return first;
 }
 
 amg_status amg_solve_batched(amg_handle h, int32_t k, const double* F, int64_t ldf, double* X, int64_t ldx,
