@@ -59,3 +59,20 @@ def test_params_defaults_and_validation_host_only():
             amgb.setup(ptr, col, val, device=-1, **bad)
         assert e.value.code == amgb.E_INVALID_ARG
     assert np.isfinite(h.level_info(0)["alg_bytes_vcycle"])
+
+
+def test_host_only_handle_rejects_solves_and_reports_store_fields():
+    """amg_solve_host_stream needs a device handle (error, not a crash, on a
+    host-only handle); level info of a host-only handle has no device store."""
+    import numpy as np
+    import pytest
+
+    import synth
+    ptr, col, val, f = synth.problem("poisson", 10)
+    h = amgb.setup(ptr, col, val, device=-1, coarse_enough=100)
+    with pytest.raises(amgb.AmgError) as e:
+        h.solve_host_stream([f, f])
+    assert e.value.code < 0 and "amg_solve_host_stream failed" in str(e.value)
+    info = h.level_info(0)
+    assert info["padded_nnz_P"] == 0 and info["padded_nnz_R"] == 0 and info["sigma_mask"] == 0
+    assert info["nnz_P"] > 0 and np.isfinite(info["alg_bytes_vcycle"])
