@@ -308,6 +308,28 @@ struct VCgUpdateMF {
         mf[i] = m[i] * rn;
         d[0] += rn * rn;
     }
+    __device__ bool aligned16() const {
+        return ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(r) | reinterpret_cast<uintptr_t>(p) |
+                 reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(mf)) &
+                15) == 0;
+    }
+    // Elements 2j and 2j+1 (same arithmetic as elem, loads issued first).
+    __device__ void elem2(int64_t j, double* d) const {
+        const double2 pv = __ldg(reinterpret_cast<const double2*>(p) + j);
+        const double2 qv = __ldg(reinterpret_cast<const double2*>(q) + j);
+        const double2 mv = __ldg(reinterpret_cast<const double2*>(m) + j);
+        double2 xv = reinterpret_cast<const double2*>(x)[j];
+        double2 rv = reinterpret_cast<const double2*>(r)[j];
+        xv.x = fma(alpha, pv.x, xv.x);
+        xv.y = fma(alpha, pv.y, xv.y);
+        rv.x = fma(-alpha, qv.x, rv.x);
+        rv.y = fma(-alpha, qv.y, rv.y);
+        reinterpret_cast<double2*>(x)[j] = xv;
+        reinterpret_cast<double2*>(r)[j] = rv;
+        reinterpret_cast<double2*>(mf)[j] = make_double2(mv.x * rv.x, mv.y * rv.y);
+        d[0] += rv.x * rv.x;
+        d[0] += rv.y * rv.y;
+    }
 };
 
 struct VBiP {
