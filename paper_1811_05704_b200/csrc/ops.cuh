@@ -132,6 +132,11 @@ struct FinSigmaX {  // FinSigma + bookkeeping of the deferred updates
 };
 
 // x += alpha p (the last deferred x update after the loop)
+// 16-B vector access for the paired (elem2) vector ops: elements 2j, 2j+1.
+__device__ __forceinline__ double2 ld2(const double* a, int64_t j) { return reinterpret_cast<const double2*>(a)[j]; }
+__device__ __forceinline__ void st2(double* a, int64_t j, double2 v) { reinterpret_cast<double2*>(a)[j] = v; }
+__device__ __forceinline__ bool al16(const void* a) { return (reinterpret_cast<uintptr_t>(a) & 15) == 0; }
+
 struct VAxpyAlpha {
     static constexpr int NDOT = 0, STREAMS = 3;
     double* x;
@@ -284,6 +289,19 @@ struct VCgUpdate {
         r[i] = rn;
         d[0] += rn * rn;
     }
+    __device__ bool aligned16() const { return al16(x) && al16(r) && al16(p) && al16(q); }
+    __device__ void elem2(int64_t j, double* d) const {
+        const double2 pv = ld2(p, j), qv = ld2(q, j);
+        double2 xv = ld2(x, j), rv = ld2(r, j);
+        xv.x = fma(alpha, pv.x, xv.x);
+        xv.y = fma(alpha, pv.y, xv.y);
+        rv.x = fma(-alpha, qv.x, rv.x);
+        rv.y = fma(-alpha, qv.y, rv.y);
+        st2(x, j, xv);
+        st2(r, j, rv);
+        d[0] += rv.x * rv.x;
+        d[0] += rv.y * rv.y;
+    }
 };
 
 // The same update, also writing mf = m o r_new for the next V-cycle's level-0
@@ -350,6 +368,16 @@ struct VBiP {
     __device__ void elem(int64_t i, double*) const {
         p[i] = first ? r[i] : fma(beta, p[i] - omega * v[i], r[i]);
     }
+    __device__ bool aligned16() const { return al16(r) && al16(v) && al16(p); }
+    __device__ void elem2(int64_t j, double*) const {
+        const double2 rv = ld2(r, j);
+        if (first) {
+            st2(p, j, rv);
+            return;
+        }
+        const double2 vv = ld2(v, j), pv = ld2(p, j);
+        st2(p, j, make_double2(fma(beta, pv.x - omega * vv.x, rv.x), fma(beta, pv.y - omega * vv.y, rv.y)));
+    }
 };
 
 struct VBiS {
@@ -366,6 +394,14 @@ struct VBiS {
         const double si = fma(-alpha, v[i], r[i]);
         s[i] = si;
         d[0] += si * si;
+    }
+    __device__ bool aligned16() const { return al16(r) && al16(v) && al16(s); }
+    __device__ void elem2(int64_t j, double* d) const {
+        const double2 rv = ld2(r, j), vv = ld2(v, j);
+        const double2 sv = make_double2(fma(-alpha, vv.x, rv.x), fma(-alpha, vv.y, rv.y));
+        st2(s, j, sv);
+        d[0] += sv.x * sv.x;
+        d[0] += sv.y * sv.y;
     }
 };
 
@@ -398,6 +434,27 @@ struct VBiX {
         r[i] = rn;
         d[0] += rhat[i] * rn;
         d[1] += rn * rn;
+    }
+    __device__ bool aligned16() const {
+        return al16(x) && al16(r) && al16(ph) && al16(sh) && al16(s) && al16(t) && al16(rhat);
+    }
+    __device__ void elem2(int64_t j, double* d) const {
+        const double2 phv = ld2(ph, j);
+        double2 xv = ld2(x, j);
+        if (half) {
+            st2(x, j, make_double2(fma(alpha, phv.x, xv.x), fma(alpha, phv.y, xv.y)));
+            return;
+        }
+        const double2 shv = ld2(sh, j), sv = ld2(s, j), tv = ld2(t, j), hv = ld2(rhat, j);
+        xv.x = fma(omega, shv.x, fma(alpha, phv.x, xv.x));
+        xv.y = fma(omega, shv.y, fma(alpha, phv.y, xv.y));
+        st2(x, j, xv);
+        const double2 rn = make_double2(fma(-omega, tv.x, sv.x), fma(-omega, tv.y, sv.y));
+        st2(r, j, rn);
+        d[0] += hv.x * rn.x;
+        d[1] += rn.x * rn.x;
+        d[0] += hv.y * rn.y;
+        d[1] += rn.y * rn.y;
     }
 };
 
