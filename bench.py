@@ -14,7 +14,8 @@ HBM.  value = V-cycles per second over the K timed steps (whole job).
                   [--problem poisson|poisson_perm|varcoef|convdiff] [--n 256]
 
 --impl reference times the oracle (plain fp64 C, oracle/) on the host cores:
-one step = one oracle CG iteration (one V-cycle) on the same system.
+one step = one full oracle solve of the same system (V-cycles / time, as
+cpu_baseline).
 
 Multi-GPU (torchrun, N > 1): strong scaling -- the same global system is
 row-partitioned over the N GPUs (halo exchange, all-reduce and coarse-level
@@ -168,12 +169,52 @@ def cpu_baseline_full_solve(ptr, col, val, f, cfg, tol, maxiter):
     res = oracle_solver(cfg)(A, f, tol=tol, maxiter=maxiter, hier=hier)
     t_solve = time.perf_counter() - t0
     vcyc = res.get("vcycles", res["iters"])
+    # a bounded 1-thread sample: one oracle V-cycle (or_precond)
+    # on the same hierarchy with the OpenMP row loops on one thread
+    one = None
+    try:
+        import ctypes
+        gomp = ctypes.CDLL("libgomp.so.1")
+        gomp.omp_get_max_threads.restype = ctypes.c_int
+        nt = gomp.omp_get_max_threads()
+        gomp.omp_set_num_threads(1)
+        try:
+            r = synth.random_vector(len(f))
+            t0 = time.perf_counter()
+            hier.precond(r)
+            one = time.perf_counter() - t0
+        finally:
+            gomp.omp_set_num_threads(nt)
+    except OSError:
+        pass
     return dict(setup_s=t_setup, solve_s=t_solve, iters=res["iters"], vcycles=vcyc, x=res["x"],
-                rel=res["rel_resid"])
+                rel=res["rel_resid"], one_thread_vcycle_s=one)
+
+
+def cpu_info():
+    """Host CPU model name and core count (the oracle baseline's machine)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+def oracle_threads():
+    """Threads the oracle's OpenMP row loops use (OMP_NUM_THREADS, else all cores)."""
+    v = os.environ.get("OMP_NUM_THREADS")
+    return int(v) if v and v.isdigit() else os.cpu_count()
 
 
 def run_reference(args, cfg):
-    """--impl reference: the oracle timed on the host cores (rank 0 only)."""
+    """--impl reference: the oracle timed on the host cores (rank 0 only).  One
+    step = one full oracle solve of the same system from x = 0 to the same
+    tolerance (setup untimed), value = V-cycles / time, exactly as cpu_baseline."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -184,29 +225,28 @@ def run_reference(args, cfg):
     hier = oracle.Hierarchy(A, relax=cfg["relax"])
     t_setup = time.perf_counter() - t0
     fn = oracle_solver(cfg)
-    x = np.zeros(len(f))
-    # one step = one Krylov iteration (maxiter = 1, restarted from the current x)
     for _ in range(args.warmup):
-        x = fn(A, f, x0=x, tol=0.0, maxiter=1, hier=hier)["x"]
-    vc = 0
+        fn(A, f, tol=args.tol, maxiter=cfg["maxiter"], hier=hier)
+    vc, iters = 0, 0
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        r = fn(A, f, x0=x, tol=0.0, maxiter=1, hier=hier)
-        x = r["x"]
+        r = fn(A, f, tol=args.tol, maxiter=cfg["maxiter"], hier=hier)
         vc += r.get("vcycles", r["iters"])
+        iters = r["iters"]
     dt = time.perf_counter() - t0
-    cores = os.cpu_count()
+    cores = oracle_threads()
     value = vc / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": value,
         "unit": "V-cycles/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, synth/)",
-        "config": {"workload": workload_name(args, cfg), "step": "one oracle Krylov iteration "
-                   "(1 V-cycle + outer work, restarted from the current x)",
-                   "oracle_setup_s": t_setup},
+        "config": {"workload": workload_name(args, cfg),
+                   "step": f"one full oracle solve from x = 0 to tol {args.tol} ({iters} iterations)",
+                   "oracle_setup_s": t_setup, **cpu_info()},
         "cpu_baseline": {"value": value, "unit": "V-cycles/s", "cores": cores, "kind": "oracle",
-                         "sample": f"{args.steps} oracle CG iterations of the {args.n}^3 system"},
+                         "sample": f"{args.steps} full oracle solves of the {args.n}^3 system "
+                                   f"({iters} iterations each; setup untimed)"},
         "e2e": {"value": value, "unit": "V-cycles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -406,12 +446,22 @@ def main():
     peak, peak_src = peaks()
     achieved = (prof_bytes / (prof_ms / 1e3)) / 1e9 if prof_ms > 0 else None
     solve_gbs = (alg_bytes / (elapsed_ms / 1e3)) / 1e9
-    traffic = None
+    # roofline.traffic: DRAM bytes per level-0 A-pass launch from the committed
+    # ncu --set full capture (profiles/ncu_traffic.json); ncu cannot run inside
+    # this process, so the capture names the libamgb.so it profiled and the line
+    # says whether that is the build running here
+    traffic, traffic_src = None, None
     try:
+        import hashlib
+        with open(amgb.LIB_PATH, "rb") as fh_:
+            lib_sha = hashlib.sha256(fh_.read()).hexdigest()
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh_:
             tj = json.load(fh_)
-            if tj.get("workload") == workload_name(args, cfg):
-                traffic = tj.get("a0_pass_bytes_per_launch")
+        if tj.get("workload") == workload_name(args, cfg):
+            traffic = tj.get("a0_pass_bytes_per_launch")
+            traffic_src = {"file": "profiles/ncu_traffic.json", "capture": tj.get("source"),
+                           "lib_sha256": tj.get("lib_sha256"), "this_lib_sha256": lib_sha,
+                           "same_build": tj.get("lib_sha256") == lib_sha}
     except Exception:
         pass
 
@@ -420,10 +470,14 @@ def main():
     parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline_full_solve(ptr, col, val, f, cfg, tol, maxiter)
-        cpu = {"value": cb["vcycles"] / cb["solve_s"], "unit": "V-cycles/s", "cores": os.cpu_count(),
+        cpu = {"value": cb["vcycles"] / cb["solve_s"], "unit": "V-cycles/s", "cores": oracle_threads(),
                "kind": "oracle",
                "sample": f"one full oracle solve of the same {args.n}^3 system ({cb['iters']} iterations, "
-                         f"{cb['solve_s']:.1f} s; oracle setup {cb['setup_s']:.1f} s untimed)"}
+                         f"{cb['solve_s']:.1f} s; oracle setup {cb['setup_s']:.1f} s untimed)",
+               **cpu_info(),
+               "one_thread": None if cb["one_thread_vcycle_s"] is None else {
+                   "value": 1.0 / cb["one_thread_vcycle_s"], "unit": "V-cycles/s (V-cycle only)", "cores": 1,
+                   "sample": "one oracle V-cycle (or_precond) of the same hierarchy, OpenMP on 1 thread"}}
         xg = x.cpu().numpy()  # N = 1: the full solution
         parity = {"oracle_iters": cb["iters"], "gpu_iters": iters_all[-1],
                   "x_rel_diff": float(np.linalg.norm(xg - cb["x"]) / np.linalg.norm(cb["x"])),
@@ -458,6 +512,7 @@ def main():
             "roofline": {
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "traffic_source": traffic_src,
                 "kernel": "level-0 A-pass kernels (one kernel template on A0 in the format pick_format chose: sell_tma at 256^3; res0 / relax+rho / cg-dir+sigma / initial and true residual)",
                 "launches_timed": prof_launch, "bytes_per_launch": prof_bytes / max(prof_launch, 1),
                 "ms_per_launch": prof_ms / max(prof_launch, 1), "peak_source": peak_src,

@@ -21,7 +21,10 @@
  *     are legal; every row must hold a positive diagonal entry (the strength test
  *     a_ij^2 > eps^2 a_ii a_jj needs it).
  *   - "device" pointers are CUDA global-memory fp64 arrays on the handle's
- *     device, 16-byte aligned, length n, not aliased with each other; "host"
+ *     device, length n, not aliased with each other, 8-byte aligned (16-byte
+ *     alignment, e.g. any cudaMalloc / torch allocation, lets the vector kernels
+ *     use paired 16-byte accesses; amg_solve_stats.flags bit 2 reports when a
+ *     solve could not); "host"
  *     pointers are ordinary (pageable or pinned) host memory.
  *   - Work is issued on the handle's stream (amg_set_stream; default: a stream
  *     the handle creates, which is ordered with the legacy default stream).  Calls that return results (amg_solve*) synchronise that
@@ -108,8 +111,15 @@ typedef struct {
     int64_t padded_nnz_P, padded_nnz_R; /* stored entries of P and R incl. padding */
     int32_t sigma_mask;                 /* bit 0/1/2: A/P/R stored SELL-C-sigma (rows sorted by
                                            length inside 256-row windows) */
-    int32_t reserved_;
+    int32_t formats;                    /* device format of A | P << 4 | R << 8 (single-GPU
+                                           handles): AMG_FMT_* */
 } amg_level_info;
+
+/* device matrix formats (amg_level_info.formats) */
+enum { AMG_FMT_CSR = 0,      /* row-block CSR (csr_rows) */
+       AMG_FMT_SELL = 1,     /* SELL-32, one thread per row (sell_rows) */
+       AMG_FMT_TMA = 2,      /* TMA-staged SELL-32 with the column-offset dictionary (sell_tma) */
+       AMG_FMT_NONE = 15 };  /* no such matrix (coarsest level: P, R) */
 
 /* Test/export hook (amg_export_level): caller-owned HOST buffers, sized from
  * amg_level_info; any pointer may be NULL to skip that array.  R = P^T. */
@@ -127,7 +137,8 @@ typedef struct {
     int32_t iters;          /* Krylov iterations (loop trips, DESIGN.md §3 R19) */
     int32_t vcycles;        /* preconditioner applications */
     int32_t status;
-    int32_t flags;          /* bit 0: the fused CG iteration ran; bit 1: reordered store */
+    int32_t flags;          /* bit 0: the fused CG iteration ran; bit 1: reordered store;
+                               bit 2: f or x not 16-B aligned (scalar vector-kernel loop) */
     int64_t kernel_launches;/* kernels this library launched during the solve */
     double solve_ms;        /* device time of the solve (events on the handle stream) */
     double rel_resid;       /* true |f - A x| / |f| */
@@ -168,6 +179,10 @@ amg_status amg_setup(int64_t n, const int64_t *ptr, const int32_t *col, const do
  * PAPER.md:141-143, 209-215. */
 amg_status amg_solve(amg_handle h, const double *f, double *x, double tol, int32_t maxiter,
                      int32_t *iters, double *rel_resid);
+
+/* Length of the f / x vectors that amg_solve* take on this handle: n on a
+ * single-GPU or virtual-rank handle, this rank's row count on an NCCL rank. */
+amg_status amg_vector_length(amg_handle h, int64_t *n);
 
 /* Same as amg_solve with HOST buffers (the end-to-end path): copies f (and the
  * initial guess x0, unless x0 is NULL = zero guess) to the device, solves, and
@@ -228,6 +243,38 @@ enum { AMG_OP_SPMV_A = 0, AMG_OP_SPMV_P = 1, AMG_OP_SPMV_R = 2, AMG_OP_RESIDUAL 
        AMG_OP_RELAX = 4, AMG_OP_COARSE = 5, AMG_OP_VCYCLE = 6 };
 amg_status amg_level_op(amg_handle h, int32_t level, int32_t op, const double *x, const double *f,
                         double *y);
+
+/* TEST HOOK: one launch of a FUSED production kernel of the V-cycle / CG
+ * iteration on level `level` (< coarsest), with the same op struct and kernel
+ * template the solve runs, on caller DEVICE vectors (natural order; a reordered
+ * store permutes them in and out).  Operand roles per op (c = level + 1):
+ *   AMG_OP_RES0         out0 = in0 - A (m o in0)           a1, zero-start sweep + residual
+ *                                                          (SPAI-0/Jacobi; Alg. 2)
+ *   AMG_OP_RES0_MF      out0 = in0 - A in1  (in1 = m o f)  a1 with the precomputed m o f
+ *   AMG_OP_RESTRICT_MF  out0 = R in0 (level c), out1 = m_c o out0   a2
+ *   AMG_OP_PROL0        out0 = m o in1 + P in0 (in0 on level c)      a5
+ *   AMG_OP_PROL0_MF     out0 = in1 + P in0  (in1 = m o f)
+ *   AMG_OP_PROL_ADD     out0 += P in0       (out0 read and written)
+ *   AMG_OP_RELAX_RHO    out0 = in0 + m o (in1 - A in0), dot = (in1, out0)   a6
+ *   AMG_OP_CHEB_STEP    Chebyshev step k = (int)scalar of one smoother call: r = in1 - A in0
+ *                       (/ a_ii when scaled), out1 = alpha_k r + beta_k out1 (k = 0: alpha_0 r;
+ *                       out1 read and written), out0 = in0 + out1, dot = (in1, out0)
+ *   AMG_OP_CG_DIR       (level 0) out0 = in0 + scalar * in1, out1 = A out0, dot = (out0, out1)
+ *                       a7 (CG direction)
+ *   AMG_OP_CG_UPDATE    (level 0, SPAI-0/Jacobi) out0 += scalar in0, out1 -= scalar in1,
+ *                       out2 = m o out1, dot = |out1| (CG update + norm)
+ * Synchronous (dot is a host output).  AMG_E_INVALID_ARG for an op the handle's
+ * smoother does not use or a missing operand; single-GPU handles only. */
+enum { AMG_OP_RES0 = 7, AMG_OP_RES0_MF = 8, AMG_OP_RESTRICT_MF = 9, AMG_OP_PROL0 = 10, AMG_OP_PROL0_MF = 11,
+       AMG_OP_PROL_ADD = 12, AMG_OP_RELAX_RHO = 13, AMG_OP_CHEB_STEP = 14, AMG_OP_CG_DIR = 15,
+       AMG_OP_CG_UPDATE = 16 };
+typedef struct {
+    const double *in0, *in1;
+    double *out0, *out1, *out2;
+    double scalar;   /* beta (CG_DIR), alpha (CG_UPDATE), step k (CHEB_STEP) */
+    double dot;      /* out: the fused reduction */
+} amg_level_op_args;
+amg_status amg_level_op_ex(amg_handle h, int32_t level, int32_t op, amg_level_op_args *args);
 
 /* ---------------------------------------------------------------- multi-GPU
  * Row partition of the hierarchy over `nranks` ranks (the paper

@@ -114,6 +114,7 @@ def lib():
             L.or_vcycle.argtypes = [_P, C.c_int, _F64P, _F64P]
             L.or_precond.argtypes = [_P, _F64P, _F64P]
             L.or_relax.argtypes = [_P, C.c_int, _F64P, _F64P]
+            L.or_cheb_step.argtypes = [_P, C.c_int, C.c_int, _F64P, _F64P, _F64P, C.POINTER(C.c_double)]
             L.or_cg.argtypes = [_P, C.c_int64, _I64P, _I32P, _F64P, C.c_int, _F64P, _F64P,
                                 C.c_double, C.c_int32, C.POINTER(C.c_int32),
                                 C.POINTER(C.c_double), C.c_void_p]
@@ -336,6 +337,15 @@ class Hierarchy:
         x = np.array(x, np.float64, copy=True)
         _check(lib().or_relax(self._h, l, np.ascontiguousarray(f, np.float64), x))
         return x
+
+    def cheb_step(self, l, k, f, x, p, alpha=0.0):
+        """Step k of the Chebyshev smoother (or_cheb_step): returns (x', p',
+        alpha_k) from x, p and alpha_{k-1}."""
+        x = np.array(x, np.float64, copy=True)
+        p = np.array(p, np.float64, copy=True)
+        a = C.c_double(alpha)
+        _check(lib().or_cheb_step(self._h, l, k, np.ascontiguousarray(f, np.float64), x, p, C.byref(a)))
+        return x, p, a.value
 
     def complexities(self):
         infos = [self.info(l) for l in range(self.nlevels)]

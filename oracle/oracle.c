@@ -698,37 +698,52 @@ int or_level_smoother(const or_hier *h, int l, double *out) {
  *        k = 1: alpha = 2d/(2d^2 - c^2),    beta = alpha d - 1, p = alpha r + beta p
  *        k > 1: alpha = 1/(d - alpha c^2/4), beta = alpha d - 1, p = alpha r + beta p
  *        x = x + p */
+/* One step k of the Chebyshev recurrence above (the loop body of or_relax,
+ * exported so tests can check the library's single-step kernel row by row):
+ * r = f - A x; scaled: r_i = r_i / a_ii; alpha_k from *alpha (= alpha_{k-1} on
+ * entry, alpha_k on return); p = alpha r (k = 0) or alpha r + beta p; x = x + p. */
+int or_cheb_step(const or_hier *h, int l, int k, const double *f, double *x, double *p, double *alpha) {
+    if (l < 0 || l >= h->nlev - 1 || h->prm.relax != 2 || k < 0) {
+        set_err("or_cheb_step: not a Chebyshev level / step");
+        return OR_E_INVALID;
+    }
+    const or_csr *A = h->A[l];
+    int64_t n = A->nrows;
+    double d = h->cheb[l][2], c = h->cheb[l][3];
+    double *r = (double *)malloc((size_t)(n > 0 ? n : 1) * sizeof(double));
+    residual(A, f, x, r);
+    if (h->prm.cheb_scaled)
+        for (int64_t i = 0; i < n; i++) r[i] = r[i] / h->dinv_src[l][i];
+    if (k == 0) {
+        *alpha = 1.0 / d;
+        for (int64_t i = 0; i < n; i++) p[i] = *alpha * r[i];
+    } else {
+        if (k == 1)
+            *alpha = 2.0 * d / (2.0 * d * d - c * c);
+        else
+            *alpha = 1.0 / (d - *alpha * c * c / 4.0);
+        double beta = *alpha * d - 1.0;
+        for (int64_t i = 0; i < n; i++) p[i] = *alpha * r[i] + beta * p[i];
+    }
+    for (int64_t i = 0; i < n; i++) x[i] = x[i] + p[i];
+    free(r);
+    return OR_OK;
+}
+
 int or_relax(const or_hier *h, int l, const double *f, double *x) {
     const or_csr *A = h->A[l];
     int64_t n = A->nrows;
-    double *r = (double *)malloc((size_t)n * sizeof(double));
     if (h->prm.relax == 0 || h->prm.relax == 1) {
+        double *r = (double *)malloc((size_t)(n > 0 ? n : 1) * sizeof(double));
         residual(A, f, x, r);
         for (int64_t i = 0; i < n; i++) x[i] = x[i] + h->m[l][i] * r[i];
+        free(r);
     } else {
-        double d = h->cheb[l][2], c = h->cheb[l][3];
-        double *p = (double *)malloc((size_t)n * sizeof(double));
-        double alpha = 0.0, beta = 0.0;
-        for (int k = 0; k < h->prm.cheb_degree; k++) {
-            residual(A, f, x, r);
-            if (h->prm.cheb_scaled)
-                for (int64_t i = 0; i < n; i++) r[i] = r[i] / h->dinv_src[l][i];
-            if (k == 0) {
-                alpha = 1.0 / d;
-                for (int64_t i = 0; i < n; i++) p[i] = alpha * r[i];
-            } else {
-                if (k == 1)
-                    alpha = 2.0 * d / (2.0 * d * d - c * c);
-                else
-                    alpha = 1.0 / (d - alpha * c * c / 4.0);
-                beta = alpha * d - 1.0;
-                for (int64_t i = 0; i < n; i++) p[i] = alpha * r[i] + beta * p[i];
-            }
-            for (int64_t i = 0; i < n; i++) x[i] = x[i] + p[i];
-        }
+        double *p = (double *)malloc((size_t)(n > 0 ? n : 1) * sizeof(double));
+        double alpha = 0.0;
+        for (int k = 0; k < h->prm.cheb_degree; k++) or_cheb_step(h, l, k, f, x, p, &alpha);
         free(p);
     }
-    free(r);
     return OR_OK;
 }
 

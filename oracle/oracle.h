@@ -101,6 +101,9 @@ int or_vcycle(const or_hier *h, int l, const double *f, double *x);
 int or_precond(const or_hier *h, const double *r, double *z);
 /* One relaxation call S(A_l, f, x) (Algorithm 2 lines "S_i(A_i, f_i, u_i)"). */
 int or_relax(const or_hier *h, int l, const double *f, double *x);
+/* Step k of the Chebyshev smoother's recurrence (the body of or_relax's loop):
+ * x, p updated in place; *alpha = alpha_{k-1} in, alpha_k out (ignored for k = 0). */
+int or_cheb_step(const or_hier *h, int l, int k, const double *f, double *x, double *p, double *alpha);
 /* Preconditioned CG / BiCGStab.  x: initial guess in,
  * solution out.  precond = 0 runs the unpreconditioned method (M = I) for pins. */
 int or_cg(const or_hier *h, int64_t n, const int64_t *ptr, const int32_t *col, const double *val,

@@ -35,6 +35,9 @@ E_INVALID_ARG, E_BAD_CSR, E_ZERO_DIAG, E_SINGULAR_COARSE = -1, -2, -3, -4
 E_COARSE_TOO_LARGE, E_OOM, E_NO_DEVICE, E_CUDA = -5, -6, -7, -10
 
 OP_SPMV_A, OP_SPMV_P, OP_SPMV_R, OP_RESIDUAL, OP_RELAX, OP_COARSE, OP_VCYCLE = range(7)
+(OP_RES0, OP_RES0_MF, OP_RESTRICT_MF, OP_PROL0, OP_PROL0_MF, OP_PROL_ADD, OP_RELAX_RHO, OP_CHEB_STEP,
+ OP_CG_DIR, OP_CG_UPDATE) = range(7, 17)
+FMT_CSR, FMT_SELL, FMT_TMA, FMT_NONE = 0, 1, 2, 15
 PROF_CLASSES = ("A0 pass", "A coarse", "transfer", "vector", "coarse solve")
 
 
@@ -72,8 +75,13 @@ class LevelInfo(C.Structure):
         ("aggregates", C.c_int64), ("is_coarsest", C.c_int32), ("dict_slices_A", C.c_int32),
         ("dev_bytes", C.c_int64), ("padded_nnz_A", C.c_int64), ("alg_bytes_vcycle", C.c_double),
         ("padded_nnz_P", C.c_int64), ("padded_nnz_R", C.c_int64), ("sigma_mask", C.c_int32),
-        ("reserved_", C.c_int32),
+        ("formats", C.c_int32),
     ]
+
+
+class LevelOpArgs(C.Structure):
+    _fields_ = [("in0", C.c_void_p), ("in1", C.c_void_p), ("out0", C.c_void_p), ("out1", C.c_void_p),
+                ("out2", C.c_void_p), ("scalar", C.c_double), ("dot", C.c_double)]
 
 
 class LevelExport(C.Structure):
@@ -118,7 +126,9 @@ _lib.amg_level_info_get.argtypes = [_V, C.c_int32, C.POINTER(LevelInfo)]
 _lib.amg_export_level.argtypes = [_V, C.c_int32, C.POINTER(LevelExport)]
 _lib.amg_solve_stats_get.argtypes = [_V, C.POINTER(SolveStats)]
 _lib.amg_level_op.argtypes = [_V, C.c_int32, C.c_int32, _V, _V, _V]
+_lib.amg_level_op_ex.argtypes = [_V, C.c_int32, C.c_int32, C.POINTER(LevelOpArgs)]
 _lib.amg_destroy.argtypes = [_V]
+_lib.amg_vector_length.argtypes = [_V, C.POINTER(C.c_int64)]
 _lib.amg_nccl_unique_id.argtypes = [_V]
 _lib.amg_solve_batched.argtypes = [_V, C.c_int32, _V, C.c_int64, _V, C.c_int64, C.c_double, C.c_int32, _V, _V]
 _lib.amg_nccl_selftest.argtypes = [C.c_int32]
@@ -131,7 +141,7 @@ _lib.amg_last_error.restype = C.c_char_p
 _lib.amg_version.restype = C.c_char_p
 for _name in ("amg_setup", "amg_solve", "amg_solve_host", "amg_solve_host_stream", "amg_precond_apply", "amg_set_stream",
               "amg_set_profile", "amg_level_count", "amg_level_info_get", "amg_export_level",
-              "amg_solve_stats_get", "amg_level_op", "amg_nccl_unique_id", "amg_setup_dist",
+              "amg_solve_stats_get", "amg_level_op", "amg_level_op_ex", "amg_vector_length", "amg_nccl_unique_id", "amg_setup_dist",
               "amg_dist_info", "amg_dist_level_info", "amg_dist_export", "amg_nccl_selftest",
               "amg_solve_batched"):
     getattr(_lib, _name).restype = C.c_int
@@ -140,7 +150,7 @@ for _name in ("amg_setup", "amg_solve", "amg_solve_host", "amg_solve_host_stream
 SYMBOLS = ("amg_params_default", "amg_setup", "amg_solve", "amg_solve_host", "amg_solve_host_stream",
            "amg_precond_apply",
            "amg_set_stream", "amg_set_profile", "amg_level_count", "amg_level_info_get",
-           "amg_export_level", "amg_solve_stats_get", "amg_level_op", "amg_destroy",
+           "amg_export_level", "amg_solve_stats_get", "amg_level_op", "amg_level_op_ex", "amg_vector_length", "amg_destroy",
            "amg_last_error", "amg_version", "amg_nccl_unique_id", "amg_setup_dist", "amg_dist_info",
            "amg_dist_level_info", "amg_dist_export", "amg_nccl_selftest", "amg_solve_batched")
 
@@ -210,12 +220,34 @@ def version() -> str:
     return _lib.amg_version().decode()
 
 
+def _host_vec(a, n: int, name: str) -> np.ndarray:
+    """A host vector the C ABI reads or writes n doubles of (no length argument
+    crosses the ABI): exactly n C-contiguous float64 values, else ValueError."""
+    if not isinstance(a, np.ndarray) or a.dtype != np.float64 or a.ndim != 1 or not a.flags.c_contiguous:
+        raise ValueError(f"{name}: need a 1-D C-contiguous float64 numpy array")
+    if a.shape[0] != n:
+        raise ValueError(f"{name}: length {a.shape[0]} != {n} (the handle's vector length)")
+    return a
+
+
+def _dev_vec(t, n: int, name: str):
+    """A CUDA float64 tensor of exactly n contiguous elements, else ValueError."""
+    import torch
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float64 or not t.is_cuda:
+        raise ValueError(f"{name}: need a CUDA float64 tensor")
+    if t.numel() != n or not t.is_contiguous():
+        raise ValueError(f"{name}: need {n} contiguous elements (got {t.numel()})")
+    return t
+
+
 def _ptr(a):
     """Address of a numpy array or torch tensor (contiguous)."""
     if isinstance(a, np.ndarray):
-        assert a.flags.c_contiguous
+        if not a.flags.c_contiguous:
+            raise ValueError("array must be C-contiguous")
         return a.ctypes.data
-    assert a.is_contiguous()
+    if not a.is_contiguous():
+        raise ValueError("tensor must be contiguous")
     return a.data_ptr()
 
 
@@ -239,6 +271,9 @@ class Hierarchy:
                                        val.ctypes.data, C.byref(self.prm), C.byref(dist),
                                        C.byref(h)), "amg_setup_dist")
         self._h = h
+        vl = C.c_int64()
+        _check(_lib.amg_vector_length(h, C.byref(vl)), "amg_vector_length")
+        self.vec_len = vl.value  # length of the f / x vectors amg_solve* take
         self.on_device = self.prm.device >= 0
         if self.on_device:
             import torch
@@ -261,7 +296,10 @@ class Hierarchy:
     def level_info(self, l: int) -> dict:
         li = LevelInfo()
         _check(_lib.amg_level_info_get(self._h, l, C.byref(li)), "amg_level_info_get")
-        return {k: getattr(li, k) for k, _ in LevelInfo._fields_ if k != "reserved"}
+        d = {k: getattr(li, k) for k, _ in LevelInfo._fields_}
+        f = d["formats"]
+        d["fmt_A"], d["fmt_P"], d["fmt_R"] = f & 15, (f >> 4) & 15, (f >> 8) & 15
+        return d
 
     def complexities(self):
         inf = [self.level_info(l) for l in range(self.nlevels)]
@@ -352,8 +390,10 @@ class Hierarchy:
         """Solve A x = f on the GPU; f, x are CUDA float64 tensors (x: initial
         guess, overwritten).  Returns (x, iters, rel_resid, status)."""
         import torch
+        _dev_vec(f, self.vec_len, "f")
         if x is None:
             x = torch.zeros_like(f)
+        _dev_vec(x, self.vec_len, "x")
         self._sync_stream()
         it, rel = C.c_int32(), C.c_double()
         st = _check(_lib.amg_solve(self._h, _ptr(f), _ptr(x), tol, maxiter, C.byref(it), C.byref(rel)),
@@ -380,10 +420,13 @@ class Hierarchy:
                    out: np.ndarray | None = None):
         """End-to-end solve with HOST arrays (copies inside the library call).
         x0 = None: zero initial guess (not copied).  out: solution buffer."""
-        f = np.ascontiguousarray(f, np.float64)
+        n = self.vec_len
+        f = _host_vec(np.ascontiguousarray(f, np.float64), n, "f")
         if out is None:
             out = np.empty_like(f)
-        x0p = None if x0 is None else _ptr(np.ascontiguousarray(x0, np.float64))
+        _host_vec(out, n, "out")
+        x0 = None if x0 is None else _host_vec(np.ascontiguousarray(x0, np.float64), n, "x0")
+        x0p = None if x0 is None else _ptr(x0)
         self._sync_stream()
         it, rel = C.c_int32(), C.c_double()
         st = _check(_lib.amg_solve_host(self._h, _ptr(f), x0p, _ptr(out), tol, maxiter, C.byref(it),
@@ -396,11 +439,15 @@ class Hierarchy:
         the solve of system j (use pinned buffers for the overlap).  fs / xs:
         sequences of float64 arrays (entries may repeat).  Returns (xs, iters,
         rels, vcycles, status of the first non-OK solve)."""
-        fs = [np.ascontiguousarray(f, np.float64) for f in fs]
+        n = self.vec_len
+        fs = [_host_vec(np.ascontiguousarray(f, np.float64), n, f"fs[{j}]") for j, f in enumerate(fs)]
         k = len(fs)
         if xs is None:
             xs = [np.empty_like(f) for f in fs]
-        assert len(xs) == k and all(x.flags.c_contiguous and x.dtype == np.float64 for x in xs)
+        if len(xs) != k:
+            raise ValueError(f"xs: {len(xs)} arrays for {k} right-hand sides")
+        for j, x in enumerate(xs):
+            _host_vec(x, n, f"xs[{j}]")
         fp = (C.c_void_p * max(k, 1))(*[_ptr(f) for f in fs])
         xp = (C.c_void_p * max(k, 1))(*[_ptr(x) for x in xs])
         it = (C.c_int32 * max(k, 1))()
@@ -415,8 +462,10 @@ class Hierarchy:
     def precond(self, r, z=None):
         """z = M r: one V-cycle from zero (asynchronous on the current stream)."""
         import torch
+        _dev_vec(r, self.vec_len, "r")
         if z is None:
             z = torch.empty_like(r)
+        _dev_vec(z, self.vec_len, "z")
         self._sync_stream()
         _check(_lib.amg_precond_apply(self._h, _ptr(r), _ptr(z)), "amg_precond_apply")
         return z
@@ -430,6 +479,18 @@ class Hierarchy:
         _check(_lib.amg_level_op(self._h, l, op, _ptr(x) if x is not None else None,
                                  _ptr(f) if f is not None else None, _ptr(y)), "amg_level_op")
         return y
+
+    def level_op_ex(self, l: int, op: int, in0=None, in1=None, out0=None, out1=None, out2=None,
+                    scalar: float = 0.0) -> float:
+        """Test hook (amg_level_op_ex): one fused production kernel on CUDA
+        float64 tensors; returns the fused dot (0.0 if the op has none)."""
+        a = LevelOpArgs()
+        for k, v in (("in0", in0), ("in1", in1), ("out0", out0), ("out1", out1), ("out2", out2)):
+            setattr(a, k, _ptr(v) if v is not None else None)
+        a.scalar = scalar
+        self._sync_stream()
+        _check(_lib.amg_level_op_ex(self._h, l, op, C.byref(a)), "amg_level_op_ex")
+        return a.dot
 
     def set_profile(self, mask: int):
         """Time kernel classes (bit c = PROF_CLASSES[c]) with CUDA events; 0 = off."""

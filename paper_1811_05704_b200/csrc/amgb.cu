@@ -299,6 +299,15 @@ struct DMat {
     double mat_bytes(bool f32) const {
         return (f32 ? 4.0 : 8.0) * nnz + (idx_bytes < 0 ? 4.0 * nnz : (double)idx_bytes);
     }
+    // row-structure bytes the format's kernel reads per pass: CSR row pointers
+    // (4 B per row) and row-block starts; SELL-32 one 8-B slice offset per 32
+    // rows; TMA two (values and column offsets per slice)
+    double ptr_bytes() const {
+        const double ns = (double)((nrows + 31) / 32);
+        if (fmt == Fmt::TMA) return 16.0 * ns;
+        if (fmt == Fmt::SELL) return 8.0 * ns;
+        return 4.0 * nrows + 4.0 * (double)csr.nblocks;
+    }
     // Multi-GPU split pass: rows [ib0, ib1) have no ghost column
     // and run while the halo exchange is in flight, the rest after it.
     bool split = false;
@@ -759,7 +768,7 @@ struct Handle {
         // keep them cached so coarse levels stay L2-resident across cycles
         const bool big = M.nnz * 12 > stream_bytes;
         const DMat& Mo = M.origin ? *M.origin : M;  // a view accounts a share of its matrix's pass
-        const double bytes = M.bytes_scale * (Mo.mat_bytes(F32) + 4.0 * Mo.nrows + 8.0 * Mo.ncols * Op::GATHER +
+        const double bytes = M.bytes_scale * (Mo.mat_bytes(F32) + Mo.ptr_bytes() + 8.0 * Mo.ncols * Op::GATHER +
                                               8.0 * Mo.nrows * Op::ROWV);
         const Red& red = red_slot ? *red_slot : p.red;
         launch(mat_class(p, M), bytes, what, [&] {
@@ -1482,7 +1491,9 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
     stats.iters = ks_host->iter;
     stats.vcycles = bicg ? 2 * ks_host->iter - (ks_host->half ? 1 : 0) : ks_host->iter;
     stats.status = ks_host->status;
-    stats.flags = cg_fused ? 1 : 0;
+    // bit 2: the caller's f or x is not 16-B aligned, so the paired 16-B vector
+    // kernels (vec_kernel elem2) took their scalar loop on x
+    stats.flags = (cg_fused ? 1 : 0) | ((((uintptr_t)f | (uintptr_t)x) & 15) ? 4 : 0);
     stats.kernel_launches = launches - launches0;
     stats.solve_ms = ms;
     stats.rel_resid = *rel;
@@ -2516,7 +2527,8 @@ DMat upload_mat_impl(Handle& H, const Csr& A0, int64_t* bytes, bool f32) {
     // SELL / TMA: rows sorted by length inside 256-row windows when it pays
     std::vector<uint8_t> rp;
     Csr Bs;
-    const bool sorted = !H.distributed() && std::getenv("AMGB_SIGMA") && sigma_sort(A0, rp, Bs);
+    const char* sg = std::getenv("AMGB_SIGMA");
+    const bool sorted = !H.distributed() && sg && sg[0] == '1' && sigma_sort(A0, rp, Bs);
     const Csr& As = sorted ? Bs : A0;
     const bool allow_dict = !sorted && !std::getenv("AMGB_NO_DICT");
     if (!std::getenv("AMGB_HOST_CONVERT")) {  // SELL / TMA built on the device
@@ -3161,6 +3173,13 @@ amg_status amg_solve(amg_handle h, const double* f, double* x, double tol, int32
     }
 }
 
+amg_status amg_vector_length(amg_handle h, int64_t* n) {
+    if (!h || !h->h || !n) return set_error(AMG_E_INVALID_ARG, "NULL argument");
+    const Handle& H = *h->h;
+    *n = (H.virt || H.parts.empty()) ? H.host.levels[0].A.nrows : H.parts[0].lv[0].n;
+    return AMG_OK;
+}
+
 amg_status amg_solve_host(amg_handle h, const double* f, const double* x0, double* x, double tol,
                           int32_t maxiter, int32_t* iters, double* rel) {
     if (amg_status st = need_device(h)) return st;
@@ -3357,6 +3376,11 @@ amg_status amg_level_info_get(amg_handle h, int32_t l, amg_level_info* out) {
         out->padded_nnz_P = coarsest ? 0 : L.P.stored;
         out->padded_nnz_R = coarsest ? 0 : L.R.stored;
         out->sigma_mask = (L.A.sigma ? 1 : 0) | (L.P.sigma ? 2 : 0) | (L.R.sigma ? 4 : 0);
+        auto code = [](const amgb::DMat& M, bool none) {
+            if (none) return (int)AMG_FMT_NONE;
+            return M.fmt == amgb::Fmt::TMA ? (int)AMG_FMT_TMA : M.fmt == amgb::Fmt::SELL ? (int)AMG_FMT_SELL : (int)AMG_FMT_CSR;
+        };
+        out->formats = code(L.A, coarsest && l > 0) | code(L.P, coarsest) << 4 | code(L.R, coarsest) << 8;
     }
     return AMG_OK;
 }
@@ -3632,6 +3656,152 @@ static amg_status level_op_impl(amgb::Handle& H, int32_t l, int32_t op, const do
         return set_error(AMG_E_CUDA, e.msg);
     }
     return AMG_OK;
+}
+
+// ---- amg_level_op_ex: the fused production kernels, one launch each --------
+static amg_status level_op_ex_impl(amgb::Handle& H, int32_t l, int32_t op, amg_level_op_args& a) {
+    using namespace amgb;
+    Part& p = H.parts[0];
+    const int nlev = (int)p.lv.size();
+    if (l < 0 || l >= nlev - 1) return set_error(AMG_E_INVALID_ARG, "amg_level_op_ex: level must have a coarser level");
+    DevLevel& L = p.lv[l];
+    DevLevel& Cl = p.lv[l + 1];
+    const bool cheb = H.prm.relax == 2;
+    try {
+        ck(cudaSetDevice(H.device), "cudaSetDevice");
+        DevTmp tmp;
+        KState* ks = tmp.get<KState>(1);
+        double* dot = tmp.get<double>(4);
+        KState k0{};
+        k0.beta = a.scalar;
+        k0.alpha = a.scalar;
+        k0.maxiter = 1 << 30;
+        ck(cudaMemcpyAsync(ks, &k0, sizeof(KState), cudaMemcpyHostToDevice, H.stream), "ks");
+        ck(cudaMemsetAsync(dot, 0, 4 * sizeof(double), H.stream), "memset");
+        const FinStore fs{dot, 1};
+        bool has_dot = false, has_res = false;
+        auto need = [&](bool ok, const char* what) {
+            if (!ok) throw CudaError{std::string("amg_level_op_ex: ") + what};
+        };
+        switch (op) {
+            case AMG_OP_RES0:  // a1: t = f - A (m o f)
+                need(!cheb && a.in0 && a.out0, "RES0 needs SPAI-0/Jacobi, in0 = f, out0");
+                H.rows(p, L.A, OpRes0{L.m, a.in0, a.out0, {}}, nullptr, "res0");
+                break;
+            case AMG_OP_RES0_MF:  // a1 with mf = m o f given: t = f - A mf
+                need(a.in0 && a.in1 && a.out0, "RES0_MF needs in0 = f, in1 = mf, out0");
+                H.rows(p, L.A, OpRes0MF{a.in1, a.in0, a.out0, {}}, nullptr, "res0 (mf)");
+                break;
+            case AMG_OP_RESTRICT_MF:  // a2: f_c = R t, mf_c = m_c o f_c
+                need(!cheb && Cl.m && a.in0 && a.out0 && a.out1, "RESTRICT_MF needs a SPAI-0/Jacobi next level");
+                H.rows(p, L.R, OpSpmvMF{a.in0, a.out0, Cl.m, a.out1, {}}, nullptr, "restrict (+mf)");
+                break;
+            case AMG_OP_PROL0:  // a5: x = m o f + P e
+                need(!cheb && a.in0 && a.in1 && a.out0, "PROL0 needs SPAI-0/Jacobi, in0 = e, in1 = f, out0");
+                H.rows(p, L.P, OpProl0{a.in0, L.m, a.in1, a.out0, {}}, nullptr, "prolong0");
+                break;
+            case AMG_OP_PROL0_MF:  // a5 with mf given: x = mf + P e
+                need(a.in0 && a.in1 && a.out0, "PROL0_MF needs in0 = e, in1 = mf, out0");
+                H.rows(p, L.P, OpProl0MF{a.in0, a.in1, a.out0, {}}, nullptr, "prolong0 (mf)");
+                break;
+            case AMG_OP_PROL_ADD:  // a5 general: x += P e
+                need(a.in0 && a.out0, "PROL_ADD needs in0 = e, out0 = x (in/out)");
+                H.rows(p, L.P, OpProlAdd{a.in0, a.out0, {}}, nullptr, "prolong");
+                break;
+            case AMG_OP_RELAX_RHO:  // a6: xo = x + m o (f - A x), (f, xo)
+                need(!cheb && a.in0 && a.in1 && a.out0 && a.in0 != a.out0, "RELAX_RHO needs in0 = x, in1 = f, out0");
+                H.rows(p, L.A, OpRelax<1, FinStore>{a.in0, L.m, a.in1, a.out0, fs}, nullptr, "relax+dot");
+                has_dot = true;
+                break;
+            case AMG_OP_CHEB_STEP: {  // one Chebyshev step k = scalar, (f, xo)
+                const int k = (int)a.scalar;
+                need(cheb && k >= 0 && k < H.prm.cheb_degree && a.in0 && a.in1 && a.out0 && a.out1 && a.in0 != a.out0,
+                     "CHEB_STEP needs Chebyshev, 0 <= k < degree, in0 = x, in1 = f, out0, out1 = p (in/out)");
+                H.rows(p, L.A,
+                       OpCheb<1, FinStore>{a.in0, a.in1, L.diag, a.out1, a.out0, L.cheb_alpha[k], L.cheb_beta[k],
+                                           H.prm.cheb_scaled, k == 0, fs},
+                       nullptr, "cheb+dot");
+                has_dot = true;
+                break;
+            }
+            case AMG_OP_CG_DIR:  // a7: p' = z + beta p, q = A p', (p', q)
+                need(l == 0 && a.in0 && a.in1 && a.out0 && a.out1, "CG_DIR on level 0: in0 = z, in1 = p, out0, out1");
+                H.rows(p, L.A, OpCgDir<FinStore>{a.in0, a.in1, a.out0, a.out1, ks, 0.0, fs}, nullptr, "cg dir");
+                has_dot = true;
+                break;
+            case AMG_OP_CG_UPDATE:  // a8: x += alpha p, r -= alpha q, mf = m o r, |r|
+                need(l == 0 && !cheb && a.in0 && a.in1 && a.out0 && a.out1 && a.out2,
+                     "CG_UPDATE on level 0 (SPAI-0/Jacobi): in0 = p, in1 = q, out0 = x, out1 = r, out2 = mf");
+                H.vec(p, L.n, VCgUpdateMF{a.out0, a.out1, a.in0, a.in1, L.m, a.out2, ks, 0.0, FinCgUpdate{ks}}, nullptr,
+                      "cg update (+mf)");
+                has_res = true;
+                break;
+            default:
+                return set_error(AMG_E_INVALID_ARG, "amg_level_op_ex: unknown op");
+        }
+        ck(cudaGetLastError(), "launch");
+        if (has_dot) {
+            ck(cudaMemcpyAsync(&a.dot, dot, sizeof(double), cudaMemcpyDeviceToHost, H.stream), "D2H");
+        } else if (has_res) {
+            KState kh{};
+            ck(cudaMemcpyAsync(&kh, ks, sizeof(KState), cudaMemcpyDeviceToHost, H.stream), "D2H");
+            ck(cudaStreamSynchronize(H.stream), "sync");
+            a.dot = kh.res;
+        }
+        ck(cudaStreamSynchronize(H.stream), "sync");  // scratch is freed at scope exit
+    } catch (const amgb::CudaError& e) {
+        return set_error(AMG_E_CUDA, e.msg);
+    }
+    return AMG_OK;
+}
+
+amg_status amg_level_op_ex(amg_handle h, int32_t l, int32_t op, amg_level_op_args* a) {
+    using namespace amgb;
+    if (amg_status st = need_device(h)) return st;
+    if (!a) return set_error(AMG_E_INVALID_ARG, "NULL args");
+    Handle& H = *h->h;
+    if (H.distributed()) return set_error(AMG_E_INVALID_ARG, "amg_level_op_ex: single-GPU handles only");
+    const int nlev = (int)H.parts[0].lv.size();
+    if (l < 0 || l >= nlev - 1) return set_error(AMG_E_INVALID_ARG, "level out of range");
+    if (!H.reordered) return level_op_ex_impl(H, l, op, *a);
+    // reordered store: every operand permuted into the stored order of its level
+    // (e and the restriction's outputs live on level l+1), outputs permuted back
+    const bool coarse_in0 = op == AMG_OP_PROL0 || op == AMG_OP_PROL0_MF || op == AMG_OP_PROL_ADD;
+    const bool coarse_out = op == AMG_OP_RESTRICT_MF;
+    const int l_in0 = coarse_in0 ? l + 1 : l, l_out = coarse_out ? l + 1 : l;
+    try {
+        ck(cudaSetDevice(H.device), "cudaSetDevice");
+        DevTmp tmp;
+        amg_level_op_args b = *a;
+        auto in = [&](const double* v, int lv) -> const double* {
+            if (!v) return nullptr;
+            double* s = tmp.get<double>(H.parts[0].lv[lv].n);
+            H.perm_in(v, s, lv);
+            return s;
+        };
+        auto io = [&](double* v, int lv) -> double* {  // outputs that are also read
+            if (!v) return nullptr;
+            double* s = tmp.get<double>(H.parts[0].lv[lv].n);
+            H.perm_in(v, s, lv);
+            return s;
+        };
+        b.in0 = in(a->in0, l_in0);
+        b.in1 = in(a->in1, l);
+        b.out0 = io(a->out0, l_out);
+        b.out1 = io(a->out1, l_out);
+        b.out2 = io(a->out2, l);
+        const amg_status st = level_op_ex_impl(H, l, op, b);
+        if (st == AMG_OK) {
+            if (a->out0) H.perm_out(b.out0, a->out0, l_out);
+            if (a->out1) H.perm_out(b.out1, a->out1, l_out);
+            if (a->out2) H.perm_out(b.out2, a->out2, l);
+            a->dot = b.dot;
+        }
+        ck(cudaStreamSynchronize(H.stream), "sync");
+        return st;
+    } catch (const amgb::CudaError& e) {
+        return set_error(AMG_E_CUDA, e.msg);
+    }
 }
 
 }  // extern "C"

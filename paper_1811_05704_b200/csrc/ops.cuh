@@ -56,6 +56,15 @@ struct FinInitRes {  // r0 = f - A x0: res, done; BiCGStab also rho = (r,r), |rh
     }
 };
 
+// Test hook (amg_level_op_ex): store the n reduced totals of a fused dot.
+struct FinStore {
+    double* out;
+    int n;
+    __device__ void operator()(const double* t) const {
+        for (int k = 0; k < n; ++k) out[k] = t[k];
+    }
+};
+
 struct FinTrueRes {
     KState* ks;
     __device__ void operator()(const double* t) const { ks->true_res = sqrt(t[0]); }
@@ -131,12 +140,12 @@ struct FinSigmaX {  // FinSigma + bookkeeping of the deferred updates
     }
 };
 
-// x += alpha p (the last deferred x update after the loop)
 // 16-B vector access for the paired (elem2) vector ops: elements 2j, 2j+1.
 __device__ __forceinline__ double2 ld2(const double* a, int64_t j) { return reinterpret_cast<const double2*>(a)[j]; }
 __device__ __forceinline__ void st2(double* a, int64_t j, double2 v) { reinterpret_cast<double2*>(a)[j] = v; }
 __device__ __forceinline__ bool al16(const void* a) { return (reinterpret_cast<uintptr_t>(a) & 15) == 0; }
 
+// x += alpha p (the last deferred x update after the loop)
 struct VAxpyAlpha {
     static constexpr int NDOT = 0, STREAMS = 3;
     double* x;

@@ -3,7 +3,10 @@ level-0 A-pass capture (scripts/gpu_ncu.sh): DRAM bytes per launch
 (dram__bytes_read.sum + dram__bytes_write.sum) of the A-pass kernels, which
 bench.py reports as roofline.traffic, plus a per-kernel table.
 
-  python scripts/ncu_traffic.py gpurun_out/prof_a0_raw.csv poisson256^3_cg_sa_spai0 "round 1 (v8)"
+  python scripts/ncu_traffic.py gpurun_out/prof_a0_raw.csv poisson256^3_cg_sa_spai0 "round 2" <lib sha256>
+
+The sha256 of the libamgb.so that was profiled is stored with the numbers, so
+bench.py can say whether its roofline.traffic comes from the build it runs.
 """
 import csv
 import json
@@ -14,7 +17,7 @@ SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 A_PASS = re.compile(r"sell_tma<1, 1, (OpRelax<1|OpCgDir|OpRes0|OpResidual)")
 
 
-def main(path, workload, source):
+def main(path, workload, source, lib_sha=None):
     rows = list(csv.reader(open(path)))
     hdr, units, data = rows[0], rows[1], rows[2:]
     col = {h: i for i, h in enumerate(hdr)}
@@ -49,10 +52,11 @@ def main(path, workload, source):
         "note": "dram__bytes_read.sum + dram__bytes_write.sum per launch, averaged over the captured "
                 "level-0 A-pass launches",
         "kernels": kernels,
+        "lib_sha256": lib_sha,
     }
     json.dump(out, open("profiles/ncu_traffic.json", "w"), indent=1)
     print(json.dumps({k: out[k] for k in ("a0_pass_bytes_per_launch", "a0_pass_kernels_averaged")}, indent=1))
 
 
 if __name__ == "__main__":
-    main(*sys.argv[1:4])
+    main(*sys.argv[1:5])

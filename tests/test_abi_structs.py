@@ -12,7 +12,8 @@ import paper_1811_05704_b200 as amgb
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PAIRS = [("amg_params", amgb.AmgParams), ("amg_level_info", amgb.LevelInfo),
          ("amg_level_export", amgb.LevelExport), ("amg_solve_stats", amgb.SolveStats),
-         ("amg_dist", amgb.AmgDist), ("amg_dist_level_export", amgb.DistLevelExport)]
+         ("amg_dist", amgb.AmgDist), ("amg_dist_level_export", amgb.DistLevelExport),
+         ("amg_level_op_args", amgb.LevelOpArgs)]
 
 
 @pytest.mark.skipif(shutil.which("gcc") is None, reason="gcc not available")

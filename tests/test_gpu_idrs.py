@@ -57,11 +57,17 @@ def test_idrs_converged_solve_matches_oracle(gen, n, s, kw):
     A = oracle.Csr(p, c, v)
     o = oracle.idrs(A, f, tol=1e-8, maxiter=300, s=s, hier=oracle.Hierarchy(A, **kw))
     assert o["status"] == 0
-    assert abs(it - o["iters"]) <= 2, (it, o["iters"])
+    # north-star bar: iterations (preconditioned products) +-1, x within 1e-8 at
+    # equal count (a run that stops one product apart is re-run at the oracle's)
+    assert abs(it - o["iters"]) <= 1, (it, o["iters"])
     xh = host(x)
-    assert np.linalg.norm(xh - o["x"]) <= 1e-6 * np.linalg.norm(o["x"])
     r = f - oracle.spmv(A, xh)
     assert np.linalg.norm(r) <= 1.01e-8 * np.linalg.norm(f)
+    if it != o["iters"]:
+        x, it, rel, st = h.solve(dev(f), tol=0.0, maxiter=o["iters"])
+        assert it == o["iters"]
+        xh = host(x)
+    assert np.linalg.norm(xh - o["x"]) <= 1e-8 * np.linalg.norm(o["x"])
 
 
 def test_idrs_edge_cases():

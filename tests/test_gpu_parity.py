@@ -243,3 +243,37 @@ def test_device_loop_and_host_loop_agree():
     x2, it2, rel2, _ = h.solve(dev(f), tol=1e-9)
     h.set_profile(0)
     assert it1 == it2 and np.array_equal(host(x1), host(x2))
+
+
+def test_misaligned_vector_views():
+    """f and x as 8-B-offset views (buf[1:n+1]): the paired 16-B vector kernels
+    take their scalar loop (stats flag bit 2), and the solve still matches the
+    oracle (iterations +-1, x within 1e-8 at equal count) and the host rejects
+    wrong lengths instead of reading past a buffer."""
+    p, c, v, f = synth.problem("poisson", 41)  # TMA store, odd n (68,921)
+    n = len(f)
+    h = amgb.setup(p, c, v)
+    fb = torch.zeros(n + 2, dtype=torch.float64, device="cuda")
+    xb = torch.zeros(n + 2, dtype=torch.float64, device="cuda")
+    fb[1:n + 1] = dev(f)
+    fv, xv = fb[1:n + 1], xb[1:n + 1]
+    assert fv.data_ptr() % 16 == 8 and xv.data_ptr() % 16 == 8
+    x, iters, rel, st = h.solve(fv, xv, tol=1e-8, maxiter=100)
+    assert h.stats()["flags"] & 4, "scalar vector-kernel loop expected"
+    o = oracle_solve(p, c, v, f, {}, 1e-8, 100)
+    assert st == amgb.OK and abs(iters - o["iters"]) <= 1 and rel <= 1.01e-8
+    if iters != o["iters"]:
+        xv.zero_()
+        x, iters, rel, st = h.solve(fv, xv, tol=0.0, maxiter=o["iters"])
+    assert np.linalg.norm(host(xv) - o["x"]) <= 1e-8 * np.linalg.norm(o["x"])
+    assert host(xb)[0] == 0.0 and host(xb)[n + 1] == 0.0  # nothing written outside the view
+    # aligned run: bit 2 clear; the same iteration count
+    x2, it2, _, _ = h.solve(dev(f), tol=1e-8, maxiter=100)
+    assert not (h.stats()["flags"] & 4) and abs(it2 - iters) <= 1
+    # wrong lengths are rejected on the host
+    with pytest.raises(ValueError):
+        h.solve(dev(f[:-1]))
+    with pytest.raises(ValueError):
+        h.solve_host(f[:-1])
+    with pytest.raises(ValueError):
+        h.solve_host_stream([f], xs=[np.empty(n - 1)])

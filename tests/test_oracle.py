@@ -747,3 +747,33 @@ def test_gmres_full_terminates_and_restart():
     assert r["status"] == oracle.OK and r["rel_resid"] <= 1e-10
     np.testing.assert_allclose(r["x"], np.linalg.solve(A.to_dense(), f), rtol=1e-8)
     assert r["vcycles"] >= r["iters"] + 1
+
+
+def test_cheb_step_composes_to_relax():
+    """or_cheb_step (one step of the Chebyshev recurrence, the loop body of
+    or_relax) chained K times equals one or_relax call bitwise, from a non-zero
+    x, scaled and unscaled; step 0 on a diagonal A from x = 0 is alpha_0 f / a_ii
+    (scaled: alpha_0 = 1/d with d = (1 + 1/30)/2 for D^-1 A = I)."""
+    for scaled in (1, 0):
+        p, c, v, f = synth.problem("varcoef", 12)
+        h = oracle.Hierarchy(oracle.Csr(p, c, v), relax="chebyshev", cheb_scaled=scaled, coarse_enough=100)
+        rng = np.random.default_rng(3)
+        for l in range(h.nlevels - 1):
+            n = h.info(l)["rows"]
+            fl, x = rng.standard_normal(n), rng.standard_normal(n)
+            xs, ps, a = x.copy(), np.zeros(n), 0.0
+            for k in range(h.prm.cheb_degree):
+                xs, ps, a = h.cheb_step(l, k, fl, xs, ps, a)
+            assert np.array_equal(xs, h.relax(l, fl, x)), (scaled, l)
+    # step 0 from x = 0: r = f exactly (A 0 = 0), so x_1 = p_1 = (1/d) (f / a_ii)
+    # (scaled) with d = (lmax + lmin) / 2 of the level's Gershgorin bounds
+    p, c, v, f = synth.problem("varcoef", 12)
+    h = oracle.Hierarchy(oracle.Csr(p, c, v), relax="chebyshev", coarse_enough=100)
+    A = h.matrix(0, "A")
+    diag = np.array([A.val[A.ptr[i]:A.ptr[i + 1]][A.col[A.ptr[i]:A.ptr[i + 1]] == i][0] for i in range(A.nrows)])
+    lmax, lmin, d, cc = h.smoother(0)
+    assert d == (lmax + lmin) / 2 and lmin == lmax * (1.0 / 30.0)
+    fl = np.random.default_rng(4).standard_normal(A.nrows)
+    x1, p1, a0 = h.cheb_step(0, 0, fl, np.zeros(A.nrows), np.zeros(A.nrows), 0.0)
+    assert a0 == 1.0 / d and np.array_equal(x1, p1)
+    assert np.array_equal(x1, a0 * (fl / diag))
