@@ -53,7 +53,11 @@ typedef enum {
     AMG_E_COARSE_TOO_LARGE = -5,/* coarsest level larger than dense_max */
     AMG_E_OOM = -6,
     AMG_E_NO_DEVICE = -7,       /* solve requested on a host-only handle */
-    AMG_E_CUDA = -10
+    AMG_E_CUDA = -10,
+    AMG_E_NCCL = -11            /* multi-GPU: NCCL unavailable or failed, or a peer rank did not
+                                   respond within AMGB_NCCL_TIMEOUT_S seconds [300] (communicator
+                                   creation, setup scatter, any host synchronisation of a solve);
+                                   the communicator is aborted and the handle must be destroyed */
 } amg_status;
 
 typedef struct amg_hierarchy *amg_handle;
@@ -278,16 +282,22 @@ amg_status amg_level_op_ex(amg_handle h, int32_t level, int32_t op, amg_level_op
 
 /* ---------------------------------------------------------------- multi-GPU
  * Row partition of the hierarchy over `nranks` ranks (the paper
- * runs the method over MPI processes).  Every rank passes the
- * SAME global matrix; the host setup is global and deterministic, each rank
- * keeps its contiguous row slice of every level (coarse rows follow their
- * aggregate roots) with ghost columns renumbered after the local ones, and
- * levels with fewer than gather_below rows are replicated on every rank.
+ * runs the method over MPI processes).  The host setup is
+ * global and deterministic (the hierarchy is the single-GPU one at every rank
+ * count); each rank keeps its contiguous row slice of every level (coarse rows
+ * follow their aggregate roots) with ghost columns renumbered after the local
+ * ones, and levels with fewer than gather_below rows are replicated on every rank.
  *   rank >= 0: one process per GPU; halo exchange / all-reduce / all-gather run
  *              over NCCL (loaded with dlopen) created from nccl_id, which rank 0
- *              obtains with amg_nccl_unique_id and broadcasts.  amg_solve then
- *              takes this rank's slice of f and x (rows row_starts[rank] ..
- *              row_starts[rank+1]-1, see amg_dist_info).
+ *              obtains with amg_nccl_unique_id and broadcasts.  Scattered setup:
+ *              the communicator is created first, then rank 0 alone builds the
+ *              hierarchy of the global matrix it was given and sends every other
+ *              rank its part over NCCL; ranks > 0 pass only n (ptr, col, val may
+ *              be NULL and are ignored) and never hold the global matrix.  A setup
+ *              error on rank 0 is returned on every rank.  amg_solve then takes
+ *              this rank's slice of f and x (rows row_starts[rank] ..
+ *              row_starts[rank+1]-1, see amg_dist_info).  Every wait on a peer is
+ *              bounded by AMGB_NCCL_TIMEOUT_S (AMG_E_NCCL).
  *   rank == -1: every rank lives in this process on one GPU ("virtual ranks":
  *              transport = device copies).  amg_solve / amg_precond_apply take
  *              the GLOBAL f and x.  Used to test the partitioned path on one GPU.
@@ -314,7 +324,8 @@ typedef struct {
 /* Write a fresh NCCL unique id (call on rank 0 only).  AMG_E_CUDA if NCCL is unavailable. */
 amg_status amg_nccl_unique_id(uint8_t id[128]);
 /* Distributed setup (see above); same errors as amg_setup, plus AMG_E_INVALID_ARG
- * for a hierarchy that cannot be distributed (a single level). */
+ * for a hierarchy that cannot be distributed (a single level) and AMG_E_NCCL.
+ * amg_export_level works on rank 0 only (the other ranks hold their parts). */
 amg_status amg_setup_dist(int64_t n, const int64_t *ptr, const int32_t *col, const double *val,
                           const amg_params *prm, const amg_dist *dist, amg_handle *out);
 /* nranks, first replicated level and the level-0 row starts (nranks+1 entries, may be NULL). */
@@ -330,6 +341,14 @@ amg_status amg_dist_export(amg_handle h, int32_t rank, int32_t level, const amg_
  * send/recv to self, all-reduce and broadcast, directly and replayed from a
  * captured CUDA graph, with the same calls the executor makes.  AMG_OK or an error. */
 amg_status amg_nccl_selftest(int32_t device);
+
+/* Self-test of the host shared-memory TEST transport (AMGB_TRANSPORT=shm: ranks
+ * of one node that share a GPU run the one-process-per-rank path through host
+ * shared memory instead of NCCL; every transfer synchronous on the host, no
+ * kernel waits on another rank).  Call from `nranks` processes with the same id;
+ * three personalised all-to-all rounds are checked.  AMG_OK or AMG_E_NCCL.
+ * Needs no GPU. */
+amg_status amg_shm_selftest(const uint8_t id[128], int32_t rank, int32_t nranks);
 
 void amg_destroy(amg_handle h);
 const char *amg_last_error(void);

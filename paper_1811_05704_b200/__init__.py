@@ -32,7 +32,7 @@ _lib = C.CDLL(LIB_PATH)
 # ---- status codes (amg_status) ----
 OK, NOT_CONVERGED, BREAKDOWN = 0, 1, 2
 E_INVALID_ARG, E_BAD_CSR, E_ZERO_DIAG, E_SINGULAR_COARSE = -1, -2, -3, -4
-E_COARSE_TOO_LARGE, E_OOM, E_NO_DEVICE, E_CUDA = -5, -6, -7, -10
+E_COARSE_TOO_LARGE, E_OOM, E_NO_DEVICE, E_CUDA, E_NCCL = -5, -6, -7, -10, -11
 
 OP_SPMV_A, OP_SPMV_P, OP_SPMV_R, OP_RESIDUAL, OP_RELAX, OP_COARSE, OP_VCYCLE = range(7)
 (OP_RES0, OP_RES0_MF, OP_RESTRICT_MF, OP_PROL0, OP_PROL0_MF, OP_PROL_ADD, OP_RELAX_RHO, OP_CHEB_STEP,
@@ -132,6 +132,7 @@ _lib.amg_vector_length.argtypes = [_V, C.POINTER(C.c_int64)]
 _lib.amg_nccl_unique_id.argtypes = [_V]
 _lib.amg_solve_batched.argtypes = [_V, C.c_int32, _V, C.c_int64, _V, C.c_int64, C.c_double, C.c_int32, _V, _V]
 _lib.amg_nccl_selftest.argtypes = [C.c_int32]
+_lib.amg_shm_selftest.argtypes = [_V, C.c_int32, C.c_int32]
 _lib.amg_setup_dist.argtypes = [C.c_int64, _V, _V, _V, C.POINTER(AmgParams), C.POINTER(AmgDist),
                                 C.POINTER(_V)]
 _lib.amg_dist_info.argtypes = [_V, C.POINTER(C.c_int32), C.POINTER(C.c_int32), _V]
@@ -143,7 +144,7 @@ for _name in ("amg_setup", "amg_solve", "amg_solve_host", "amg_solve_host_stream
               "amg_set_profile", "amg_level_count", "amg_level_info_get", "amg_export_level",
               "amg_solve_stats_get", "amg_level_op", "amg_level_op_ex", "amg_vector_length", "amg_nccl_unique_id", "amg_setup_dist",
               "amg_dist_info", "amg_dist_level_info", "amg_dist_export", "amg_nccl_selftest",
-              "amg_solve_batched"):
+              "amg_solve_batched", "amg_shm_selftest", "amg_vector_length"):
     getattr(_lib, _name).restype = C.c_int
 
 # Exported C symbols (tests check them against include/amgb.h).
@@ -152,7 +153,8 @@ SYMBOLS = ("amg_params_default", "amg_setup", "amg_solve", "amg_solve_host", "am
            "amg_set_stream", "amg_set_profile", "amg_level_count", "amg_level_info_get",
            "amg_export_level", "amg_solve_stats_get", "amg_level_op", "amg_level_op_ex", "amg_vector_length", "amg_destroy",
            "amg_last_error", "amg_version", "amg_nccl_unique_id", "amg_setup_dist", "amg_dist_info",
-           "amg_dist_level_info", "amg_dist_export", "amg_nccl_selftest", "amg_solve_batched")
+           "amg_dist_level_info", "amg_dist_export", "amg_nccl_selftest", "amg_solve_batched",
+           "amg_shm_selftest")
 
 RELAX = {"spai0": 0, "damped_jacobi": 1, "chebyshev": 2}
 COARSENING = {"smoothed_aggregation": 0, "aggregation": 1}
@@ -255,20 +257,27 @@ class Hierarchy:
     """amg_setup handle: AMG hierarchy of A, resident on the GPU (device >= 0) or
     host-only (device = -1, for setup/export only)."""
 
-    def __init__(self, ptr, col, val, params: dict | None = None, dist: AmgDist | None = None, **kw):
-        self._ptr = np.ascontiguousarray(ptr, np.int64)
-        col = np.ascontiguousarray(col, np.int32)
-        val = np.ascontiguousarray(val, np.float64)
-        self.n = len(self._ptr) - 1
+    def __init__(self, ptr, col, val, params: dict | None = None, dist: AmgDist | None = None, n: int | None = None,
+                 **kw):
         self.prm = make_params(params, **kw)
         self.dist = dist
         h = C.c_void_p()
-        if dist is None:
-            _check(_lib.amg_setup(self.n, self._ptr.ctypes.data, col.ctypes.data, val.ctypes.data,
-                                  C.byref(self.prm), C.byref(h)), "amg_setup")
+        if ptr is None:
+            # scattered multi-GPU setup, rank > 0: the matrix lives on rank 0 only
+            if dist is None or dist.rank <= 0 or n is None:
+                raise ValueError("ptr/col/val may be omitted only on NCCL ranks > 0 (with n given)")
+            self.n = int(n)
+            p_ptr = p_col = p_val = None
         else:
-            _check(_lib.amg_setup_dist(self.n, self._ptr.ctypes.data, col.ctypes.data,
-                                       val.ctypes.data, C.byref(self.prm), C.byref(dist),
+            self._ptr = np.ascontiguousarray(ptr, np.int64)
+            col = np.ascontiguousarray(col, np.int32)
+            val = np.ascontiguousarray(val, np.float64)
+            self.n = len(self._ptr) - 1
+            p_ptr, p_col, p_val = self._ptr.ctypes.data, col.ctypes.data, val.ctypes.data
+        if dist is None:
+            _check(_lib.amg_setup(self.n, p_ptr, p_col, p_val, C.byref(self.prm), C.byref(h)), "amg_setup")
+        else:
+            _check(_lib.amg_setup_dist(self.n, p_ptr, p_col, p_val, C.byref(self.prm), C.byref(dist),
                                        C.byref(h)), "amg_setup_dist")
         self._h = h
         vl = C.c_int64()
@@ -517,18 +526,27 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+def shm_selftest(tag: bytes, rank: int, nranks: int) -> None:
+    """amg_shm_selftest: the host shared-memory test transport (no GPU)."""
+    buf = (C.c_uint8 * 128)(*tag[:128].ljust(128, b"\0"))
+    _check(_lib.amg_shm_selftest(C.cast(buf, C.c_void_p), rank, nranks), "amg_shm_selftest")
+
+
 def nccl_selftest(device: int = 0) -> None:
     """amg_nccl_selftest: the NCCL calls of the multi-GPU executor on a 1-rank comm."""
     _check(_lib.amg_nccl_selftest(device), "amg_nccl_selftest")
 
 
 def setup_dist(ptr, col, val, nranks: int, rank: int = -1, gather_below: int = 0,
-               nccl_id: bytes | None = None, params: dict | None = None, **kw) -> Hierarchy:
+               nccl_id: bytes | None = None, params: dict | None = None, n: int | None = None,
+               **kw) -> Hierarchy:
     """amg_setup_dist: row-partitioned hierarchy (rank = -1: every rank in this
-    process on one GPU; rank >= 0: one NCCL rank per process)."""
+    process on one GPU; rank >= 0: one NCCL rank per process -- rank 0 builds the
+    hierarchy and sends every rank its part, so ranks > 0 may pass ptr = col =
+    val = None and the global row count n)."""
     d = AmgDist()
     d.nranks, d.rank, d.gather_below = nranks, rank, gather_below
     if nccl_id is not None:
         for i, b in enumerate(nccl_id[:128]):
             d.nccl_id[i] = b
-    return Hierarchy(ptr, col, val, params, dist=d, **kw)
+    return Hierarchy(ptr, col, val, params, dist=d, n=n, **kw)

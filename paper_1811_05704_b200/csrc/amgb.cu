@@ -28,6 +28,7 @@
 #include <functional>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/amgb.h"
@@ -40,6 +41,7 @@
 #include "kernels.cuh"
 #include "ops.cuh"
 #include "setup.hpp"
+#include "shm.hpp"
 
 namespace amgb {
 
@@ -116,6 +118,7 @@ thread_local std::string g_err;
 
 struct CudaError {
     std::string msg;
+    int code = AMG_E_CUDA;  // AMG_E_NCCL for a failed / timed-out collective
 };
 
 inline void ck(cudaError_t e, const char* what) {
@@ -129,7 +132,8 @@ inline void ckn(int r, const char* what) {
     if (r != 0) {
         Nccl& n = Nccl::get();
         throw CudaError{std::string(what) + ": NCCL error " + std::to_string(r) +
-                        (n.getErrorString ? std::string(" ") + n.getErrorString(r) : std::string())};
+                            (n.getErrorString && r > 0 ? std::string(" ") + n.getErrorString(r) : std::string()),
+                        AMG_E_NCCL};
     }
 }
 
@@ -439,8 +443,11 @@ struct Handle {
     bool virt = false;     // every part lives in this process (one GPU)
     int lg = 1;            // first replicated level
     void* nccl = nullptr;  // ncclComm_t (NCCL mode)
+    std::unique_ptr<ShmComm> shm;  // test transport (AMGB_TRANSPORT=shm): ranks sharing one GPU
     std::vector<std::vector<int64_t>> starts;  // level_starts
     std::vector<RankPart> host_parts;          // host copies (export / upload)
+    std::vector<LevelMeta> meta;               // every level's global sizes / smoother bounds (all ranks)
+    std::vector<double> coarse_inv;            // row-major A_L^-1 (replicated coarsest level)
     std::vector<Part> parts;
     double** d_defer_ptrs = nullptr;       // virtual all-reduce: device array of part->defer
     KState* ks_host = nullptr;             // pinned (part 0)
@@ -850,6 +857,62 @@ struct Handle {
         ck(cudaStreamWaitEvent(stream, ev_halo, 0), "wait halo");
         halo_pending = false;
     }
+    // Host synchronisation.  On an NCCL rank a peer that died or stalls would
+    // block cudaStreamSynchronize forever; instead poll the stream and the
+    // communicator's asynchronous error, and after nccl_timeout_s() without
+    // progress abort the communicator (in-flight NCCL kernels exit) and throw
+    // AMG_E_NCCL.  The handle is unusable afterwards.
+    bool nccl_dead = false;
+    double nccl_timeout = 300.0;
+    void nccl_fail(const std::string& why) {
+        Nccl& nc = Nccl::get();
+        if (nccl && nc.commAbort && !nccl_dead) nc.commAbort(nccl);
+        nccl_dead = true;
+        nccl = nullptr;
+        throw CudaError{"NCCL: " + why + " (communicator aborted; destroy the handle)", AMG_E_NCCL};
+    }
+    void sync(cudaStream_t s) {
+        if (nccl_dead) throw CudaError{"NCCL communicator was aborted earlier", AMG_E_NCCL};
+        if (!nccl) {
+            ck(cudaStreamSynchronize(s), "sync");
+            return;
+        }
+        Nccl& nc = Nccl::get();
+        const auto t0 = std::chrono::steady_clock::now();
+        for (int spin = 0;; ++spin) {
+            const cudaError_t q = cudaStreamQuery(s);
+            if (q == cudaSuccess) break;
+            if (q != cudaErrorNotReady) ck(q, "sync");
+            if (nc.commGetAsyncError) {
+                int ae = 0;
+                nc.commGetAsyncError(nccl, &ae);
+                if (ae != 0 && ae != kNcclInProgress)
+                    nccl_fail("asynchronous error " + std::to_string(ae) +
+                              (nc.getErrorString ? std::string(" ") + nc.getErrorString(ae) : std::string()));
+            }
+            if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > nccl_timeout)
+                nccl_fail("no progress for " + std::to_string((int)nccl_timeout) + " s (a peer rank died or stalled)");
+            if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+        }
+    }
+    // test transport: personalised all-to-all of host bytes (errors -> AMG_E_NCCL)
+    void shm_a2a(const std::vector<std::vector<uint8_t>>& out, std::vector<std::vector<uint8_t>>& in) {
+        try {
+            shm->alltoallv(out, in);
+        } catch (const std::exception& e) {
+            throw CudaError{e.what(), AMG_E_NCCL};
+        }
+    }
+    template <class T>
+    static std::vector<uint8_t> bytes_of(const T* p, int64_t n) {
+        const auto* b = reinterpret_cast<const uint8_t*>(p);
+        return std::vector<uint8_t>(b, b + n * sizeof(T));
+    }
+    std::vector<uint8_t> d2h_bytes(const double* d, int64_t n) {
+        std::vector<uint8_t> v(n * sizeof(double));
+        if (n) ck(cudaMemcpy(v.data(), d, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H (shm)");
+        return v;
+    }
     template <class Op>
     void vec(Part& p, int64_t n, const Op& op, const int32_t* gate, const char* what) {
         if (n == 0) {
@@ -902,6 +965,22 @@ struct Handle {
                        "halo copy");
                 }
             }
+        } else if (shm) {  // test transport: synchronous, through host shared memory
+            Part& p = parts[0];
+            DevLevel& L = p.lv[l];
+            double* dst = sel(p) + L.n;
+            sync(stream);
+            std::vector<std::vector<uint8_t>> out(nranks), in;
+            for (size_t j = 0; j < L.plan.send_peer.size(); ++j)
+                out[L.plan.send_peer[j]] = d2h_bytes(L.sendbuf + L.plan.send_off[j], L.plan.send_cnt[j]);
+            shm_a2a(out, in);
+            for (size_t k = 0; k < L.plan.recv_peer.size(); ++k) {
+                const auto& b = in[L.plan.recv_peer[k]];
+                if ((int64_t)b.size() != L.plan.recv_cnt[k] * 8) throw CudaError{"shm halo: size mismatch", AMG_E_NCCL};
+                if (!b.empty())
+                    ck(cudaMemcpy(dst + L.plan.recv_off[k], b.data(), b.size(), cudaMemcpyHostToDevice), "H2D (shm)");
+            }
+            return;  // nothing pending
         } else {
             Nccl& nc = Nccl::get();
             Part& p = parts[0];
@@ -930,6 +1009,15 @@ struct Handle {
         if (virt) {
             launch(AMG_PROF_VECTOR, 0, "allreduce (virtual)",
                    [&] { sum_parts_kernel<<<1, 32, 0, stream>>>(d_defer_ptrs, (int)parts.size(), nv); });
+        } else if (shm) {  // test transport: every rank sums the totals in rank order
+            Part& p = parts[0];
+            sync(stream);
+            std::vector<std::vector<uint8_t>> out(nranks, d2h_bytes(p.red.defer, nv)), in;
+            shm_a2a(out, in);
+            std::vector<double> tot(nv, 0.0);
+            for (int r = 0; r < nranks; ++r)
+                for (int k = 0; k < nv; ++k) tot[k] += reinterpret_cast<const double*>(in[r].data())[k];
+            ck(cudaMemcpy(p.red.defer, tot.data(), nv * sizeof(double), cudaMemcpyHostToDevice), "H2D (shm)");
         } else {
             Part& p = parts[0];
             ckn(Nccl::get().allReduce(p.red.defer, p.red.defer, nv, kNcclDouble, kNcclSum, nccl, stream),
@@ -958,6 +1046,15 @@ struct Handle {
                                            stream),
                            "allgather copy");
                 }
+        } else if (shm) {  // test transport: every rank sends its slice to every rank
+            double* buf = sel(parts[0]);
+            const int me = parts[0].rank;
+            sync(stream);
+            std::vector<std::vector<uint8_t>> out(nranks, d2h_bytes(buf + st[me], st[me + 1] - st[me])), in;
+            shm_a2a(out, in);
+            for (int q = 0; q < nranks; ++q)
+                if (q != me && !in[q].empty())
+                    ck(cudaMemcpy(buf + st[q], in[q].data(), in[q].size(), cudaMemcpyHostToDevice), "H2D (shm)");
         } else {
             Nccl& nc = Nccl::get();
             double* buf = sel(parts[0]);
@@ -1337,12 +1434,12 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
         }
     }
     ck(cudaMemcpyAsync(ks_host, parts[0].ks, sizeof(KState), cudaMemcpyDeviceToHost, stream), "ks read");
-    ck(cudaStreamSynchronize(stream), "sync");
+    sync(stream);
     collect(rec_direct, 0, true);
     if (ks_host->nf == 0.0) {  // zero right-hand side: x = 0
         for (Part& p : parts)
             ck(cudaMemsetAsync(x + (virt ? p.row0 : 0), 0, p.lv[0].n * sizeof(double), stream), "memset");
-        ck(cudaStreamSynchronize(stream), "sync");
+        sync(stream);
         *iters = 0;
         *rel = 0.0;
         stats = amg_solve_stats{};
@@ -1353,7 +1450,7 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
 
     // Krylov loop: two iterations per host round trip, replayed from a CUDA
     // graph; kernels of iterations past convergence exit at their gate.
-    const bool use_graph = prm.use_graph && !sync_debug;
+    const bool use_graph = prm.use_graph && !sync_debug && !shm;  // shm transport: host-synchronous
     auto two_iterations = [&] {
         for (int k = 0; k < 2; ++k) {
             cur_iter = k;
@@ -1416,7 +1513,7 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
         const int iter_before = ks_host->iter;
         ck(cudaGraphLaunch(graph, stream), "graph launch");
         ck(cudaMemcpyAsync(ks_host, parts[0].ks, sizeof(KState), cudaMemcpyDeviceToHost, stream), "ks read");
-        ck(cudaStreamSynchronize(stream), "sync");
+        sync(stream);
         // the body ran ceil(iters / 2) times; iteration 0 of a body ran that
         // often, iteration 1 one time less when the count is odd
         const int ran = ks_host->iter - iter_before + (ks_host->status ? 1 : 0);
@@ -1458,7 +1555,7 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
             two_iterations();
         }
         ck(cudaMemcpyAsync(ks_host, parts[0].ks, sizeof(KState), cudaMemcpyDeviceToHost, stream), "ks read");
-        ck(cudaStreamSynchronize(stream), "sync");
+        sync(stream);
         const int ran = ks_host->iter - iter_before + (ks_host->done && ks_host->status ? 1 : 0);
         collect(use_graph ? rec_graph : rec_direct, ran, !use_graph);
     }
@@ -1481,7 +1578,7 @@ amg_status Handle::solve(const double* f, double* x, double tol, int32_t maxiter
                "x out");
     ck(cudaEventRecord(ev1, stream), "event");
     ck(cudaMemcpyAsync(ks_host, parts[0].ks, sizeof(KState), cudaMemcpyDeviceToHost, stream), "ks read");
-    ck(cudaStreamSynchronize(stream), "sync");
+    sync(stream);
     collect(rec_direct, 0, true);
     *iters = ks_host->iter;
     *rel = ks_host->true_res / ks_host->nf;
@@ -1691,7 +1788,7 @@ amg_status Handle::solve_batched(int k, const double* F, int64_t ldf, double* X,
     ck(cudaMemsetAsync(batch.pa, 0, n * K * sizeof(double), stream), "memset");
     ck(cudaMemsetAsync(batch.pb, 0, n * K * sizeof(double), stream), "memset");
     ck(cudaMemcpyAsync(kh, batch.ks, sizeof(KStateB), cudaMemcpyDeviceToHost, stream), "ks read");
-    ck(cudaStreamSynchronize(stream), "sync");
+    sync(stream);
     collect(rec_direct, 0, true);
     // FinInitResB does not know which columns have f = 0: mark them done
     // (x = 0 for them) before iterating
@@ -1711,7 +1808,7 @@ amg_status Handle::solve_batched(int k, const double* F, int64_t ldf, double* X,
         while (!kh->done) {
             for (int it = 0; it < 2; ++it) cg_iteration_b<K>(it);
             ck(cudaMemcpyAsync(kh, batch.ks, sizeof(KStateB), cudaMemcpyDeviceToHost, stream), "ks read");
-            ck(cudaStreamSynchronize(stream), "sync");
+            sync(stream);
         }
     } else if (!kh->done) {
         if (!batch.graph) {  // conditional WHILE node around two iterations (device-side loop)
@@ -1771,7 +1868,7 @@ amg_status Handle::solve_batched(int k, const double* F, int64_t ldf, double* X,
            [&] { unpack_cols<K><<<grid_for(n), kBlock, 0, stream>>>(batch.xw, k, n, X, ldx, batch.ks); });
     ck(cudaEventRecord(ev1, stream), "event");
     ck(cudaMemcpyAsync(kh, batch.ks, sizeof(KStateB), cudaMemcpyDeviceToHost, stream), "ks read");
-    ck(cudaStreamSynchronize(stream), "sync");
+    sync(stream);
     int itmax = 0;
     for (int j = 0; j < K; ++j) itmax = std::max(itmax, kh->iter[j]);
     const int bodies = (itmax + 1) / 2;
@@ -1909,11 +2006,11 @@ amg_status Handle::solve_gmres(const double* f, double* x, double tol, int32_t m
     rows(p, p.lv[0].A, OpResidual<1, FinGmresRestart>{x, f, gm.r, FinGmresRestart{gm.ks}}, nullptr, "gmres r0");
     vec(p, n, VGmresScale{gm.r, gm.V, &gm.ks->hn, {}}, &gm.ks->done, "gmres v0");
     ck(cudaMemcpyAsync(kh, gm.ks, sizeof(KStateG), cudaMemcpyDeviceToHost, stream), "ks read");
-    ck(cudaStreamSynchronize(stream), "sync");
+    sync(stream);
     collect(rec_direct, 0, true);
     if (kh->nf == 0.0) {  // zero right-hand side: x = 0
         ck(cudaMemsetAsync(x, 0, n * sizeof(double), stream), "memset");
-        ck(cudaStreamSynchronize(stream), "sync");
+        sync(stream);
         *iters = 0;
         *rel = 0.0;
         stats = amg_solve_stats{};
@@ -1967,13 +2064,13 @@ amg_status Handle::solve_gmres(const double* f, double* x, double tol, int32_t m
             ck(cudaGraphLaunch(gm.graph, stream), "graph launch");
             launches += gm.graph_kernels;
             ck(cudaMemcpyAsync(kh, gm.ks, sizeof(KStateG), cudaMemcpyDeviceToHost, stream), "ks read");
-            ck(cudaStreamSynchronize(stream), "sync");
+            sync(stream);
             collect(gm.rec, kh->k - k_before, false);  // steps that ran + the cycle end
         } else {
             for (int j = 0; j < m; ++j) gmres_step(j);
             gmres_cycle_end(f, x);
             ck(cudaMemcpyAsync(kh, gm.ks, sizeof(KStateG), cudaMemcpyDeviceToHost, stream), "ks read");
-            ck(cudaStreamSynchronize(stream), "sync");
+            sync(stream);
             collect(rec_direct, 0, true);
         }
         ++cycles;
@@ -1981,7 +2078,7 @@ amg_status Handle::solve_gmres(const double* f, double* x, double tol, int32_t m
     rows(p, p.lv[0].A, OpResidual<1, FinTrueResG>{x, f, gm.r, FinTrueResG{gm.ks}}, nullptr, "true res");
     ck(cudaEventRecord(ev1, stream), "event");
     ck(cudaMemcpyAsync(kh, gm.ks, sizeof(KStateG), cudaMemcpyDeviceToHost, stream), "ks read");
-    ck(cudaStreamSynchronize(stream), "sync");
+    sync(stream);
     collect(rec_direct, 0, true);
     *iters = kh->k;
     *rel = kh->beta / kh->nf;
@@ -2130,11 +2227,11 @@ amg_status Handle::solve_idrs_t(const double* f, double* x, double tol, int32_t 
                                                                    p.red);
     });
     ck(cudaMemcpyAsync(kh, idr.ks, sizeof(KStateI), cudaMemcpyDeviceToHost, stream), "ks read");
-    ck(cudaStreamSynchronize(stream), "sync");
+    sync(stream);
     collect(rec_direct, 0, true);
     if (kh->nf == 0.0) {  // zero right-hand side: x = 0
         ck(cudaMemsetAsync(x, 0, n * sizeof(double), stream), "memset");
-        ck(cudaStreamSynchronize(stream), "sync");
+        sync(stream);
         *iters = 0;
         *rel = 0.0;
         stats = amg_solve_stats{};
@@ -2182,19 +2279,19 @@ amg_status Handle::solve_idrs_t(const double* f, double* x, double tol, int32_t 
             ck(cudaGraphLaunch(idr.graph, stream), "graph launch");
             launches += idr.graph_kernels;
             ck(cudaMemcpyAsync(kh, idr.ks, sizeof(KStateI), cudaMemcpyDeviceToHost, stream), "ks read");
-            ck(cudaStreamSynchronize(stream), "sync");
+            sync(stream);
             collect(idr.rec, kh->it - it_before, false);  // the steps that ran
         } else {
             idr_cycle<S>(x);
             ck(cudaMemcpyAsync(kh, idr.ks, sizeof(KStateI), cudaMemcpyDeviceToHost, stream), "ks read");
-            ck(cudaStreamSynchronize(stream), "sync");
+            sync(stream);
             collect(rec_direct, 0, true);
         }
     }
     rows(p, p.lv[0].A, OpResidual<1, FinTrueResI>{x, f, idr.r, FinTrueResI{idr.ks}}, nullptr, "true res");
     ck(cudaEventRecord(ev1, stream), "event");
     ck(cudaMemcpyAsync(kh, idr.ks, sizeof(KStateI), cudaMemcpyDeviceToHost, stream), "ks read");
-    ck(cudaStreamSynchronize(stream), "sync");
+    sync(stream);
     collect(rec_direct, 0, true);
     *iters = kh->it;
     *rel = kh->res / kh->nf;
@@ -2232,7 +2329,7 @@ amg_status Handle::solve_api(const double* f, double* x, double tol, int32_t max
     perm_in(x, rx);
     const amg_status st = solve_dispatch(rf, rx, tol, maxiter, iters, rel);
     perm_out(rx, x);
-    ck(cudaStreamSynchronize(stream), "sync");
+    sync(stream);
     stats.flags |= 2;  // bit 1: reordered store
     return st;
 }
@@ -2783,7 +2880,7 @@ void upload_part(Handle& H, const RankPart& RP, Part& P) {
     P.lv.resize(nlev);
     for (int l = 0; l < nlev; ++l) {
         const LevelPart& lp = RP.lv[l];
-        const HostLevel& hl = H.host.levels[l];
+        const LevelMeta& hl = H.meta[l];
         DevLevel& L = P.lv[l];
         const bool coarsest = l == nlev - 1;
         L.replicated = lp.replicated;
@@ -2859,7 +2956,7 @@ void upload_part(Handle& H, const RankPart& RP, Part& P) {
         }
     }
     P.nL = RP.lv.back().ma().nrows;
-    P.coarse_inv = H.upload(H.reordered ? H.coarse_inv_perm : H.host.coarse_inv);
+    P.coarse_inv = H.upload(H.reordered ? H.coarse_inv_perm : H.coarse_inv);
     P.lv.back().dev_bytes += 8 * P.nL * P.nL;
     const int64_t nv0 = P.lv[0].n + P.lv[0].ng;
     void* pp = nullptr;
@@ -2975,16 +3072,280 @@ static amg_status check_params(const amg_params& p) {
     return AMG_OK;
 }
 
+// Host hierarchy of the global matrix (Algorithm 1): CSR copy,
+// then the GPU or host builder.  Throws SetupError / std exceptions.
+static void build_host(amgb::Handle& H, int64_t n, const int64_t* ptr, const int32_t* col, const double* val) {
+    using namespace amgb;
+    const amg_params& prm = H.prm;
+    validate_csr(n, ptr, col);
+    Csr A0;
+    A0.nrows = A0.ncols = n;
+    A0.ptr.resize(n + 1);  // uninitialised: first touch in the parallel copy
+    A0.col.resize(ptr[n]);
+    A0.val.resize(ptr[n]);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        A0.ptr[i + 1] = ptr[i + 1];
+        for (int64_t k = ptr[i]; k < ptr[i + 1]; ++k) {
+            A0.col[k] = col[k];
+            A0.val[k] = val[k];
+        }
+    }
+    A0.ptr[0] = ptr[0];
+    SetupParams sp;
+    sp.smoothed = prm.coarsening == 0;
+    sp.eps_strong = prm.eps_strong;
+    sp.eps_decay = prm.eps_decay;
+    sp.p_omega = prm.p_omega;
+    sp.relax = prm.relax;
+    sp.jacobi_omega = prm.jacobi_omega;
+    sp.cheb_degree = prm.cheb_degree;
+    sp.cheb_lower = prm.cheb_lower;
+    sp.cheb_scaled = prm.cheb_scaled != 0;
+    sp.coarse_enough = prm.coarse_enough;
+    sp.max_levels = prm.max_levels;
+    sp.dense_max = prm.dense_max;
+    H.host = prm.setup_device == 1 && prm.device >= 0 ? build_hierarchy_gpu(std::move(A0), sp, prm.device)
+                                                      : build_hierarchy(std::move(A0), sp);
+    H.meta = level_meta(H.host);
+    H.coarse_inv = H.host.coarse_inv;
+}
+
+// CUDA context, streams and events of a device handle.
+static void device_init(amgb::Handle& H) {
+    using namespace amgb;
+    const auto tc = std::chrono::steady_clock::now();
+    ck(cudaSetDevice(H.prm.device), "cudaSetDevice");
+    ck(cudaFree(nullptr), "context");
+    if (std::getenv("AMGB_SETUP_TIMING"))
+        std::fprintf(stderr, "[setup] CUDA context %.1f ms\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tc).count());
+    H.device = H.prm.device;
+    ck(cudaDeviceGetAttribute(&H.num_sms, cudaDevAttrMultiProcessorCount, H.prm.device), "attr");
+    ck(cudaEventCreate(&H.ev0), "event");
+    ck(cudaEventCreate(&H.ev1), "event");
+    ck(cudaStreamCreate(&H.own_stream), "stream");  // capture needs a non-legacy stream
+    H.stream = H.own_stream;
+    if (H.nranks > 1) {  // halo transfers overlap interior rows
+        ck(cudaStreamCreateWithFlags(&H.comm_stream, cudaStreamNonBlocking), "comm stream");
+        ck(cudaEventCreateWithFlags(&H.ev_pack, cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&H.ev_halo, cudaEventDisableTiming), "event");
+    }
+}
+
+// Upload the host parts (device store, work vectors, Krylov state).
+static void device_upload(amgb::Handle& H) {
+    using namespace amgb;
+    H.parts.resize(H.host_parts.size());
+    const auto tu = std::chrono::steady_clock::now();
+    for (size_t i = 0; i < H.parts.size(); ++i) upload_part(H, H.host_parts[i], H.parts[i]);
+    if (std::getenv("AMGB_SETUP_TIMING"))
+        std::fprintf(stderr, "[setup] device store %.1f ms (H2D %.2f GB in %.1f ms)\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tu).count(),
+                     H.upload_bytes / 1e9, H.upload_ms);
+    if (H.virt) {
+        std::vector<double*> ptrs;
+        for (auto& p : H.parts) ptrs.push_back(p.red.defer);
+        H.d_defer_ptrs = H.upload(ptrs);
+    }
+    ck(cudaMallocHost(&H.ks_host, sizeof(KState)), "cudaMallocHost");
+    ck(cudaDeviceSynchronize(), "setup sync");
+    if (H.reordered) {
+        const int64_t n0 = H.parts[0].lv[0].n;
+        for (const auto& q : H.reorder_q) H.dq.push_back(H.upload(q));
+        H.dq0 = H.dq[0];
+        H.rf = H.dalloc(n0);
+        H.rx = H.dalloc(n0);
+    }
+    H.on_device = true;
+}
+
+static amg_status setup_error_status(const std::exception_ptr& ep) {
+    using namespace amgb;
+    try {
+        std::rethrow_exception(ep);
+    } catch (const SetupError& e) {
+        return set_error((amg_status)e.code, e.msg);
+    } catch (const std::bad_alloc&) {
+        return set_error(AMG_E_OOM, "host allocation failed during setup");
+    } catch (const CudaError& e) {
+        return set_error(e.msg.find("out of memory") != std::string::npos ? AMG_E_OOM : (amg_status)e.code, e.msg);
+    } catch (const std::exception& e) {
+        return set_error(AMG_E_INVALID_ARG, e.what());
+    }
+    return set_error(AMG_E_INVALID_ARG, "setup failed");
+}
+
+// Scattered setup of one NCCL rank: the communicator first
+// (with a timeout), then rank 0 alone builds the global hierarchy and the
+// partition, and sends every other rank the byte image of its part (pack_part)
+// over NCCL; the other ranks never see the global matrix (their ptr / col / val
+// may be NULL).  A setup error on rank 0 is broadcast, so every rank returns it.
+static amg_status setup_scatter(std::unique_ptr<amgb::Handle> H, int64_t n, const int64_t* ptr, const int32_t* col,
+                                const double* val, int rank, int64_t gather_below, const uint8_t* nccl_id,
+                                amg_handle* out) {
+    using namespace amgb;
+    const int nranks = H->nranks;
+    Nccl& nc = Nccl::get();
+    const char* tr = std::getenv("AMGB_TRANSPORT");
+    const bool use_shm = tr && std::string(tr) == "shm";  // test transport (shm.hpp)
+    if (!use_shm && !nc.ok) return set_error(AMG_E_NCCL, "NCCL unavailable: " + nc.error);
+    H->nccl_timeout = nccl_timeout_s();
+    try {
+        device_init(*H);
+        if (use_shm) {
+            try {
+                H->shm = std::make_unique<ShmComm>(nccl_id, rank, nranks, H->nccl_timeout);
+            } catch (const std::exception& e) {
+                return set_error(AMG_E_NCCL, std::string("shm transport: ") + e.what());
+            }
+        } else {
+            const int rc = nccl_comm_init_timeout(&H->nccl, nranks, nccl_id, rank, H->prm.device, H->nccl_timeout);
+            if (rc == -2) {
+                H->nccl = nullptr;
+                return set_error(AMG_E_NCCL, "ncclCommInitRank: the other ranks did not join within " +
+                                                 std::to_string((int)H->nccl_timeout) + " s (AMGB_NCCL_TIMEOUT_S)");
+            }
+            ckn(rc, "ncclCommInitRank");
+        }
+    } catch (...) {
+        return setup_error_status(std::current_exception());
+    }
+    // status block broadcast by rank 0: [status, bytes for rank 0..nranks-1], message
+    constexpr int kMsg = 512;
+    const size_t hdr_bytes = (size_t)(1 + nranks) * sizeof(int64_t) + kMsg;
+    std::vector<uint8_t> hdr(hdr_bytes, 0);
+    auto hdr_i64 = [&](int k) -> int64_t& { return reinterpret_cast<int64_t*>(hdr.data())[k]; };
+    std::vector<std::vector<uint8_t>> blobs;
+    PartHeader ph;
+    RankPart own;
+    if (rank == 0) {
+        amg_status st = AMG_OK;
+        try {
+            if (n <= 0 || n > INT32_MAX || !ptr || (ptr[n] > 0 && (!col || !val)))
+                throw SetupError{AMG_E_INVALID_ARG, "rank 0 needs the global matrix (n, ptr, col, val)"};
+            const auto t0 = std::chrono::steady_clock::now();
+            build_host(*H, n, ptr, col, val);
+            H->lg = first_replicated_level(H->host, nranks, gather_below);
+            H->starts = level_starts(H->host, nranks, H->lg);
+            ph.meta = H->meta;
+            ph.lg = H->lg;
+            ph.starts = H->starts;
+            ph.coarse_inv = H->coarse_inv;
+            blobs.resize(nranks);
+            for (int r = 1; r < nranks; ++r) {
+                RankPart rp = build_rank_part(H->host, nranks, r, H->lg, H->starts);
+                pack_part(ph, rp, blobs[r]);
+            }
+            own = build_rank_part(H->host, nranks, 0, H->lg, H->starts);
+            if (std::getenv("AMGB_SETUP_TIMING"))
+                std::fprintf(stderr, "[setup] rank 0: hierarchy + %d parts %.1f ms\n", nranks,
+                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+        } catch (...) {
+            st = setup_error_status(std::current_exception());
+        }
+        hdr_i64(0) = st;
+        for (int r = 1; r < nranks && st == AMG_OK; ++r) hdr_i64(1 + r) = (int64_t)blobs[r].size();
+        if (st != AMG_OK) std::snprintf(reinterpret_cast<char*>(hdr.data() + (1 + nranks) * 8), kMsg, "%s",
+                                        g_err.c_str());
+    }
+    uint8_t* dbuf = nullptr;
+    amg_status st = AMG_OK;
+    if (H->shm) {  // test transport: the same protocol through host shared memory
+        try {
+            std::vector<std::vector<uint8_t>> out(nranks), in;
+            if (rank == 0)
+                for (int r = 0; r < nranks; ++r) out[r] = hdr;
+            H->shm_a2a(out, in);
+            hdr = in[0];
+            if (hdr_i64(0) != AMG_OK) {
+                const std::string msg(reinterpret_cast<const char*>(hdr.data() + (1 + nranks) * 8));
+                return set_error((amg_status)hdr_i64(0), rank == 0 ? g_err : "rank 0 setup failed: " + msg);
+            }
+            out.assign(nranks, {});
+            if (rank == 0)
+                for (int r = 1; r < nranks; ++r) out[r] = std::move(blobs[r]);
+            H->shm_a2a(out, in);
+            if (rank == 0) {
+                H->host_parts.push_back(std::move(own));
+            } else {
+                RankPart rp;
+                unpack_part(in[0].data(), in[0].size(), ph, rp);
+                if (rp.rank != rank || rp.nranks != nranks) throw SetupError{AMG_E_INVALID_ARG, "scattered setup: wrong part"};
+                H->meta = ph.meta;
+                H->lg = ph.lg;
+                H->starts = ph.starts;
+                H->coarse_inv = ph.coarse_inv;
+                H->host_parts.push_back(std::move(rp));
+            }
+            device_upload(*H);
+        } catch (...) {
+            return setup_error_status(std::current_exception());
+        }
+        *out = new amg_hierarchy{std::move(H)};
+        return AMG_OK;
+    }
+    try {
+        ck(cudaMalloc(&dbuf, hdr_bytes), "cudaMalloc (scatter)");
+        ck(cudaMemcpy(dbuf, hdr.data(), hdr_bytes, cudaMemcpyHostToDevice), "H2D");
+        ckn(nc.broadcast(dbuf, dbuf, hdr_bytes, kNcclUint8, 0, H->nccl, H->stream), "ncclBroadcast (setup status)");
+        H->sync(H->stream);
+        ck(cudaMemcpy(hdr.data(), dbuf, hdr_bytes, cudaMemcpyDeviceToHost), "D2H");
+        cudaFree(dbuf);
+        dbuf = nullptr;
+        if (hdr_i64(0) != AMG_OK) {
+            const std::string msg(reinterpret_cast<const char*>(hdr.data() + (1 + nranks) * 8));
+            return set_error((amg_status)hdr_i64(0), rank == 0 ? g_err : "rank 0 setup failed: " + msg);
+        }
+        // rank 0 -> rank r: the part image (one p2p transfer per rank)
+        if (rank == 0) {
+            size_t mx = 0;
+            for (int r = 1; r < nranks; ++r) mx = std::max(mx, blobs[r].size());
+            ck(cudaMalloc(&dbuf, std::max<size_t>(mx, 1)), "cudaMalloc (scatter)");
+            for (int r = 1; r < nranks; ++r) {
+                ck(cudaMemcpy(dbuf, blobs[r].data(), blobs[r].size(), cudaMemcpyHostToDevice), "H2D part");
+                ckn(nc.send(dbuf, blobs[r].size(), kNcclUint8, r, H->nccl, H->stream), "ncclSend (part)");
+                H->sync(H->stream);
+                std::vector<uint8_t>().swap(blobs[r]);
+            }
+            H->host_parts.push_back(std::move(own));
+        } else {
+            const size_t bytes = (size_t)hdr_i64(1 + rank);
+            std::vector<uint8_t> img(bytes);
+            ck(cudaMalloc(&dbuf, std::max<size_t>(bytes, 1)), "cudaMalloc (scatter)");
+            ckn(nc.recv(dbuf, bytes, kNcclUint8, 0, H->nccl, H->stream), "ncclRecv (part)");
+            H->sync(H->stream);
+            ck(cudaMemcpy(img.data(), dbuf, bytes, cudaMemcpyDeviceToHost), "D2H part");
+            RankPart rp;
+            unpack_part(img.data(), img.size(), ph, rp);
+            if (rp.rank != rank || rp.nranks != nranks) throw SetupError{AMG_E_INVALID_ARG, "scattered setup: wrong part"};
+            H->meta = ph.meta;
+            H->lg = ph.lg;
+            H->starts = ph.starts;
+            H->coarse_inv = ph.coarse_inv;
+            H->host_parts.push_back(std::move(rp));
+        }
+        if (dbuf) cudaFree(dbuf);
+        dbuf = nullptr;
+        device_upload(*H);
+    } catch (...) {
+        if (dbuf) cudaFree(dbuf);
+        st = setup_error_status(std::current_exception());
+    }
+    if (st != AMG_OK) return st;
+    *out = new amg_hierarchy{std::move(H)};
+    return AMG_OK;
+}
+
 // Common setup: host hierarchy, partition, upload.  rank = -1: every part in
-// this process (virtual); nranks = 1: single GPU.
+// this process (virtual); nranks = 1: single GPU; rank >= 0 on a device: the
+// scattered setup above.
 static amg_status setup_impl(int64_t n, const int64_t* ptr, const int32_t* col, const double* val,
                              const amg_params* prm_in, int nranks, int rank, int64_t gather_below,
                              const uint8_t* nccl_id, amg_handle* out) {
     using namespace amgb;
     if (!out) return set_error(AMG_E_INVALID_ARG, "out is NULL");
     *out = nullptr;
-    if (n <= 0 || n > INT32_MAX || !ptr || (!col && ptr[n] > 0) || (!val && ptr[n] > 0))
-        return set_error(AMG_E_INVALID_ARG, "n must be in [1, 2^31) and ptr/col/val non-NULL");
     if (nranks < 1 || rank < -1 || rank >= nranks) return set_error(AMG_E_INVALID_ARG, "nranks / rank");
     amg_params prm;
     if (prm_in)
@@ -2997,38 +3358,13 @@ static amg_status setup_impl(int64_t n, const int64_t* ptr, const int32_t* col, 
     H->sync_debug = std::getenv("AMGB_SYNC_DEBUG") != nullptr;
     H->nranks = nranks;
     H->virt = nranks > 1 && rank < 0;
+    if (nranks > 1 && rank >= 0 && prm.device >= 0)
+        return setup_scatter(std::move(H), n, ptr, col, val, rank, gather_below, nccl_id, out);
+    if (n <= 0 || n > INT32_MAX || !ptr || (!col && ptr[n] > 0) || (!val && ptr[n] > 0))
+        return set_error(AMG_E_INVALID_ARG, "n must be in [1, 2^31) and ptr/col/val non-NULL");
     try {
-        validate_csr(n, ptr, col);
-        Csr A0;
-        A0.nrows = A0.ncols = n;
-        A0.ptr.resize(n + 1);  // uninitialised: first touch in the parallel copy
-        A0.col.resize(ptr[n]);
-        A0.val.resize(ptr[n]);
-#pragma omp parallel for schedule(static)
-        for (int64_t i = 0; i < n; ++i) {
-            A0.ptr[i + 1] = ptr[i + 1];
-            for (int64_t k = ptr[i]; k < ptr[i + 1]; ++k) {
-                A0.col[k] = col[k];
-                A0.val[k] = val[k];
-            }
-        }
-        A0.ptr[0] = ptr[0];
-        SetupParams sp;
-        sp.smoothed = prm.coarsening == 0;
-        sp.eps_strong = prm.eps_strong;
-        sp.eps_decay = prm.eps_decay;
-        sp.p_omega = prm.p_omega;
-        sp.relax = prm.relax;
-        sp.jacobi_omega = prm.jacobi_omega;
-        sp.cheb_degree = prm.cheb_degree;
-        sp.cheb_lower = prm.cheb_lower;
-        sp.cheb_scaled = prm.cheb_scaled != 0;
-        sp.coarse_enough = prm.coarse_enough;
-        sp.max_levels = prm.max_levels;
-        sp.dense_max = prm.dense_max;
         const auto t0 = std::chrono::steady_clock::now();
-        H->host = prm.setup_device == 1 && prm.device >= 0 ? build_hierarchy_gpu(std::move(A0), sp, prm.device)
-                                        : build_hierarchy(std::move(A0), sp);
+        build_host(*H, n, ptr, col, val);
         const auto t1 = std::chrono::steady_clock::now();
         H->lg = first_replicated_level(H->host, nranks, gather_below);
         H->starts = level_starts(H->host, nranks, H->lg);
@@ -3047,72 +3383,26 @@ static amg_status setup_impl(int64_t n, const int64_t* ptr, const int32_t* col, 
         } else if (rank < 0) {
             for (int r = 0; r < nranks; ++r)
                 H->host_parts.push_back(build_rank_part(H->host, nranks, r, H->lg, H->starts));
-        } else {
+        } else {  // host-only handle of one rank (device = -1): global setup, own part
             H->host_parts.push_back(build_rank_part(H->host, nranks, rank, H->lg, H->starts));
         }
         if (std::getenv("AMGB_SETUP_TIMING"))
             std::fprintf(stderr, "[setup] hierarchy %.1f ms, partition %.1f ms\n",
                          std::chrono::duration<double, std::milli>(t1 - t0).count(),
                          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count());
-    } catch (const SetupError& e) {
-        return set_error((amg_status)e.code, e.msg);
-    } catch (const std::bad_alloc&) {
-        return set_error(AMG_E_OOM, "host allocation failed during setup");
-    } catch (const std::exception& e) {
-        return set_error(AMG_E_INVALID_ARG, e.what());
+    } catch (...) {
+        return setup_error_status(std::current_exception());
     }
     if (prm.device < 0) {
         *out = new amg_hierarchy{std::move(H)};
         return AMG_OK;
     }
     try {
-        const auto tc = std::chrono::steady_clock::now();
-        ck(cudaSetDevice(prm.device), "cudaSetDevice");
-        ck(cudaFree(nullptr), "context");
-        if (std::getenv("AMGB_SETUP_TIMING"))
-            std::fprintf(stderr, "[setup] CUDA context %.1f ms\n",
-                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tc).count());
-        H->device = prm.device;
-        ck(cudaDeviceGetAttribute(&H->num_sms, cudaDevAttrMultiProcessorCount, prm.device), "attr");
-        ck(cudaEventCreate(&H->ev0), "event");
-        ck(cudaEventCreate(&H->ev1), "event");
-        ck(cudaStreamCreate(&H->own_stream), "stream");  // capture needs a non-legacy stream
-        H->stream = H->own_stream;
-        if (nranks > 1) {  // halo transfers overlap interior rows
-            ck(cudaStreamCreateWithFlags(&H->comm_stream, cudaStreamNonBlocking), "comm stream");
-            ck(cudaEventCreateWithFlags(&H->ev_pack, cudaEventDisableTiming), "event");
-            ck(cudaEventCreateWithFlags(&H->ev_halo, cudaEventDisableTiming), "event");
-        }
-        if (nranks > 1 && rank >= 0) {
-            Nccl& nc = Nccl::get();
-            if (!nc.ok) return set_error(AMG_E_CUDA, "NCCL unavailable: " + nc.error);
-            ckn(nccl_comm_init(&H->nccl, nranks, nccl_id, rank), "ncclCommInitRank");
-        }
-        H->parts.resize(H->host_parts.size());
-        const auto tu = std::chrono::steady_clock::now();
-        for (size_t i = 0; i < H->parts.size(); ++i) upload_part(*H, H->host_parts[i], H->parts[i]);
-        if (std::getenv("AMGB_SETUP_TIMING"))
-            std::fprintf(stderr, "[setup] device store %.1f ms (H2D %.2f GB in %.1f ms)\n",
-                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tu).count(),
-                         H->upload_bytes / 1e9, H->upload_ms);
-        if (H->virt) {
-            std::vector<double*> ptrs;
-            for (auto& p : H->parts) ptrs.push_back(p.red.defer);
-            H->d_defer_ptrs = H->upload(ptrs);
-        }
-        ck(cudaMallocHost(&H->ks_host, sizeof(KState)), "cudaMallocHost");
-        ck(cudaDeviceSynchronize(), "setup sync");
-        if (H->reordered) {
-            const int64_t n0 = H->parts[0].lv[0].n;
-            for (const auto& q : H->reorder_q) H->dq.push_back(H->upload(q));
-            H->dq0 = H->dq[0];
-            H->rf = H->dalloc(n0);
-            H->rx = H->dalloc(n0);
-        }
-        H->on_device = true;
-    } catch (const amgb::CudaError& e) {
+        device_init(*H);
+        device_upload(*H);
+    } catch (...) {
         cudaGetLastError();
-        return set_error(e.msg.find("out of memory") != std::string::npos ? AMG_E_OOM : AMG_E_CUDA, e.msg);
+        return setup_error_status(std::current_exception());
     }
     *out = new amg_hierarchy{std::move(H)};
     return AMG_OK;
@@ -3126,9 +3416,9 @@ amg_status amg_setup(int64_t n, const int64_t* ptr, const int32_t* col, const do
 amg_status amg_nccl_unique_id(uint8_t id[128]) {
     if (!id) return set_error(AMG_E_INVALID_ARG, "id is NULL");
     amgb::Nccl& nc = amgb::Nccl::get();
-    if (!nc.ok) return set_error(AMG_E_CUDA, "NCCL unavailable: " + nc.error);
+    if (!nc.ok) return set_error(AMG_E_NCCL, "NCCL unavailable: " + nc.error);
     const int r = nc.getUniqueId(id);
-    if (r != 0) return set_error(AMG_E_CUDA, "ncclGetUniqueId failed");
+    if (r != 0) return set_error(AMG_E_NCCL, "ncclGetUniqueId failed");
     return AMG_OK;
 }
 
@@ -3169,14 +3459,14 @@ amg_status amg_solve(amg_handle h, const double* f, double* x, double tol, int32
         return h->h->solve_api(f, x, tol, maxiter, iters, rel);
     } catch (const amgb::CudaError& e) {
         cudaGetLastError();
-        return set_error(AMG_E_CUDA, e.msg);
+        return set_error((amg_status)e.code, e.msg);
     }
 }
 
 amg_status amg_vector_length(amg_handle h, int64_t* n) {
     if (!h || !h->h || !n) return set_error(AMG_E_INVALID_ARG, "NULL argument");
     const Handle& H = *h->h;
-    *n = (H.virt || H.parts.empty()) ? H.host.levels[0].A.nrows : H.parts[0].lv[0].n;
+    *n = (H.virt || H.parts.empty()) ? H.meta[0].rows : H.parts[0].lv[0].n;
     return AMG_OK;
 }
 
@@ -3185,7 +3475,7 @@ amg_status amg_solve_host(amg_handle h, const double* f, const double* x0, doubl
     if (amg_status st = need_device(h)) return st;
     if (!f || !x || !iters || !rel) return set_error(AMG_E_INVALID_ARG, "f, x, iters, rel");
     Handle& H = *h->h;
-    const int64_t n = H.virt ? H.host.levels[0].A.nrows : H.parts[0].lv[0].n;
+    const int64_t n = H.virt ? H.meta[0].rows : H.parts[0].lv[0].n;
     try {
         ck(cudaSetDevice(H.device), "cudaSetDevice");
         if (!H.hf) {
@@ -3199,11 +3489,11 @@ amg_status amg_solve_host(amg_handle h, const double* f, const double* x0, doubl
             ck(cudaMemsetAsync(H.hx, 0, n * sizeof(double), H.stream), "zero x0");
         amg_status st = H.solve_api(H.hf, H.hx, tol, maxiter, iters, rel);
         ck(cudaMemcpyAsync(x, H.hx, n * sizeof(double), cudaMemcpyDeviceToHost, H.stream), "D2H x");
-        ck(cudaStreamSynchronize(H.stream), "sync");
+        H.sync(H.stream);
         return st;
     } catch (const amgb::CudaError& e) {
         cudaGetLastError();
-        return set_error(AMG_E_CUDA, e.msg);
+        return set_error((amg_status)e.code, e.msg);
     }
 }
 
@@ -3214,7 +3504,7 @@ amg_status amg_solve_host_stream(amg_handle h, int32_t k, const double* const* f
     for (int32_t j = 0; j < k; ++j)
         if (!f[j] || !x[j]) return set_error(AMG_E_INVALID_ARG, "f[j] / x[j] is NULL");
     Handle& H = *h->h;
-    const int64_t n = H.virt ? H.host.levels[0].A.nrows : H.parts[0].lv[0].n;
+    const int64_t n = H.virt ? H.meta[0].rows : H.parts[0].lv[0].n;
     const size_t bytes = (size_t)n * sizeof(double);
     cudaStream_t cs = nullptr;
     cudaEvent_t in[2] = {nullptr, nullptr}, out[2] = {nullptr, nullptr}, done = nullptr;
@@ -3264,7 +3554,7 @@ amg_status amg_solve_host_stream(amg_handle h, int32_t k, const double* const* f
         ck(cudaStreamSynchronize(cs), "sync");
     } catch (const amgb::CudaError& e) {
         cudaGetLastError();
-        first = set_error(AMG_E_CUDA, e.msg);
+        first = set_error((amg_status)e.code, e.msg);
     }
     if (cs) cudaStreamSynchronize(cs), cudaStreamDestroy(cs);
     for (int b = 0; b < 2; ++b) {
@@ -3300,7 +3590,7 @@ amg_status amg_solve_batched(amg_handle h, int32_t k, const double* F, int64_t l
             else if (k <= 4) st = H.solve_batched<4>(k, Fs, n, Xs, n, tol, maxiter, iters, rel);
             else st = H.solve_batched<8>(k, Fs, n, Xs, n, tol, maxiter, iters, rel);
             for (int j = 0; j < k; ++j) H.perm_out(Xs + j * n, X + j * ldx);
-            ck(cudaStreamSynchronize(H.stream), "sync");
+            H.sync(H.stream);
             return st;
         }
         if (k <= 2) return H.solve_batched<2>(k, F, ldf, X, ldx, tol, maxiter, iters, rel);
@@ -3308,7 +3598,7 @@ amg_status amg_solve_batched(amg_handle h, int32_t k, const double* F, int64_t l
         return H.solve_batched<8>(k, F, ldf, X, ldx, tol, maxiter, iters, rel);
     } catch (const amgb::CudaError& e) {
         cudaGetLastError();
-        return set_error(AMG_E_CUDA, e.msg);
+        return set_error((amg_status)e.code, e.msg);
     }
 }
 
@@ -3327,7 +3617,7 @@ amg_status amg_precond_apply(amg_handle h, const double* r, double* z) {
         }
         ck(cudaGetLastError(), "launch");
     } catch (const amgb::CudaError& e) {
-        return set_error(AMG_E_CUDA, e.msg);
+        return set_error((amg_status)e.code, e.msg);
     }
     return AMG_OK;
 }
@@ -3350,24 +3640,24 @@ amg_status amg_set_profile(amg_handle h, int32_t mask) {
 
 amg_status amg_level_count(amg_handle h, int32_t* nlevels) {
     if (!h || !h->h || !nlevels) return set_error(AMG_E_INVALID_ARG, "NULL argument");
-    *nlevels = (int32_t)h->h->host.levels.size();
+    *nlevels = (int32_t)h->h->meta.size();
     return AMG_OK;
 }
 
 amg_status amg_level_info_get(amg_handle h, int32_t l, amg_level_info* out) {
     if (!h || !h->h || !out) return set_error(AMG_E_INVALID_ARG, "NULL argument");
     const Handle& H = *h->h;
-    if (l < 0 || l >= (int)H.host.levels.size()) return set_error(AMG_E_INVALID_ARG, "level out of range");
-    const auto& hl = H.host.levels[l];
-    const bool coarsest = l == (int)H.host.levels.size() - 1;
+    if (l < 0 || l >= (int)H.meta.size()) return set_error(AMG_E_INVALID_ARG, "level out of range");
+    const auto& hl = H.meta[l];
+    const bool coarsest = l == (int)H.meta.size() - 1;
     std::memset(out, 0, sizeof(*out));
-    out->rows = hl.A.nrows;
-    out->nnz_A = hl.A.nnz();
-    out->nnz_P = coarsest ? 0 : hl.P.nnz();
-    out->cols_P = coarsest ? 0 : hl.P.ncols;
+    out->rows = hl.rows;
+    out->nnz_A = hl.nnz_A;
+    out->nnz_P = coarsest ? 0 : hl.nnz_P;
+    out->cols_P = coarsest ? 0 : hl.cols_P;
     out->aggregates = coarsest ? 0 : hl.n_agg;
     out->is_coarsest = coarsest;
-    out->alg_bytes_vcycle = amgb::level_alg_bytes(hl.A.nrows, hl.A.nnz(), out->nnz_P, out->cols_P, H.prm, coarsest);
+    out->alg_bytes_vcycle = amgb::level_alg_bytes(hl.rows, hl.nnz_A, out->nnz_P, out->cols_P, H.prm, coarsest);
     if (!H.parts.empty()) {
         out->dev_bytes = H.parts[0].lv[l].dev_bytes;
         out->padded_nnz_A = H.parts[0].lv[l].padA;
@@ -3394,6 +3684,9 @@ static void copy_csr(const amgb::Csr& M, int64_t* p, int32_t* c, double* v) {
 amg_status amg_export_level(amg_handle h, int32_t l, const amg_level_export* out) {
     if (!h || !h->h || !out) return set_error(AMG_E_INVALID_ARG, "NULL argument");
     const Handle& H = *h->h;
+    if (H.host.levels.empty())
+        return set_error(AMG_E_INVALID_ARG, "amg_export_level: this rank holds no global hierarchy (scattered "
+                                            "multi-GPU setup: export on rank 0)");
     if (l < 0 || l >= (int)H.host.levels.size()) return set_error(AMG_E_INVALID_ARG, "level out of range");
     const auto& hl = H.host.levels[l];
     const bool coarsest = l == (int)H.host.levels.size() - 1;
@@ -3501,7 +3794,7 @@ amg_status amg_dist_export(amg_handle h, int32_t rank, int32_t l, const amg_dist
 amg_status amg_nccl_selftest(int32_t device) {
     using namespace amgb;
     Nccl& nc = Nccl::get();
-    if (!nc.ok) return set_error(AMG_E_CUDA, "NCCL unavailable: " + nc.error);
+    if (!nc.ok) return set_error(AMG_E_NCCL, "NCCL unavailable: " + nc.error);
     void* comm = nullptr;
     double* buf = nullptr;
     cudaStream_t s = nullptr;
@@ -3549,12 +3842,12 @@ amg_status amg_nccl_selftest(int32_t device) {
             ck(cudaMemcpy(r.data(), buf, r.size() * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
             for (int i = 0; i < n; ++i)
                 if (r[n + i] != h[i] || r[2 * n + i] != h[2 * n + i] || r[3 * n + i] != h[3 * n + i]) {
-                    st = set_error(AMG_E_CUDA, "NCCL self-test: wrong data (pass " + std::to_string(pass) + ")");
+                    st = set_error(AMG_E_NCCL, "NCCL self-test: wrong data (pass " + std::to_string(pass) + ")");
                     break;
                 }
         }
     } catch (const CudaError& e) {
-        st = set_error(AMG_E_CUDA, e.msg);
+        st = set_error((amg_status)e.code, e.msg);
     }
     if (ge) cudaGraphExecDestroy(ge);
     if (g) cudaGraphDestroy(g);
@@ -3562,6 +3855,30 @@ amg_status amg_nccl_selftest(int32_t device) {
     if (s) cudaStreamDestroy(s);
     if (comm && nc.commDestroy) nc.commDestroy(comm);
     return st;
+}
+
+amg_status amg_shm_selftest(const uint8_t id[128], int32_t rank, int32_t nranks) {
+    using namespace amgb;
+    if (!id || nranks < 1 || rank < 0 || rank >= nranks) return set_error(AMG_E_INVALID_ARG, "id, rank, nranks");
+    try {
+        ShmComm c(id, rank, nranks, nccl_timeout_s());
+        // payload rank -> p of round k: (1000 r + 10 p + k) repeated, sizes 0, small, 1 MB
+        for (int k = 0; k < 3; ++k) {
+            auto len = [&](int r, int p) { return (size_t)(k == 2 ? (1 << 20) : (r + p + k) % 3 == 0 ? 0 : 17 * (r + 1)); };
+            std::vector<std::vector<uint8_t>> out(nranks), in;
+            for (int p = 0; p < nranks; ++p) out[p].assign(len(rank, p), (uint8_t)(100 * rank + 10 * p + k));
+            c.alltoallv(out, in);
+            for (int p = 0; p < nranks; ++p) {
+                if (in[p].size() != len(p, rank)) return set_error(AMG_E_NCCL, "shm self-test: wrong size");
+                for (uint8_t b : in[p])
+                    if (b != (uint8_t)(100 * p + 10 * rank + k)) return set_error(AMG_E_NCCL, "shm self-test: wrong data");
+            }
+        }
+        c.barrier();
+    } catch (const std::exception& e) {
+        return set_error(AMG_E_NCCL, std::string("shm self-test: ") + e.what());
+    }
+    return AMG_OK;
 }
 
 static amg_status level_op_impl(amgb::Handle& H, int32_t l, int32_t op, const double* x, const double* f, double* y);
@@ -3588,10 +3905,10 @@ amg_status amg_level_op(amg_handle h, int32_t l, int32_t op, const double* x, co
         if (f) H.perm_in(f, fs, l);
         const amg_status st = level_op_impl(H, l, op, xs, fs, ys);
         if (st == AMG_OK) H.perm_out(ys, y, ly);
-        ck(cudaStreamSynchronize(H.stream), "sync");
+        H.sync(H.stream);
         return st;
     } catch (const amgb::CudaError& e) {
-        return set_error(AMG_E_CUDA, e.msg);
+        return set_error((amg_status)e.code, e.msg);
     }
 }
 
@@ -3653,7 +3970,7 @@ static amg_status level_op_impl(amgb::Handle& H, int32_t l, int32_t op, const do
         }
         ck(cudaGetLastError(), "launch");
     } catch (const amgb::CudaError& e) {
-        return set_error(AMG_E_CUDA, e.msg);
+        return set_error((amg_status)e.code, e.msg);
     }
     return AMG_OK;
 }
@@ -3745,12 +4062,12 @@ static amg_status level_op_ex_impl(amgb::Handle& H, int32_t l, int32_t op, amg_l
         } else if (has_res) {
             KState kh{};
             ck(cudaMemcpyAsync(&kh, ks, sizeof(KState), cudaMemcpyDeviceToHost, H.stream), "D2H");
-            ck(cudaStreamSynchronize(H.stream), "sync");
+            H.sync(H.stream);
             a.dot = kh.res;
         }
-        ck(cudaStreamSynchronize(H.stream), "sync");  // scratch is freed at scope exit
+        H.sync(H.stream);  // scratch is freed at scope exit
     } catch (const amgb::CudaError& e) {
-        return set_error(AMG_E_CUDA, e.msg);
+        return set_error((amg_status)e.code, e.msg);
     }
     return AMG_OK;
 }
@@ -3797,10 +4114,10 @@ amg_status amg_level_op_ex(amg_handle h, int32_t l, int32_t op, amg_level_op_arg
             if (a->out2) H.perm_out(b.out2, a->out2, l);
             a->dot = b.dot;
         }
-        ck(cudaStreamSynchronize(H.stream), "sync");
+        H.sync(H.stream);
         return st;
     } catch (const amgb::CudaError& e) {
-        return set_error(AMG_E_CUDA, e.msg);
+        return set_error((amg_status)e.code, e.msg);
     }
 }
 

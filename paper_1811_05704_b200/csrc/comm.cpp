@@ -3,7 +3,13 @@
 
 #include <dlfcn.h>
 
+#include <chrono>
+#include <condition_variable>
+#include <cstdlib>
 #include <cstring>
+#include <memory>
+#include <mutex>
+#include <thread>
 
 namespace amgb {
 
@@ -47,6 +53,8 @@ Nccl& Nccl::get() {
         reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(sym("ncclBroadcast"));
     n.getErrorString = reinterpret_cast<const char* (*)(int)>(sym("ncclGetErrorString"));
     n.ok = all;
+    n.commGetAsyncError = reinterpret_cast<int (*)(void*, int*)>(dlsym(h, "ncclCommGetAsyncError"));
+    n.commAbort = reinterpret_cast<int (*)(void*)>(dlsym(h, "ncclCommAbort"));
     if (!all) n.error = "libnccl.so.2 lacks a required symbol";
     return n;
 }
@@ -57,6 +65,39 @@ int nccl_comm_init(void** comm, int nranks, const uint8_t id[128], int rank) {
     UniqueId u;
     std::memcpy(u.internal, id, 128);
     return reinterpret_cast<InitRankFn>(n.commInitRank)(comm, nranks, u, rank);
+}
+
+double nccl_timeout_s() {
+    const char* e = std::getenv("AMGB_NCCL_TIMEOUT_S");
+    const double t = e ? std::atof(e) : 0.0;
+    return t > 0 ? t : 300.0;
+}
+
+int nccl_comm_init_timeout(void** comm, int nranks, const uint8_t id[128], int rank, int device, double timeout_s) {
+    struct Shared {
+        std::mutex m;
+        std::condition_variable cv;
+        bool done = false;
+        int rc = 0;
+        void* comm = nullptr;
+    };
+    auto sh = std::make_shared<Shared>();
+    uint8_t idc[128];
+    std::memcpy(idc, id, 128);
+    std::thread([sh, nranks, rank, device, idc]() {
+        cudaSetDevice(device);
+        void* c = nullptr;
+        const int rc = nccl_comm_init(&c, nranks, idc, rank);
+        std::lock_guard<std::mutex> g(sh->m);
+        sh->rc = rc;
+        sh->comm = c;
+        sh->done = true;
+        sh->cv.notify_all();
+    }).detach();
+    std::unique_lock<std::mutex> lk(sh->m);
+    if (!sh->cv.wait_for(lk, std::chrono::duration<double>(timeout_s), [&] { return sh->done; })) return -2;
+    *comm = sh->comm;
+    return sh->rc;
 }
 
 }  // namespace amgb

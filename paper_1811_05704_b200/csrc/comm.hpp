@@ -25,6 +25,10 @@ struct Nccl {
     int (*allReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
     int (*broadcast)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
     const char* (*getErrorString)(int) = nullptr;
+    // fault handling (optional symbols; NCCL >= 2.4): a peer that died or never
+    // joined turns into AMG_E_NCCL after a timeout instead of a hang
+    int (*commGetAsyncError)(void*, int*) = nullptr;
+    int (*commAbort)(void*) = nullptr;
 
     static Nccl& get();  // loads on first call
 };
@@ -32,7 +36,21 @@ struct Nccl {
 constexpr int kNcclDouble = 8;  // ncclFloat64
 constexpr int kNcclSum = 0;     // ncclSum
 
+constexpr int kNcclUint8 = 1;   // ncclUint8
+constexpr int kNcclInProgress = 7;
+
 // ncclCommInitRank with the 128-byte unique id.
 int nccl_comm_init(void** comm, int nranks, const uint8_t id[128], int rank);
+
+// Seconds a multi-GPU handle waits for a peer (communicator creation, the
+// setup scatter, every host synchronisation of a solve) before it aborts the
+// communicator and reports AMG_E_NCCL: AMGB_NCCL_TIMEOUT_S, default 300.
+double nccl_timeout_s();
+
+// nccl_comm_init on a helper thread (device `device` current there), waiting at
+// most timeout_s: 0 = the communicator is up; -2 = timed out (the helper thread
+// stays blocked inside NCCL and is detached: the peers never joined); other
+// values: the NCCL error.
+int nccl_comm_init_timeout(void** comm, int nranks, const uint8_t id[128], int rank, int device, double timeout_s);
 
 }  // namespace amgb

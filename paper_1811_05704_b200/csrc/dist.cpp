@@ -2,6 +2,7 @@
 #include "dist.hpp"
 
 #include <algorithm>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 
@@ -189,6 +190,164 @@ RankPart build_rank_part(const HostHierarchy& H, int nranks, int rank, int lg,
         }
     }
     return RP;
+}
+
+std::vector<LevelMeta> level_meta(const HostHierarchy& H) {
+    std::vector<LevelMeta> m(H.levels.size());
+    for (size_t l = 0; l < H.levels.size(); ++l) {
+        const HostLevel& hl = H.levels[l];
+        const bool coarsest = l + 1 == H.levels.size();
+        m[l].rows = hl.A.nrows;
+        m[l].nnz_A = hl.A.nnz();
+        m[l].nnz_P = coarsest ? 0 : hl.P.nnz();
+        m[l].cols_P = coarsest ? 0 : hl.P.ncols;
+        m[l].n_agg = coarsest ? 0 : hl.n_agg;
+        m[l].lmax = hl.lmax;
+        m[l].lmin = hl.lmin;
+        m[l].cheb_d = hl.cheb_d;
+        m[l].cheb_c = hl.cheb_c;
+    }
+    return m;
+}
+
+namespace {
+
+struct Writer {
+    std::vector<uint8_t>& b;
+    template <class T>
+    void put(const T& v) {
+        const auto* p = reinterpret_cast<const uint8_t*>(&v);
+        b.insert(b.end(), p, p + sizeof(T));
+    }
+    template <class V>
+    void vec(const V& v) {
+        put<int64_t>((int64_t)v.size());
+        const auto* p = reinterpret_cast<const uint8_t*>(v.data());
+        b.insert(b.end(), p, p + v.size() * sizeof(typename V::value_type));
+    }
+    void csr(const Csr& M) {
+        put(M.nrows);
+        put(M.ncols);
+        vec(M.ptr);
+        vec(M.col);
+        vec(M.val);
+    }
+};
+
+struct Reader {
+    const uint8_t* p;
+    const uint8_t* end;
+    void need(size_t n) const {
+        if ((size_t)(end - p) < n) throw SetupError{-1, "scattered setup: truncated part image"};
+    }
+    template <class T>
+    T get() {
+        need(sizeof(T));
+        T v;
+        std::memcpy(&v, p, sizeof(T));
+        p += sizeof(T);
+        return v;
+    }
+    template <class V>
+    void vec(V& v) {
+        const int64_t n = get<int64_t>();
+        if (n < 0) throw SetupError{-1, "scattered setup: bad part image"};
+        const size_t bytes = (size_t)n * sizeof(typename V::value_type);
+        need(bytes);
+        v.resize(n);
+        if (bytes) std::memcpy(v.data(), p, bytes);
+        p += bytes;
+    }
+    void csr(Csr& M) {
+        M.nrows = get<int64_t>();
+        M.ncols = get<int64_t>();
+        vec(M.ptr);
+        vec(M.col);
+        vec(M.val);
+    }
+};
+
+constexpr uint64_t kPartMagic = 0x414d4742504152ULL;  // "AMGBPAR"
+
+}  // namespace
+
+void pack_part(const PartHeader& hd, const RankPart& rp, std::vector<uint8_t>& out) {
+    out.clear();
+    Writer w{out};
+    w.put(kPartMagic);
+    w.vec(hd.meta);
+    w.put<int32_t>(hd.lg);
+    w.put<int64_t>((int64_t)hd.starts.size());
+    for (const auto& st : hd.starts) w.vec(st);
+    w.vec(hd.coarse_inv);
+    w.put<int32_t>(rp.rank);
+    w.put<int32_t>(rp.nranks);
+    w.put<int32_t>(rp.lg);
+    w.put<int64_t>((int64_t)rp.lv.size());
+    for (const LevelPart& lp : rp.lv) {
+        w.put<int32_t>(lp.replicated);
+        w.put<int32_t>(lp.next_replicated);
+        w.put(lp.row0);
+        w.put(lp.row1);
+        w.put(lp.crow0);
+        w.put(lp.crow1);
+        w.csr(lp.ma());
+        w.csr(lp.mp());
+        w.csr(lp.mr());
+        const HaloPlan& h = lp.halo;
+        w.put(h.nloc);
+        w.put(h.nghost);
+        w.vec(h.ghost_global);
+        w.vec(h.recv_peer);
+        w.vec(h.recv_off);
+        w.vec(h.recv_cnt);
+        w.vec(h.send_peer);
+        w.vec(h.send_off);
+        w.vec(h.send_cnt);
+        w.vec(h.send_idx);
+        w.vec(lp.m);
+        w.vec(lp.diag);
+    }
+    w.put(kPartMagic);
+}
+
+void unpack_part(const uint8_t* p, size_t n, PartHeader& hd, RankPart& rp) {
+    Reader r{p, p + n};
+    if (r.get<uint64_t>() != kPartMagic) throw SetupError{-1, "scattered setup: bad part image"};
+    r.vec(hd.meta);
+    hd.lg = r.get<int32_t>();
+    hd.starts.resize(r.get<int64_t>());
+    for (auto& st : hd.starts) r.vec(st);
+    r.vec(hd.coarse_inv);
+    rp.rank = r.get<int32_t>();
+    rp.nranks = r.get<int32_t>();
+    rp.lg = r.get<int32_t>();
+    rp.lv.resize(r.get<int64_t>());
+    for (LevelPart& lp : rp.lv) {
+        lp.replicated = r.get<int32_t>() != 0;
+        lp.next_replicated = r.get<int32_t>() != 0;
+        lp.row0 = r.get<int64_t>();
+        lp.row1 = r.get<int64_t>();
+        lp.crow0 = r.get<int64_t>();
+        lp.crow1 = r.get<int64_t>();
+        r.csr(lp.A);
+        r.csr(lp.P);
+        r.csr(lp.R);
+        HaloPlan& h = lp.halo;
+        h.nloc = r.get<int64_t>();
+        h.nghost = r.get<int64_t>();
+        r.vec(h.ghost_global);
+        r.vec(h.recv_peer);
+        r.vec(h.recv_off);
+        r.vec(h.recv_cnt);
+        r.vec(h.send_peer);
+        r.vec(h.send_off);
+        r.vec(h.send_cnt);
+        r.vec(h.send_idx);
+        r.vec(lp.m);
+        r.vec(lp.diag);
+    }
+    if (r.get<uint64_t>() != kPartMagic || r.p != r.end) throw SetupError{-1, "scattered setup: bad part image"};
 }
 
 }  // namespace amgb

@@ -67,4 +67,24 @@ std::vector<std::vector<int64_t>> level_starts(const HostHierarchy& H, int nrank
 RankPart build_rank_part(const HostHierarchy& H, int nranks, int rank, int lg,
                          const std::vector<std::vector<int64_t>>& starts);
 
+// ---- scattered setup (one process per GPU): rank 0 builds the global host
+// hierarchy once and sends every other rank its part, plus what a rank needs
+// to know about the whole hierarchy (level sizes, smoother bounds, partition,
+// the replicated coarse inverse).  The other ranks never hold the global matrix.
+struct LevelMeta {
+    int64_t rows = 0, nnz_A = 0, nnz_P = 0, cols_P = 0, n_agg = 0;
+    double lmax = 0, lmin = 0, cheb_d = 0, cheb_c = 0;
+};
+std::vector<LevelMeta> level_meta(const HostHierarchy& H);
+
+struct PartHeader {
+    std::vector<LevelMeta> meta;
+    int lg = 0;
+    std::vector<std::vector<int64_t>> starts;
+    std::vector<double> coarse_inv;
+};
+// Flat byte image of (header, part) and back (same host ABI on every rank).
+void pack_part(const PartHeader& hd, const RankPart& rp, std::vector<uint8_t>& out);
+void unpack_part(const uint8_t* p, size_t n, PartHeader& hd, RankPart& rp);
+
 }  // namespace amgb
