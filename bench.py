@@ -64,6 +64,9 @@ def parse():
                     help="mixed: fp32 hierarchy values in the V-cycle (not the headline; SURVEY §8f rank 2)")
     ap.add_argument("--reorder", default="auto", choices=["auto", "on", "off"],
                     help="locality reordering of the device store (params reorder 2 / 1 / 0)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="weak: BASELINE configs[4], Poisson on 256 x 256 x 256N (one 256^3 block per GPU); "
+                         "value = unknown-V-cycles/s (rows x V-cycles / s)")
     ap.add_argument("--json-out", default=None)
     return ap.parse_args()
 
@@ -326,8 +329,18 @@ def main():
         if world > 1:
             dist.barrier()
 
-    ptr, col, val, f = problem_arrays(args.problem, args.n)
-    n, nnz = len(f), int(ptr[-1])
+    weak = args.scaling == "weak"
+    if weak and args.problem != "poisson":
+        raise SystemExit("--scaling weak is the Poisson configuration (BASELINE.json configs[4])")
+    # multi-GPU: scattered setup -- rank 0 alone builds the global matrix and
+    # the hierarchy; the other ranks only need their slice of f
+    if rank == 0 or world == 1:
+        ptr, col, val, f = synth.weak_poisson(world, args.n) if weak else problem_arrays(args.problem, args.n)
+        n, nnz = len(f), int(ptr[-1])
+    else:
+        ptr = col = val = f = None
+        n = args.n ** 3 * world if weak else synth.problem_rows(args.problem, args.n)
+        nnz = None
     prm = {"precond.relax.type": cfg["relax"], "solver.type": cfg["solver"], "precision": args.precision}
     torch.empty(1, device=f"cuda:{local}")  # CUDA context creation stays outside setup_s
     torch.cuda.synchronize()
@@ -344,9 +357,12 @@ def main():
             uid.copy_(torch.tensor(list(amgb.nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(uid, 0)
         h = amgb.setup_dist(ptr, col, val, nranks=world, rank=rank, nccl_id=bytes(uid.cpu().tolist()),
-                            params=prm, device=local, use_graph=0 if args.no_graph else 1)
+                            params=prm, device=local, use_graph=0 if args.no_graph else 1, n=n)
         st = h.dist_info()["row_starts"]
         r0, r1 = int(st[rank]), int(st[rank + 1])
+        if f is None:
+            f = np.empty(n)
+            f[r0:r1] = np.ones(r1 - r0) if weak else synth.rhs_slice(args.problem, args.n, r0, r1)
     setup_s = time.perf_counter() - t0
     infos = [h.level_info(l) for l in range(h.nlevels)]
     nl = r1 - r0
@@ -414,6 +430,8 @@ def main():
     t_max_ms = float(t_local.item())
     # one global solve per step: the job's V-cycles are those of the solve
     value = float(vc_total) / (t_max_ms / 1e3)
+    if weak:  # whole-job work of a weak-scaling step: rows x V-cycles
+        value *= n
 
     # ---- end-to-end through the public API with HOST buffers (amg_solve_host_stream)
     e2e = None
@@ -436,7 +454,8 @@ def main():
         te = torch.tensor([dt], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": float(vc_e) / float(te.item()), "unit": "V-cycles/s",
+        e2e = {"value": float(vc_e) / float(te.item()) * (n if weak else 1),
+               "unit": "unknown-V-cycles/s" if weak else "V-cycles/s",
                "h2d_bytes_per_step": 8 * nl, "d2h_bytes_per_step": 8 * nl,
                "ms_per_step": 1e3 * float(te.item()) / args.steps,
                "timing": "host wall clock around one amg_solve_host_stream call of K systems (per system: "
@@ -468,7 +487,7 @@ def main():
     # ---- CPU baseline: the oracle on this host (rank 0, N = 1 only)
     cpu = None
     parity = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not weak:
         cb = cpu_baseline_full_solve(ptr, col, val, f, cfg, tol, maxiter)
         cpu = {"value": cb["vcycles"] / cb["solve_s"], "unit": "V-cycles/s", "cores": oracle_threads(),
                "kind": "oracle",
@@ -485,14 +504,17 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": METRIC,
-            "value": value, "unit": "V-cycles/s", "n_gpus": world, "steps": args.steps,
+            "metric": METRIC if not weak else
+            "AMG-CG unknown-V-cycles/s, 3D Poisson weak scaling 256^3 per GPU (BASELINE configs[4])",
+            "value": value, "unit": "unknown-V-cycles/s" if weak else "V-cycles/s", "n_gpus": world,
+            "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None,
+            "scaling": args.scaling, "vs_baseline": None,
             "dtype": "f64" if args.precision == "double" else "f64 (V-cycle matrix values f32)",
             "data": "synthetic (seeded generators, synth/): 7-point FD Poisson, f = 1",
             "config": {
-                "workload": workload_name(args, cfg), "n": n, "nnz": nnz, "tol": tol,
+                "workload": (f"poisson{args.n}x{args.n}x{args.n * world}_weak_cg_sa_spai0" if weak
+                             else workload_name(args, cfg)), "n": n, "nnz": nnz, "tol": tol,
                 "solver": cfg["solver"], "relax": cfg["relax"], "coarsening": "smoothed_aggregation",
                 "parallelism": "1 GPU" if world == 1 else
                 f"row partition over {world} GPUs (NCCL halo exchange + all-reduce; levels < "
@@ -506,7 +528,7 @@ def main():
                 "setup": "numeric steps on the GPU (strength, P, R, RAP, smoother), aggregation + coarse inverse on "
                          "the host; CUDA context created before the timer" if cfg.get("setup_device", 1) else "host",
                 "l2": "inputs larger than L2 (level-0 matrix %.2f GB + hierarchy vs 126 MB L2); no flush"
-                      % (12e-9 * nnz),
+                      % (12e-9 * infos[0]["nnz_A"]),
                 "solve_alg_GBps": solve_gbs, "solve_roofline_frac": solve_gbs / peak,
             },
             "roofline": {

@@ -2,8 +2,9 @@
 // numeric steps of the hierarchy construction -- strength of connection,
 // smoothed prolongation, R = P^T, the Galerkin products A P and R (A P), the
 // SPAI-0 / Jacobi diagonals and the Chebyshev bound's row sums -- run on the
-// device; the greedy aggregation stays on the host (Phase 1 is sequential by
-// definition, R3) and so does the coarsest dense inverse.
+// device, and so does the greedy aggregation: its sequential Phase 1 (R3) is
+// reproduced exactly by dependency propagation rounds (aggregate_dev below).
+// The coarsest dense inverse (253 rows at 256^3) stays on the host.
 //
 // Every device step performs exactly the host's operations in the host's
 // order (setup.cpp): one thread per row, sums in ascending column / inner
@@ -338,6 +339,135 @@ __global__ void k_smoother(int64_t n, const int64_t* ptr, const double* val, con
     }
 }
 
+// ---- aggregation on the device (R3; setup.cpp aggregate()) ----------------
+// Phase 1 is the sequential greedy scan "i becomes a root iff i and all of S_i
+// are unassigned when i is visited; a root claims S_i".  Its outcome has a
+// parallel characterisation: j is assigned at time i iff some root r < i has
+// j in {r} u S_r, so with D(i) = { r < i : ({i} u S_i) n ({r} u S_r) != {} }
+//   i is a root  <=>  every r in D(i) is a non-root,
+//   i is not     <=>  some r in D(i) is a root.
+// Decisions therefore propagate from lower to higher indices: cnt(i) counts the
+// (j, r) paths of D(i) (with multiplicity), a decided non-root r decrements the
+// counts of its dependents, a decided root makes its undecided dependents
+// non-roots, and a count reaching 0 makes i a root.  Each node is decided once,
+// by exactly the rule of the sequential scan, so roots, ids (root rank in
+// ascending order), claims and Phase 2 are BITWISE the host's.
+constexpr int32_t kUnd = 0, kRoot = 1, kNonRoot = 2;
+
+// strong pattern (j != i, ascending columns) of A: row lengths, then columns
+__global__ void k_s_len(int64_t n, const int64_t* ptr, const uint8_t* S, int64_t* sptr) {
+    ROWS_LOOP(i, n) {
+        int64_t c = 0;
+        for (int64_t k = ptr[i]; k < ptr[i + 1]; ++k) c += S[k];
+        sptr[i + 1] = c;
+    }
+}
+__global__ void k_s_fill(int64_t n, const int64_t* ptr, const int32_t* col, const uint8_t* S, const int64_t* sptr,
+                         int32_t* scol) {
+    ROWS_LOOP(i, n) {
+        int64_t o = sptr[i];
+        for (int64_t k = ptr[i]; k < ptr[i + 1]; ++k)
+            if (S[k]) scol[o++] = col[k];
+    }
+}
+
+// entries of the ascending list c[lo, hi) that are < x
+__device__ __forceinline__ int64_t count_below(const int32_t* c, int64_t lo, int64_t hi, int64_t x) {
+    int64_t a = lo, b = hi;
+    while (a < b) {
+        const int64_t m = (a + b) / 2;
+        if (c[m] < x) a = m + 1;
+        else b = m;
+    }
+    return a - lo;
+}
+
+// cnt(i) = sum over j in {i} u S_i of |{ r in {j} u S^T_j : r < i }|
+__global__ void k_agg_count(int64_t n, const int64_t* sptr, const int32_t* scol, const int64_t* tptr,
+                            const int32_t* tcol, int32_t* cnt, int32_t* state, int32_t* F, int32_t* fsize) {
+    ROWS_LOOP(i, n) {
+        int64_t c = count_below(tcol, tptr[i], tptr[i + 1], i);  // j = i
+        for (int64_t k = sptr[i]; k < sptr[i + 1]; ++k) {
+            const int64_t j = scol[k];
+            c += (j < i) + count_below(tcol, tptr[j], tptr[j + 1], i);
+        }
+        cnt[i] = (int32_t)c;
+        if (c == 0) {
+            state[i] = kRoot;
+            F[atomicAdd(fsize, 1)] = (int32_t)i;
+        } else {
+            state[i] = kUnd;
+        }
+    }
+}
+
+// one propagation round over the frontier F (nodes decided in the last round)
+__global__ void k_agg_round(const int32_t* F, const int32_t* fsize, const int64_t* sptr, const int32_t* scol,
+                            const int64_t* tptr, const int32_t* tcol, int32_t* cnt, int32_t* state, int32_t* Fn,
+                            int32_t* fnsize) {
+    const int32_t m = *fsize;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t r = F[t];
+        const bool root = state[r] == kRoot;
+        auto touch = [&](int32_t i) {  // dependent i > r of r
+            if (root) {
+                if (atomicCAS(&state[i], kUnd, kNonRoot) == kUnd) Fn[atomicAdd(fnsize, 1)] = i;
+            } else if (atomicSub(&cnt[i], 1) == 1) {
+                if (atomicCAS(&state[i], kUnd, kRoot) == kUnd) Fn[atomicAdd(fnsize, 1)] = i;
+            }
+        };
+        auto visit = [&](int64_t j) {  // i in {j} u S^T_j, i > r
+            if (j > r) touch((int32_t)j);
+            for (int64_t k = tptr[j] + count_below(tcol, tptr[j], tptr[j + 1], (int64_t)r + 1); k < tptr[j + 1]; ++k)
+                touch(tcol[k]);
+        };
+        visit(r);
+        for (int64_t k = sptr[r]; k < sptr[r + 1]; ++k) visit(scol[k]);
+    }
+}
+
+__global__ void k_agg_flags(int64_t n, const int32_t* state, int32_t* flag, int32_t* und) {
+    ROWS_LOOP(i, n) {
+        flag[i] = state[i] == kRoot;
+        if (state[i] == kUnd) atomicAdd(und, 1);
+    }
+}
+
+// Phase 1 claims: a root r takes id rank(r) for itself and S_r
+__global__ void k_agg_claim(int64_t n, const int32_t* state, const int32_t* rank, const int64_t* sptr,
+                            const int32_t* scol, int32_t* id, int64_t* root) {
+    ROWS_LOOP(i, n) {
+        if (state[i] != kRoot) continue;
+        const int32_t a = rank[i];
+        id[i] = a;
+        root[a] = i;
+        for (int64_t k = sptr[i]; k < sptr[i + 1]; ++k) id[scol[k]] = a;
+    }
+}
+
+// Phase 2 from the Phase-1 snapshot: the strongest aggregated strong
+// neighbour, ascending k, strict > (the lowest column wins ties)
+__global__ void k_agg_phase2(int64_t n, const int64_t* ptr, const int32_t* col, const double* val, const uint8_t* S,
+                             const int32_t* snap, int32_t* id, int32_t* left) {
+    ROWS_LOOP(i, n) {
+        if (snap[i] >= 0) continue;
+        double best = -1.0;
+        int32_t pick = -1;
+        for (int64_t k = ptr[i]; k < ptr[i + 1]; ++k) {
+            if (!S[k]) continue;
+            const int32_t j = col[k];
+            if (snap[j] < 0) continue;
+            const double w = fabs(val[k]);
+            if (w > best) {
+                best = w;
+                pick = snap[j];
+            }
+        }
+        id[i] = pick;
+        if (pick < 0) atomicAdd(left, 1);
+    }
+}
+
 // inclusive prefix sum in place over v[1..n] (v[0] = 0): CSR row pointers
 void scan_ptr(DVec<int64_t>& v) {
     const int64_t n = v.n - 1;
@@ -420,6 +550,92 @@ DCsr product(const DCsr& A, const DCsr& B, const Csr* hA, const Csr* hB) {
 
 }  // namespace
 
+// Device aggregation (kernels above): ids on the device (did) and on the host,
+// roots ascending.  Returns the aggregate count.
+int64_t aggregate_dev(const DCsr& dA, const DVec<uint8_t>& S, DVec<int32_t>& did, std::vector<int32_t>& id,
+                      std::vector<int64_t>& root, int* rounds_out) {
+    const int64_t n = dA.nrows;
+    // strong pattern and its transpose
+    DCsr Sc;
+    Sc.nrows = Sc.ncols = n;
+    Sc.ptr.resize(n + 1);
+    k_s_len<<<blocks_for(n), kThreads>>>(n, dA.ptr.p, S.p, Sc.ptr.p);
+    scan_ptr(Sc.ptr);
+    const int64_t ns = last_of(Sc.ptr);
+    if (ns >= INT32_MAX) gfail(-1, "GPU aggregation: too many strong connections");
+    Sc.col.resize(ns);
+    Sc.val.resize(ns);  // unused by the pattern transpose
+    k_s_fill<<<blocks_for(n), kThreads>>>(n, dA.ptr.p, dA.col.p, S.p, Sc.ptr.p, Sc.col.p);
+    gck(cudaGetLastError(), "strong pattern");
+    DCsr St = transpose_dev(Sc);  // rows ascending within each column
+    // Phase 1: counts, initial roots, propagation rounds
+    DVec<int32_t> cnt(n), state(n), F0(n), F1(n), sizes(2);
+    gck(cudaMemset(sizes.p, 0, 2 * sizeof(int32_t)), "memset");
+    k_agg_count<<<blocks_for(n), kThreads>>>(n, Sc.ptr.p, Sc.col.p, St.ptr.p, St.col.p, cnt.p, state.p, F0.p,
+                                             sizes.p);
+    gck(cudaGetLastError(), "agg count");
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = sms * 8;
+    int32_t* F[2] = {F0.p, F1.p};
+    int rounds = 0;
+    for (;;) {
+        // a batch of rounds without host synchronisation; an empty frontier
+        // makes a round a no-op
+        for (int b = 0; b < 16; ++b, ++rounds) {
+            const int c = rounds & 1;
+            gck(cudaMemsetAsync(sizes.p + (c ^ 1), 0, sizeof(int32_t)), "memset");
+            k_agg_round<<<grid, kThreads>>>(F[c], sizes.p + c, Sc.ptr.p, Sc.col.p, St.ptr.p, St.col.p, cnt.p,
+                                            state.p, F[c ^ 1], sizes.p + (c ^ 1));
+        }
+        gck(cudaGetLastError(), "agg round");
+        int32_t sz = 0;
+        gck(cudaMemcpy(&sz, sizes.p + (rounds & 1), sizeof(int32_t), cudaMemcpyDeviceToHost), "D2H");
+        if (sz == 0) break;
+        if (rounds > 4 * n + 64) gfail(-1, "GPU aggregation did not converge");
+    }
+    if (rounds_out) *rounds_out = rounds;
+    DVec<int32_t> flag(n), rank(n), und(1);
+    gck(cudaMemset(und.p, 0, sizeof(int32_t)), "memset");
+    k_agg_flags<<<blocks_for(n), kThreads>>>(n, state.p, flag.p, und.p);
+    int32_t h_und = 0;
+    gck(cudaMemcpy(&h_und, und.p, sizeof(int32_t), cudaMemcpyDeviceToHost), "D2H");
+    if (h_und != 0) gfail(-1, "GPU aggregation left undecided rows");
+    size_t tmp = 0;
+    gck(cub::DeviceScan::ExclusiveSum(nullptr, tmp, flag.p, rank.p, (int)n), "scan size");
+    DVec<unsigned char> t((int64_t)tmp);
+    gck(cub::DeviceScan::ExclusiveSum(t.p, tmp, flag.p, rank.p, (int)n), "scan");
+    int32_t last_rank = 0, last_flag = 0;
+    gck(cudaMemcpy(&last_rank, rank.p + n - 1, sizeof(int32_t), cudaMemcpyDeviceToHost), "D2H");
+    gck(cudaMemcpy(&last_flag, flag.p + n - 1, sizeof(int32_t), cudaMemcpyDeviceToHost), "D2H");
+    int64_t count = (int64_t)last_rank + last_flag;
+    did.resize(n);
+    gck(cudaMemset(did.p, 0xff, n * sizeof(int32_t)), "memset");  // -1
+    DVec<int64_t> droot(std::max<int64_t>(count, 1));
+    k_agg_claim<<<blocks_for(n), kThreads>>>(n, state.p, rank.p, Sc.ptr.p, Sc.col.p, did.p, droot.p);
+    // Phase 2 from the snapshot
+    DVec<int32_t> snap(n), left(1);
+    gck(cudaMemcpy(snap.p, did.p, n * sizeof(int32_t), cudaMemcpyDeviceToDevice), "D2D");
+    gck(cudaMemset(left.p, 0, sizeof(int32_t)), "memset");
+    k_agg_phase2<<<blocks_for(n), kThreads>>>(n, dA.ptr.p, dA.col.p, dA.val.p, S.p, snap.p, did.p, left.p);
+    gck(cudaGetLastError(), "agg phase 2");
+    id = did.to_host();
+    root.resize(count);
+    if (count) gck(cudaMemcpy(root.data(), droot.p, count * sizeof(int64_t), cudaMemcpyDeviceToHost), "D2H");
+    int32_t h_left = 0;
+    gck(cudaMemcpy(&h_left, left.p, sizeof(int32_t), cudaMemcpyDeviceToHost), "D2H");
+    if (h_left) {  // Phase 3 (provably empty, R3): leftovers become singletons in ascending order
+        for (int64_t i = 0; i < n; ++i)
+            if (id[i] < 0) {
+                id[i] = (int32_t)count++;
+                root.push_back(i);
+            }
+        did.from(id);
+    }
+    return count;
+}
+
 HostHierarchy build_hierarchy_gpu(Csr A0, const SetupParams& prm, int device) {
     gck(cudaSetDevice(device), "cudaSetDevice");
     const bool timing = std::getenv("AMGB_SETUP_TIMING") != nullptr;
@@ -456,19 +672,27 @@ HostHierarchy build_hierarchy_gpu(Csr A0, const SetupParams& prm, int device) {
         DVec<uint8_t> S(dA.nnz());
         k_strength<<<blocks_for(n), kThreads>>>(n, dA.ptr.p, dA.col.p, dA.val.p, d.p, eps * eps, S.p);
         gck(cudaGetLastError(), "strength");
-        const std::vector<uint8_t> Sh = S.to_host();
         lap("strength", lv);
-        // aggregation on the host (sequential Phase 1)
+        // aggregation (R3): on the device (AMGB_HOST_AGGREGATE=1: the host routine)
         std::vector<int32_t> id;
         std::vector<int64_t> root;
-        const int64_t cnt = aggregate(L.A, Sh, id, &root);
+        DVec<int32_t> did;
+        std::vector<uint8_t> Sh;
+        int64_t cnt = 0;
+        if (std::getenv("AMGB_HOST_AGGREGATE")) {
+            Sh = S.to_host();
+            cnt = aggregate(L.A, Sh, id, &root);
+            did.from(id);
+        } else {
+            int rounds = 0;
+            cnt = aggregate_dev(dA, S, did, id, root, &rounds);
+            if (timing) std::fprintf(stderr, "[gsetup] level %zu aggregation: %d propagation rounds\n", lv, rounds);
+        }
         lap("aggregate", lv);
         const bool slow = static_cast<double>(cnt) > 0.95 * static_cast<double>(n);
         if (cnt == n || (slow && prev_slow)) break;
         prev_slow = slow;
         // prolongation
-        DVec<int32_t> did;
-        did.from(id);
         DCsr dP;
         int64_t lmax = 0;
         for (int64_t i = 0; i < n; ++i) lmax = std::max<int64_t>(lmax, L.A.ptr[i + 1] - L.A.ptr[i]);
@@ -491,6 +715,7 @@ HostHierarchy build_hierarchy_gpu(Csr A0, const SetupParams& prm, int device) {
             k_p_fill<<<blocks_for(n), kThreads>>>(n, dA.ptr.p, dA.col.p, dA.val.p, S.p, did.p, prm.p_omega, dP.ptr.p,
                                                   dP.col.p, dP.val.p);
         } else {  // a row longer than the per-thread list: the host routine
+            if (Sh.empty()) Sh = S.to_host();
             dP = upload(prolongation(L.A, Sh, id, cnt, prm.smoothed, prm.p_omega));
         }
         gck(cudaGetLastError(), "prolongation");

@@ -174,5 +174,27 @@ def problem(name, n):
     raise ValueError(name)
 
 
+def problem_rows(name, n):
+    """Rows of problem(name, n) without building it (every generator is n^3)."""
+    if name not in ("poisson", "poisson_perm", "varcoef", "convdiff"):
+        raise ValueError(name)
+    return n ** 3
+
+
+def rhs_slice(name, n, r0, r1):
+    """Rows r0..r1-1 of problem(name, n)'s right-hand side without building the
+    matrix (f = 1 for every configuration; a permutation of ones
+    is ones) -- what a rank > 0 of the scattered multi-GPU setup needs."""
+    problem_rows(name, n)
+    return np.ones(r1 - r0)
+
+
+def weak_poisson(nranks, n=256):
+    """Weak-scaling configuration (BASELINE.json configs[4], §8c): Poisson
+    on the global box n x n x (n nranks), h = 1/(n+1) in every direction, so
+    each rank's z-slab is one n^3 block.  Returns (ptr, col, val, f)."""
+    return poisson3d(n, n, n * nranks, h=1.0 / (n + 1))
+
+
 def random_vector(n, seed=SEED_VEC):
     return np.random.default_rng(seed).standard_normal(n)

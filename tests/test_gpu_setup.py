@@ -1,7 +1,8 @@
 """GPU setup phase (params setup_device = "gpu", the default on a device;
 SURVEY §8f rank 3; gsetup.cu):
-strength, smoothed P, R = P^T, A P, R (A P) and the smoother data on the device,
-aggregation and the coarse inverse on the host.  The device steps perform the
+strength, aggregation (Phase 1 reproduced exactly by dependency-propagation
+rounds), smoothed P, R = P^T, A P, R (A P) and the smoother data on the device,
+the coarse inverse on the host.  The device steps perform the
 host's operations in the host's order without FMA contraction, so the whole
 hierarchy must be BITWISE equal to the host setup's (which tests/
 test_setup_parity.py pins bitwise to the oracle), and so must the solve.
@@ -149,3 +150,46 @@ def test_device_format_conversion_matches_host(gen, n, kw):
     torch.cuda.synchronize()
     assert itd == ith and reld == relh
     assert np.array_equal(xd.cpu().numpy(), xh.cpu().numpy())
+
+
+def random_mmatrix(n, deg, seed):
+    """Unstructured non-symmetric M-matrix: deg random off-diagonal entries per
+    row with independent magnitudes, so the strength pattern is NOT symmetric
+    (exercises S versus S^T in the device aggregation)."""
+    rng = np.random.default_rng(seed)
+    rows = np.repeat(np.arange(n), deg)
+    cols = (rows + rng.integers(1, n, size=n * deg)) % n
+    vals = -rng.uniform(0.01, 1.0, size=n * deg) ** 3
+    import scipy.sparse as sp
+    M = sp.coo_matrix((vals, (rows, cols)), shape=(n, n)).tocsr()
+    M.sum_duplicates()
+    d = np.asarray(abs(M).sum(axis=1)).ravel() + 0.5
+    M = (M + sp.diags(d)).tocsr()
+    M.sort_indices()
+    return M.indptr.astype(np.int64), M.indices.astype(np.int32), M.data.astype(np.float64), np.ones(n)
+
+
+@pytest.mark.parametrize("case", ["poisson256", "varcoef96", "random"])
+def test_gpu_aggregation_bitwise(case):
+    """Aggregates, roots (via the hierarchy) and every level of the GPU setup --
+    aggregation included -- bitwise equal to the host builder's, at the
+    headline size 256^3, on log-random coefficients, and on an unstructured
+    matrix with a non-symmetric strength pattern; the finest level's aggregates
+    also equal the oracle's or_aggregate."""
+    if case == "poisson256":
+        p, c, v, f = synth.problem("poisson", 256)
+    elif case == "varcoef96":
+        p, c, v, f = synth.problem("varcoef", 96)
+    else:
+        p, c, v, f = random_mmatrix(60000, 6, 11)
+    hg = amgb.setup(p, c, v)                        # device (default)
+    hh = amgb.setup(p, c, v, device=-1)             # host builder, host-only handle
+    assert hg.nlevels == hh.nlevels >= 2
+    for l in range(hh.nlevels - 1):
+        ag, ah = hg.export_level(l)["aggregates"], hh.export_level(l)["aggregates"]
+        assert np.array_equal(ag, ah), (case, l, int(np.sum(ag != ah)))
+    if case != "poisson256":
+        assert_same_hierarchy(hg, hh)
+    A = oracle.Csr(p, c, v)
+    ido, cnt = oracle.aggregate(A, oracle.strength(A, 0.08))
+    assert np.array_equal(hg.export_level(0)["aggregates"], ido)
