@@ -123,6 +123,7 @@ typedef struct {
 enum { AMG_FMT_CSR = 0,      /* row-block CSR (csr_rows) */
        AMG_FMT_SELL = 1,     /* SELL-32, one thread per row (sell_rows) */
        AMG_FMT_TMA = 2,      /* TMA-staged SELL-32 with the column-offset dictionary (sell_tma) */
+       AMG_FMT_TMACSR = 3,   /* TMA-staged CSR, padding-free (csr_tma) */
        AMG_FMT_NONE = 15 };  /* no such matrix (coarsest level: P, R) */
 
 /* Test/export hook (amg_export_level): caller-owned HOST buffers, sized from

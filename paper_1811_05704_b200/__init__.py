@@ -37,7 +37,7 @@ E_COARSE_TOO_LARGE, E_OOM, E_NO_DEVICE, E_CUDA, E_NCCL = -5, -6, -7, -10, -11
 OP_SPMV_A, OP_SPMV_P, OP_SPMV_R, OP_RESIDUAL, OP_RELAX, OP_COARSE, OP_VCYCLE = range(7)
 (OP_RES0, OP_RES0_MF, OP_RESTRICT_MF, OP_PROL0, OP_PROL0_MF, OP_PROL_ADD, OP_RELAX_RHO, OP_CHEB_STEP,
  OP_CG_DIR, OP_CG_UPDATE) = range(7, 17)
-FMT_CSR, FMT_SELL, FMT_TMA, FMT_NONE = 0, 1, 2, 15
+FMT_CSR, FMT_SELL, FMT_TMA, FMT_TMACSR, FMT_NONE = 0, 1, 2, 3, 15
 PROF_CLASSES = ("A0 pass", "A coarse", "transfer", "vector", "coarse solve")
 
 

@@ -287,14 +287,21 @@ HostTmaCols tma_cols(const Csr& A, HostSell& S, bool allow_dict) {
     return T;
 }
 
+// bytes of one stage of the TMA-staged CSR kernel (csr_tma): values, columns
+// (tile_ent each, a multiple of 4) and the tile's row pointers, 16-B aligned
+inline size_t tcsr_stage_bytes(int64_t tile_ent, bool f32) {
+    return (((size_t)tile_ent * ((f32 ? 4 : 8) + 4) + (size_t)(kTcRows + 8) * 4) + 15) & ~(size_t)15;
+}
+
 // A device matrix in the format chosen for it.
-enum class Fmt { CSR, SELL, TMA };
+enum class Fmt { CSR, SELL, TMA, TMACSR };
 
 struct DMat {
     Fmt fmt = Fmt::CSR;
     Sell sell;
     SellTma tma;
     CsrDev csr;
+    CsrTma tcsr;
     int64_t nrows = 0, ncols = 0, nnz = 0, stored = 0;
     int64_t idx_bytes = -1;  // column-index bytes the format needs (-1: 4 per entry)
     int64_t ndict = 0;       // TMA slices stored with an offset dictionary
@@ -310,6 +317,7 @@ struct DMat {
         const double ns = (double)((nrows + 31) / 32);
         if (fmt == Fmt::TMA) return 16.0 * ns;
         if (fmt == Fmt::SELL) return 8.0 * ns;
+        if (fmt == Fmt::TMACSR) return 4.0 * nrows;
         return 4.0 * nrows + 4.0 * (double)csr.nblocks;
     }
     // Multi-GPU split pass: rows [ib0, ib1) have no ghost column
@@ -328,7 +336,13 @@ struct DMat {
         v.idx_bytes = idx_bytes;
         v.bytes_scale = scale;
         v.origin = origin ? origin : this;
-        if (fmt == Fmt::TMA) {
+        if (fmt == Fmt::TMACSR) {
+            v.tcsr = tcsr;
+            v.tcsr.row0 = tcsr.row0 + r0;
+            v.tcsr.nrows = r1 - r0;
+            v.tcsr.ptr = tcsr.ptr + r0;
+            v.tcsr.ntiles = (r1 - r0 + kTcRows - 1) / kTcRows;
+        } else if (fmt == Fmt::TMA) {
             v.tma = tma;
             v.tma.row0 = tma.row0 + r0;
             v.tma.nrows = r1 - r0;
@@ -374,7 +388,7 @@ std::pair<int64_t, int64_t> interior_range(const Csr& M, int64_t nloc, Fmt fmt, 
         a = *lo;
         b = *(hi - 1);
     } else {
-        const int64_t g = fmt == Fmt::TMA ? 256 : 32;
+        const int64_t g = (fmt == Fmt::TMA || fmt == Fmt::TMACSR) ? 256 : 32;
         a = (a + g - 1) / g * g;
         b = b == M.nrows ? b : b / g * g;
     }
@@ -757,7 +771,30 @@ struct Handle {
         else
             rows_tma_impl<T, false, F32>(M, op, gate, red);
     }
-    // a part with no rows contributes zeros to an all-reduce
+    template <bool STREAM, bool F32, class Op>
+    void rows_tcsr_impl(const CsrTma& M, const Op& op, const int32_t* gate, const Red& red) {
+        auto kern = csr_tma<STREAM, Op, F32>;
+        CsrTma m = M;
+        m.smem_stage = (int32_t)tcsr_stage_bytes(M.tile_ent, F32);
+        const size_t smem = (size_t)kTmaStages * m.smem_stage + 2 * kTmaStages * 8;
+        static size_t configured = 0;  // per instantiation
+        if (smem > configured) {
+            ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
+            configured = smem;
+        }
+        // resident CTAs per SM: shared memory (228 KB per SM) and the launch bounds
+        const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(minb_of<Op>(4), (228 * 1024) / (smem + 1024)));
+        const int g = (int)std::max<int64_t>(1, std::min<int64_t>(M.ntiles, (int64_t)num_sms * per_sm));
+        klaunch(kern, g, kTmaThreads, smem, m, op, gate, red);
+    }
+    template <bool F32, class Op>
+    void rows_tcsr(const CsrTma& M, const Op& op, const int32_t* gate, const Red& red, bool stream_loads) {
+        if (stream_loads)
+            rows_tcsr_impl<true, F32>(M, op, gate, red);
+        else
+            rows_tcsr_impl<false, F32>(M, op, gate, red);
+    }
+        // a part with no rows contributes zeros to an all-reduce
     void zero_defer(Part& p, const Red* r = nullptr) {
         const Red& red = r ? *r : p.red;
         if (red.defer) ck(cudaMemsetAsync(red.defer, 0, 4 * sizeof(double), stream), "memset");
@@ -781,6 +818,8 @@ struct Handle {
         launch(mat_class(p, M), bytes, what, [&] {
             if (M.fmt == Fmt::TMA) {  // T = 1 lane per row (narrow rows only, pick_format)
                 rows_tma<1, F32>(M.tma, op, gate, red, big);
+            } else if (M.fmt == Fmt::TMACSR) {
+                rows_tcsr<F32>(M.tcsr, op, gate, red, big);
             } else if (M.fmt == Fmt::CSR) {
                 switch (M.csr.G) {
                     case 1: rows_csr<1, F32>(M.csr, op, gate, red, big); break;
@@ -2366,6 +2405,18 @@ namespace {
 // Matrix format policy: AMGB_FORMAT = auto (default) | csr | sell | tma.
 // auto: row-block CSR for matrices with < 65536 rows (coarse levels: few, long
 // rows); otherwise TMA-staged SELL-32 for narrow rows, SELL-32 for wide ones.
+// stage capacity (entries) of the TMA-staged CSR format: the largest tile's
+// value / column range after aligning its start down to 16 bytes
+int64_t tcsr_tile_ent(const Csr& A) {
+    int64_t te = 4;
+    for (int64_t r0 = 0; r0 < A.nrows; r0 += kTcRows) {
+        const int64_t r1 = std::min<int64_t>(r0 + kTcRows, A.nrows);
+        const int64_t e0 = A.ptr[r0], e1 = A.ptr[r1];
+        te = std::max<int64_t>(te, ((e1 - (e0 & ~(int64_t)3)) + 3) & ~(int64_t)3);  // columns (values need <= this)
+    }
+    return te;
+}
+
 Fmt pick_format(const Csr& A) {
     const char* e = std::getenv("AMGB_FORMAT");
     const std::string f = e ? e : "auto";
@@ -2376,12 +2427,29 @@ Fmt pick_format(const Csr& A) {
     // a TMA stage holds a tile of 8 slices x 32 rows x (longest row) entries at
     // 12 B, kTmaStages of them must fit the 227 KB of shared memory per CTA
     const bool tma_fits = (int64_t)kTmaStages * 256 * 12 * std::max<int64_t>(lmax, 1) + 64 <= 227 * 1024;
+    const bool tcsr_fits = A.nrows > 0 && A.nnz() < INT32_MAX &&
+                           (int64_t)kTmaStages * (int64_t)tcsr_stage_bytes(tcsr_tile_ent(A), false) + 64 <= 227 * 1024;
     if (f == "tma") return tma_fits ? Fmt::TMA : Fmt::SELL;
+    if (f == "tmacsr") return tcsr_fits ? Fmt::TMACSR : Fmt::SELL;
     if (A.nrows < 65536) return Fmt::CSR;
-    // narrow rows (level-0 A, P): TMA-staged SELL-32, one thread per row.  Wide
-    // rows (coarse A, R): their gathers are L2-bound and one thread per row of a
-    // register-pipelined SELL-32 measured faster than T > 1 lanes per row.
-    return lmax <= 12 ? Fmt::TMA : Fmt::SELL;
+    // SELL-32 padding: every row of a 32-row slice is stored at the slice's
+    // longest row's length
+    int64_t stored = 0;
+    for (int64_t s0 = 0; s0 < A.nrows; s0 += 32) {
+        int64_t w = 0;
+        for (int64_t r = s0; r < std::min<int64_t>(s0 + 32, A.nrows); ++r) w = std::max<int64_t>(w, A.ptr[r + 1] - A.ptr[r]);
+        stored += 32 * w;
+    }
+    const double pad = A.nnz() ? (double)stored / (double)A.nnz() : 1.0;
+    // AMGB_TMACSR: 0 never, 1 narrow padded matrices (default), 2 also wide ones
+    const char* tc = std::getenv("AMGB_TMACSR");
+    const int tmode = tc ? std::atoi(tc) : 1;
+    // narrow rows: TMA-staged SELL-32 when its slices are (nearly) unpadded --
+    // the level-0 stencil, whose slices also compress to an offset dictionary --
+    // else the padding-free TMA-staged CSR (smoothed-aggregation P).  Wide rows
+    // (coarse A, R): register-pipelined SELL-32, one thread per row.
+    if (lmax <= 12) return (tmode >= 1 && pad > 1.15 && tcsr_fits) ? Fmt::TMACSR : Fmt::TMA;
+    return (tmode >= 2 && pad > 1.05 && tcsr_fits) ? Fmt::TMACSR : Fmt::SELL;
 }
 
 // Row blocks of the CSR kernel: at most kEnt entries and a row cap chosen from
@@ -2619,6 +2687,34 @@ DMat upload_mat_impl(Handle& H, const Csr& A0, int64_t* bytes, bool f32) {
         if (f32) d.csr.valf = H.upload(std::vector<float>(A.val.begin(), A.val.end()));
         d.stored = d.nnz;
         *bytes += (int64_t)(ptr32.size() * 4 + A.col.size() * 12 + blocks.size() * 4);
+        return d;
+    }
+    if (d.fmt == Fmt::TMACSR) {  // CSR with padded arrays (csr_tma reads 16-B aligned ranges)
+        const int64_t n = A.nrows, nnz = A.nnz();
+        std::vector<int32_t> p32(n + 1 + 8);
+        for (int64_t i = 0; i <= n; ++i) p32[i] = (int32_t)A.ptr[i];
+        for (int64_t i = n + 1; i < n + 9; ++i) p32[i] = (int32_t)nnz;
+        hvec<int32_t> col(nnz + 4);
+        hvec<double> val(nnz + 2);
+        std::copy(A.col.begin(), A.col.end(), col.begin());
+        std::copy(A.val.begin(), A.val.end(), val.begin());
+        for (int k = 0; k < 4; ++k) col[nnz + k] = 0;
+        val[nnz] = val[nnz + 1] = 0.0;
+        CsrTma& t = d.tcsr;
+        t.nrows = n;
+        t.ncols = A.ncols;
+        t.ntiles = (n + kTcRows - 1) / kTcRows;
+        t.tile_ent = (int32_t)tcsr_tile_ent(A);
+        t.ptr = H.upload(p32);
+        t.col = H.upload(col);
+        t.val = H.upload(val);
+        if (f32) {
+            std::vector<float> vf(nnz + 4, 0.0f);
+            for (int64_t k = 0; k < nnz; ++k) vf[k] = (float)A.val[k];
+            t.valf = H.upload(vf);
+        }
+        d.stored = nnz;
+        *bytes += (int64_t)(p32.size() * 4 + col.size() * 4 + val.size() * 8);
         return d;
     }
     // SELL / TMA: rows sorted by length inside 256-row windows when it pays
@@ -3668,7 +3764,10 @@ amg_status amg_level_info_get(amg_handle h, int32_t l, amg_level_info* out) {
         out->sigma_mask = (L.A.sigma ? 1 : 0) | (L.P.sigma ? 2 : 0) | (L.R.sigma ? 4 : 0);
         auto code = [](const amgb::DMat& M, bool none) {
             if (none) return (int)AMG_FMT_NONE;
-            return M.fmt == amgb::Fmt::TMA ? (int)AMG_FMT_TMA : M.fmt == amgb::Fmt::SELL ? (int)AMG_FMT_SELL : (int)AMG_FMT_CSR;
+            return M.fmt == amgb::Fmt::TMA      ? (int)AMG_FMT_TMA
+                   : M.fmt == amgb::Fmt::TMACSR ? (int)AMG_FMT_TMACSR
+                   : M.fmt == amgb::Fmt::SELL   ? (int)AMG_FMT_SELL
+                                                : (int)AMG_FMT_CSR;
         };
         out->formats = code(L.A, coarsest && l > 0) | code(L.P, coarsest) << 4 | code(L.R, coarsest) << 8;
     }

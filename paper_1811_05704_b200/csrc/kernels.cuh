@@ -477,6 +477,131 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sel
     if constexpr (Op::NDOT > 0) grid_reduce<Op::NDOT>(dots, red, op.fin);
 }
 
+// ----------------------------------------------------------------- TMA-staged CSR kernel
+// Padding-free alternative to the TMA-staged SELL-32 for matrices whose rows
+// differ in length (smoothed-aggregation P and R, coarse A: SELL-32 pads every
+// row of a 32-row slice to the slice's longest row, 26 % of P0's stored entries
+// at 256^3).  A tile is 256 consecutive rows; its entries are the contiguous
+// CSR range [ptr[r0], ptr[r0 + 256]), which the producer warp moves into a
+// kTmaStages-deep shared-memory ring with three cp.async.bulk copies (values,
+// columns, the tile's 257 row pointers; each source aligned down to 16 bytes,
+// the arrays padded so the rounded-up tail stays in bounds).  Consumer warp w
+// owns rows 32 w .. 32 w + 31 of the tile, one thread per row: its entries are
+// read from shared memory in ascending column order (the CSR order of the
+// paper's product), gathers issued UN at a time, then the fused epilogue.
+constexpr int kTcRows = 256;  // rows per tile (8 consumer warps x 32)
+
+struct CsrTma {
+    int64_t nrows = 0, ncols = 0, ntiles = 0;
+    int64_t row0 = 0;             // first row of this (sub-)matrix view (a multiple of 256)
+    const int32_t* ptr = nullptr; // row pointers of the view's rows (absolute entry offsets, nnz < 2^31),
+                                  // readable up to 8 past the last row
+    const int32_t* col = nullptr; // padded by 4 entries
+    const double* val = nullptr;  // padded by 2 entries
+    const float* valf = nullptr;  // fp32 copy (mixed precision), padded by 4
+    int32_t tile_ent = 0;         // stage capacity in entries (max over tiles, incl. alignment slack)
+    int32_t smem_stage = 0;       // bytes of one stage
+};
+
+template <bool STREAM, class Op, bool F32 = false>
+__global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(2)) csr_tma(CsrTma A, Op op, const int32_t* gate,
+                                                                         Red red) {
+    using VT = std::conditional_t<F32, float, double>;
+    constexpr int VB = (int)sizeof(VT);
+    constexpr int VA = 16 / VB;  // value alignment unit (entries)
+    constexpr int UN = unroll_of<Op>(8);
+    pdl_wait();
+    if (gated(gate)) return;
+    op.prepare();
+    extern __shared__ __align__(128) unsigned char smem[];
+    // stage layout: val[tile_ent] | col[tile_ent] | ptr[kTcRows + 8]; barriers after the stages
+    const int te = A.tile_ent;
+    const size_t sb = (size_t)A.smem_stage;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTmaStages * sb);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kTmaStages; ++s) {
+            mbar_init(smem_u32(bars + s), 1);
+            mbar_init(smem_u32(bars + kTmaStages + s), kBlock / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    constexpr int ND = Op::NDOT > 0 ? Op::NDOT : 1;
+    double dots[ND];
+#pragma unroll
+    for (int k = 0; k < ND; ++k) dots[k] = 0.0;
+
+    if (warp == kBlock / 32) {  // ---------------- producer warp
+        if (lane == 0) {
+            uint64_t policy = 0;
+            if constexpr (STREAM) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+            int i = 0;
+            for (int64_t t = blockIdx.x; t < A.ntiles; t += gridDim.x, ++i) {
+                const int s = i % kTmaStages;
+                if (i >= kTmaStages) mbar_wait(smem_u32(bars + kTmaStages + s), ((i / kTmaStages) & 1) ^ 1);
+                const int64_t r0 = t * kTcRows;
+                const int64_t r1 = r0 + kTcRows < A.nrows ? r0 + kTcRows : A.nrows;
+                const int32_t e0 = A.ptr[r0], e1 = A.ptr[r1];
+                const int32_t va = e0 & ~(VA - 1), ca = e0 & ~3;
+                const uint32_t nv = (uint32_t)(((e1 - va) + VA - 1) & ~(VA - 1));
+                const uint32_t nc = (uint32_t)(((e1 - ca) + 3) & ~3);
+                const uint32_t np = (uint32_t)(((r1 - r0 + 1) + 3) & ~3);
+                const uint32_t full = smem_u32(bars + s);
+                unsigned char* st = smem + (size_t)s * sb;
+                mbar_expect_tx(full, nv * (uint32_t)VB + nc * 4u + np * 4u);
+                if (nv) {
+                    if constexpr (F32)
+                        bulk_g2s<STREAM>(smem_u32(st), A.valf + va, nv * 4u, full, policy);
+                    else
+                        bulk_g2s<STREAM>(smem_u32(st), A.val + va, nv * 8u, full, policy);
+                }
+                if (nc) bulk_g2s<STREAM>(smem_u32(st + (size_t)te * VB), A.col + ca, nc * 4u, full, policy);
+                bulk_g2s<STREAM>(smem_u32(st + (size_t)te * (VB + 4)), A.ptr + r0, np * 4u, full, policy);
+            }
+        }
+    } else {  // ------------------------------------ consumer warps
+        int i = 0;
+        for (int64_t t = blockIdx.x; t < A.ntiles; t += gridDim.x, ++i) {
+            const int s = i % kTmaStages;
+            const int64_t lrow = t * kTcRows + warp * 32 + lane;
+            const bool has_row = lrow < A.nrows;
+            const int64_t row = A.row0 + lrow;
+            typename Op::Row rr{};
+            if constexpr (cols_of<Op>() == 1)
+                if (has_row) rr = op.load(row);  // in flight during the wait
+            mbar_wait(smem_u32(bars + s), (i / kTmaStages) & 1);
+            const unsigned char* st = smem + (size_t)s * sb;
+            const int32_t* sp = reinterpret_cast<const int32_t*>(st + (size_t)te * (VB + 4));
+            const int32_t e0 = sp[0];
+            const VT* sv = reinterpret_cast<const VT*>(st) - (e0 & ~(VA - 1));
+            const int32_t* sc = reinterpret_cast<const int32_t*>(st + (size_t)te * VB) - (e0 & ~3);
+            acc_t<Op> sum{};
+            if (has_row) {
+                const int32_t pb = sp[warp * 32 + lane], pe = sp[warp * 32 + lane + 1];
+                for (int32_t k0 = pb; k0 < pe; k0 += UN) {
+                    acc_t<Op> xv[UN];
+                    int32_t c[UN];
+#pragma unroll
+                    for (int u = 0; u < UN; ++u) c[u] = k0 + u < pe ? sc[k0 + u] : 0;
+#pragma unroll
+                    for (int u = 0; u < UN; ++u) xv[u] = (k0 + u < pe) ? op.gather(c[u]) : acc_t<Op>{};
+#pragma unroll
+                    for (int u = 0; u < UN; ++u)
+                        if (k0 + u < pe) fma_acc(sum, (double)sv[k0 + u], xv[u]);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(bars + kTmaStages + s));  // stage free
+            if constexpr (cols_of<Op>() > 1)
+                if (has_row) rr = op.load(row);
+            if (has_row) op.row(row, sum, rr, dots);
+        }
+    }
+    pdl_trigger();
+    if constexpr (Op::NDOT > 0) grid_reduce<Op::NDOT>(dots, red, op.fin);
+}
+
 // ----------------------------------------------------------------- row-block CSR kernel
 // Padding-free alternative to SELL for any row-length mix ("CSR-stream").  The
 // rows are cut on the host into blocks of at most kEnt entries (and kRowsMax

@@ -2,10 +2,11 @@
 device format the headline runs (VERDICT r1 "next #1").  GPU only (-m gpu).
 
 pick_format (amgb.cu) stores a matrix with >= 65,536 rows as TMA-staged SELL-32
-(narrow rows: A0, P0, P1 at 256^3) or SELL-32 (wide rows: R0, A1, R1), and
-smaller ones as row-block CSR; AMGB_FORMAT = sell | tma forces a format on every
-level, AMGB_NO_DICT=1 stores the TMA format with explicit column indices instead
-of the per-slice offset dictionary.  Each case runs every op of Algorithm 2
+(narrow, unpadded rows: A0 at 256^3), TMA-staged CSR (narrow rows that SELL-32
+would pad by > 15 %: P0, P1) or SELL-32 (wide rows: R0, A1, R1), and smaller
+ones as row-block CSR; AMGB_FORMAT = sell | tma | tmacsr forces a format on
+every level, AMGB_NO_DICT=1 stores the TMA format with explicit column indices
+instead of the per-slice offset dictionary.  Each case runs every op of Algorithm 2
  and of the CG iteration
 through amg_level_op / amg_level_op_ex -- the op structs and kernel templates the
 solve launches -- and compares every output row with the oracle on the same
@@ -93,21 +94,44 @@ FORMATS = {  # env of the device store
     "sell": {"AMGB_FORMAT": "sell"},
     "tma": {"AMGB_FORMAT": "tma"},
     "tma_explicit": {"AMGB_FORMAT": "tma", "AMGB_NO_DICT": "1"},
+    "tmacsr": {"AMGB_FORMAT": "tmacsr"},
 }
 
 
-def expected_fmt(fmt, rows, wide):
+def sell_padding(M):
+    """Stored / nnz of M as SELL-32 (every row at its 32-row slice's longest)."""
+    ln = lens(M)
+    pad = np.zeros(-(-len(ln) // 32) * 32)
+    pad[:len(ln)] = ln
+    return 32 * pad.reshape(-1, 32).max(axis=1).sum() / max(M.nnz, 1) if M.nrows else 1.0
+
+
+def expected_fmt(fmt, M):
     if fmt == "sell":
         return amgb.FMT_SELL
+    if fmt == "tmacsr":
+        return amgb.FMT_SELL if tcsr_wide(M) else amgb.FMT_TMACSR
     if fmt.startswith("tma"):
-        return amgb.FMT_SELL if wide else amgb.FMT_TMA
-    if rows < 65536:
+        return amgb.FMT_SELL if tma_wide(M) else amgb.FMT_TMA
+    if M.nrows < 65536:
         return amgb.FMT_CSR
-    return amgb.FMT_SELL if wide else amgb.FMT_TMA
+    if max_row(M) > 12:
+        return amgb.FMT_SELL
+    return amgb.FMT_TMACSR if sell_padding(M) > 1.15 and not tcsr_wide(M) else amgb.FMT_TMA
 
 
 def max_row(M):
     return int(lens(M).max()) if M.nrows else 0
+
+
+def tcsr_wide(M):
+    # two stages of the largest 256-row tile's entries (12 B) + row pointers
+    te = 4
+    for r0 in range(0, M.nrows, 256):
+        e0, e1 = int(M.ptr[r0]), int(M.ptr[min(r0 + 256, M.nrows)])
+        te = max(te, ((e1 - (e0 & ~3)) + 3) & ~3)
+    stage = (te * 12 + (256 + 8) * 4 + 15) & ~15
+    return 2 * stage + 64 > 227 * 1024
 
 
 def tma_wide(M):
@@ -141,8 +165,7 @@ def test_fused_kernels_per_row(gen, n, kw, fmt, monkeypatch):
         info = h.level_info(l)
         # the store is in the format this case is about
         for key, M in (("fmt_A", A), ("fmt_P", P), ("fmt_R", R)):
-            wide = max_row(M) > 12 if fmt == "auto" else tma_wide(M)
-            assert info[key] == expected_fmt(fmt, M.nrows, wide), (l, key, info["formats"])
+            assert info[key] == expected_fmt(fmt, M), (l, key, info["formats"])
         if fmt == "tma_explicit":
             assert info["dict_slices_A"] == 0
         n_l, nc = A.nrows, P.ncols
@@ -267,7 +290,7 @@ def test_fused_kernels_per_row(gen, n, kw, fmt, monkeypatch):
         assert abs(res * res - rr) <= dot_bound(r_ref, r_ref, b_r, b_r) + 4 * U * rr, (res, rr)
 
 
-@pytest.mark.parametrize("fmt", ["auto", "sell", "tma_explicit"])
+@pytest.mark.parametrize("fmt", ["auto", "sell", "tma_explicit", "tmacsr"])
 def test_vcycle_and_solve_per_format(fmt, monkeypatch):
     """The whole V-cycle (1e-12) and a converged CG solve (iterations +-1, x within
     1e-8 at equal count) in each format at >= 65,536 rows."""
@@ -287,8 +310,8 @@ def test_vcycle_and_solve_per_format(fmt, monkeypatch):
 
 def test_level1_in_sell_and_tma_under_auto(monkeypatch):
     """88^3 (681,472 rows): level 1 has >= 65,536 rows, so under the default policy
-    A1 and R0 run sell_rows and P0 / P1 run sell_tma, as at 256^3; every op of
-    levels 0-1 per row against the oracle."""
+    A1 and R0 run sell_rows, A0 sell_tma and P0 csr_tma, as at 256^3; every op
+    of levels 0-1 per row against the oracle."""
     for k in ("AMGB_FORMAT", "AMGB_NO_DICT"):
         monkeypatch.delenv(k, raising=False)
     p, c, v, f = synth.problem("poisson", 88)
@@ -296,7 +319,7 @@ def test_level1_in_sell_and_tma_under_auto(monkeypatch):
     o = oracle.Hierarchy(oracle.Csr(p, c, v))
     i1 = h.level_info(1)
     assert i1["rows"] >= 65536
-    assert h.level_info(0)["fmt_A"] == amgb.FMT_TMA and h.level_info(0)["fmt_P"] == amgb.FMT_TMA
+    assert h.level_info(0)["fmt_A"] == amgb.FMT_TMA and h.level_info(0)["fmt_P"] == amgb.FMT_TMACSR
     assert h.level_info(0)["fmt_R"] == amgb.FMT_SELL and i1["fmt_A"] == amgb.FMT_SELL
     rng = np.random.default_rng(7)
     for l in (0, 1):

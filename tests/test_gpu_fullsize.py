@@ -73,6 +73,7 @@ def test_headline_h0_poisson256_full_size():
     p, c, v, f = synth.problem("poisson", 256)
     h = amgb.setup(p, c, v)
     assert h.level_info(0)["fmt_A"] == amgb.FMT_TMA and h.level_info(0)["dict_slices_A"] > 0
+    assert h.level_info(0)["fmt_P"] == amgb.FMT_TMACSR
     A = oracle.Csr(p, c, v)
     ho = oracle.Hierarchy(A)
     assert h.nlevels == ho.nlevels
