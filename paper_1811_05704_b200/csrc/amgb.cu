@@ -42,6 +42,7 @@
 #include "ops.cuh"
 #include "setup.hpp"
 #include "shm.hpp"
+#include "tail.cuh"
 
 namespace amgb {
 
@@ -962,6 +963,117 @@ struct Handle {
                [&] { klaunch(vec_kernel<Op>, grid_for(n), kBlock, 0, n, op, gate, p.red); });
     }
 
+    // ------------------------------------------------------------ tail cycle
+    // The V-cycle below level tail_level runs as one cooperative kernel
+    // (tail.cuh) when every matrix there is in the row-block CSR format and the
+    // smoother is SPAI-0 / Jacobi with one sweep each way; AMGB_NO_TAIL=1 off.
+    int tail_level = -1;
+    int tail_grid = 0;
+    void setup_tail() {
+        tail_level = -1;
+        if (distributed() || parts.size() != 1 || prm.relax == 2 || prm.npre != 1 || prm.npost != 1 ||
+            prm.precision != 0 || std::getenv("AMGB_NO_TAIL"))
+            return;
+        const auto& lv = parts[0].lv;
+        const int nlev = (int)lv.size();
+        if (nlev < 2 || nlev - 1 > kTailMax / 4) return;
+        int lt = nlev - 1;
+        while (lt > 0 && lv[lt - 1].A.fmt == Fmt::CSR && lv[lt - 1].P.fmt == Fmt::CSR &&
+               lv[lt - 1].R.fmt == Fmt::CSR && lv[lt - 1].m)
+            --lt;
+        if (lt >= nlev - 1) return;  // nothing but the coarse solve
+        int per_sm = 0;
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tail_cycle<FinRho>, kBlock, 0), "occupancy");
+        if (per_sm < 1) return;
+        tail_grid = num_sms * std::min(per_sm, 2);
+        tail_level = lt;
+    }
+    bool tail_usable(int l) const { return tail_level >= 0 && l >= tail_level; }
+    // algorithmic bytes of one CSR step (the launch it replaces)
+    static double tail_step_bytes(const DMat& M, int gather, int rowv) {
+        return M.mat_bytes(false) + M.ptr_bytes() + 8.0 * M.ncols * gather + 8.0 * M.nrows * rowv;
+    }
+    void tail_vcycle(int l, const double* ftop, double* otop, const int32_t* gate, bool with_rho) {
+        Part& p = parts[0];
+        const int nlev = (int)p.lv.size();
+        TailProg P;
+        double bytes = 0.0;
+        auto add = [&](int op, const DMat* M, const double* a, const double* b, const double* f, const double* m,
+                       double* y, double* y2) {
+            TailStep& t = P.s[P.nsteps++];
+            t.op = op;
+            t.a = a, t.b = b, t.f = f, t.m = m, t.y = y, t.y2 = y2;
+            if (M) {
+                t.G = M->csr.G;
+                t.nrows = M->nrows;
+                t.ptr = M->csr.ptr;
+                t.col = M->csr.col;
+                t.val = M->csr.val;
+            }
+        };
+        for (int k = l; k < nlev - 1; ++k) {  // down: zero-start sweep + residual, restriction
+            DevLevel& L = p.lv[k];
+            DevLevel& C = p.lv[k + 1];
+            const double* fk = k == l ? ftop : L.f;
+            const bool mfk = L.mf != nullptr && (k > l || k > 0 || mf0);
+            if (mfk) {
+                add(kTailRes0MF, &L.A, nullptr, L.mf, fk, nullptr, L.t, nullptr);
+                bytes += tail_step_bytes(L.A, 1, 2);
+            } else {
+                add(kTailRes0, &L.A, nullptr, nullptr, fk, L.m, L.t, nullptr);
+                bytes += tail_step_bytes(L.A, 2, 1);
+            }
+            if (C.mf) {
+                add(kTailSpmvMF, &L.R, L.t, nullptr, nullptr, C.m, C.f, C.mf);
+                bytes += tail_step_bytes(L.R, 1, 3);
+            } else {
+                add(kTailSpmv, &L.R, L.t, nullptr, nullptr, nullptr, C.f, nullptr);
+                bytes += tail_step_bytes(L.R, 1, 1);
+            }
+        }
+        {  // coarsest: dense inverse
+            DevLevel& Lc = p.lv[nlev - 1];
+            TailStep& t = P.s[P.nsteps++];
+            t.op = kTailGemv;
+            t.nrows = Lc.n;
+            t.val = p.coarse_inv;
+            t.f = Lc.f;
+            t.y = Lc.o;
+            bytes += 8.0 * Lc.n * Lc.n + 16.0 * Lc.n;
+        }
+        for (int k = nlev - 2; k >= l; --k) {  // up: prolongation-correction, post-smoothing
+            DevLevel& L = p.lv[k];
+            DevLevel& C = p.lv[k + 1];
+            const double* fk = k == l ? ftop : L.f;
+            const bool mfk = L.mf != nullptr && (k > l || k > 0 || mf0);
+            if (mfk) {
+                add(kTailProl0MF, &L.P, C.o, L.mf, nullptr, nullptr, L.x, nullptr);
+                bytes += tail_step_bytes(L.P, 1, 2);
+            } else {
+                add(kTailProl0, &L.P, C.o, nullptr, fk, L.m, L.x, nullptr);
+                bytes += tail_step_bytes(L.P, 1, 3);
+            }
+            if (k == l && with_rho) P.rho_step = P.nsteps;
+            add(kTailRelax, &L.A, nullptr, L.x, fk, L.m, k == l ? otop : L.o, nullptr);
+            bytes += tail_step_bytes(L.A, 1, 3);
+        }
+        launch(AMG_PROF_COARSE_SOLVE, bytes, "tail cycle", [&] {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(tail_grid);
+            cfg.blockDim = dim3(kBlock);
+            cfg.stream = stream;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeCooperative;
+            at[0].val.cooperative = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            if (with_rho)
+                ck(cudaLaunchKernelEx(&cfg, tail_cycle<FinRho>, P, gate, p.red.partial, FinRho{p.ks}), "tail cycle");
+            else
+                ck(cudaLaunchKernelEx(&cfg, tail_cycle<NoFin>, P, gate, p.red.partial, NoFin{}), "tail cycle");
+        });
+    }
+
     // ------------------------------------------------------------ collectives
     using Sel = std::function<double*(Part&)>;
     using CSel = std::function<const double*(Part&)>;
@@ -1151,6 +1263,11 @@ struct Handle {
 // FinRho).  Returns true if the dot was fused.
 bool Handle::vcycle(int l, const CSel& fsel, const Sel& osel, const GSel& gate, bool with_rho) {
     const int nlev = (int)parts[0].lv.size();
+    if (l < nlev - 1 && tail_usable(l)) {
+        Part& p = parts[0];
+        tail_vcycle(l, fsel(p), osel(p), gate(p), with_rho);
+        return with_rho;
+    }
     if (l == nlev - 1) {  // coarsest: out = A_L^-1 f, replicated
         for (Part& p : parts) {
             DevLevel& L = p.lv[l];
@@ -3245,6 +3362,7 @@ static void device_upload(amgb::Handle& H) {
         H.d_defer_ptrs = H.upload(ptrs);
     }
     ck(cudaMallocHost(&H.ks_host, sizeof(KState)), "cudaMallocHost");
+    H.setup_tail();
     ck(cudaDeviceSynchronize(), "setup sync");
     if (H.reordered) {
         const int64_t n0 = H.parts[0].lv[0].n;
