@@ -116,7 +116,9 @@ typedef struct {
     int32_t sigma_mask;                 /* bit 0/1/2: A/P/R stored SELL-C-sigma (rows sorted by
                                            length inside 256-row windows) */
     int32_t formats;                    /* device format of A | P << 4 | R << 8 (single-GPU
-                                           handles): AMG_FMT_* */
+                                           handles): AMG_FMT_*; value storage
+                                           of A << 12 | P << 14 | R << 16: 0 fp64 array,
+                                           1 8-bit / 2 16-bit index into a value table */
 } amg_level_info;
 
 /* device matrix formats (amg_level_info.formats) */

@@ -308,6 +308,7 @@ class Hierarchy:
         d = {k: getattr(li, k) for k, _ in LevelInfo._fields_}
         f = d["formats"]
         d["fmt_A"], d["fmt_P"], d["fmt_R"] = f & 15, (f >> 4) & 15, (f >> 8) & 15
+        d["vidx_A"], d["vidx_P"], d["vidx_R"] = (f >> 12) & 3, (f >> 14) & 3, (f >> 16) & 3
         return d
 
     def complexities(self):

@@ -42,7 +42,6 @@
 #include "ops.cuh"
 #include "setup.hpp"
 #include "shm.hpp"
-#include "tail.cuh"
 
 namespace amgb {
 
@@ -290,8 +289,8 @@ HostTmaCols tma_cols(const Csr& A, HostSell& S, bool allow_dict) {
 
 // bytes of one stage of the TMA-staged CSR kernel (csr_tma): values, columns
 // (tile_ent each, a multiple of 4) and the tile's row pointers, 16-B aligned
-inline size_t tcsr_stage_bytes(int64_t tile_ent, bool f32) {
-    return (((size_t)tile_ent * ((f32 ? 4 : 8) + 4) + (size_t)(kTcRows + 8) * 4) + 15) & ~(size_t)15;
+inline size_t tcsr_stage_bytes(int64_t tile_ent, bool f32, bool vix = false) {
+    return (((size_t)tile_ent * ((vix ? 1 : f32 ? 4 : 8) + 4) + (size_t)(kTcRows + 8) * 4) + 15) & ~(size_t)15;
 }
 
 // A device matrix in the format chosen for it.
@@ -305,11 +304,12 @@ struct DMat {
     CsrTma tcsr;
     int64_t nrows = 0, ncols = 0, nnz = 0, stored = 0;
     int64_t idx_bytes = -1;  // column-index bytes the format needs (-1: 4 per entry)
+    int vbytes = 8;          // value bytes per entry: 8, or 1 / 2 with value-indexed storage
     int64_t ndict = 0;       // TMA slices stored with an offset dictionary
     bool sigma = false;      // rows sorted by length inside 256-row windows (sigma_sort)
     // algorithmic matrix bytes of one pass: values + the indices the format needs
     double mat_bytes(bool f32) const {
-        return (f32 ? 4.0 : 8.0) * nnz + (idx_bytes < 0 ? 4.0 * nnz : (double)idx_bytes);
+        return (f32 ? 4.0 : (double)vbytes) * nnz + (idx_bytes < 0 ? 4.0 * nnz : (double)idx_bytes);
     }
     // row-structure bytes the format's kernel reads per pass: CSR row pointers
     // (4 B per row) and row-block starts; SELL-32 one 8-B slice offset per 32
@@ -494,7 +494,14 @@ struct Handle {
         allocs.push_back(p);
         return static_cast<T*>(p);
     }
-    double* dalloc(int64_t n) {
+    void tfree(const void* p) {  // release a talloc / upload allocation early
+        auto it = std::find(allocs.begin(), allocs.end(), const_cast<void*>(p));
+        if (it != allocs.end()) {
+            cudaFree(*it);
+            allocs.erase(it);
+        }
+    }
+        double* dalloc(int64_t n) {
         void* p = nullptr;
         ck(cudaMalloc(&p, std::max<int64_t>(n, 1) * sizeof(double)), "cudaMalloc");
         ck(cudaMemset(p, 0, std::max<int64_t>(n, 1) * sizeof(double)), "cudaMemset");
@@ -755,7 +762,9 @@ struct Handle {
     template <int T, bool STREAM, bool F32, class Op>
     void rows_tma_impl(const SellTma& M, const Op& op, const int32_t* gate, const Red& red) {
         auto kern = sell_tma<T, STREAM, Op, F32>;
-        const size_t smem = (size_t)kTmaStages * M.tile_ent * (F32 ? 8 : 12) + 2 * kTmaStages * 8;
+        const bool vix = !F32 && M.vi8 != nullptr;
+        const size_t smem =
+            (vix ? kVTabBytes : 0) + (size_t)kTmaStages * M.tile_ent * (vix ? 5 : F32 ? 8 : 12) + 2 * kTmaStages * 8;
         static size_t configured = 0;  // per instantiation
         if (smem > configured) {
             ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
@@ -776,8 +785,9 @@ struct Handle {
     void rows_tcsr_impl(const CsrTma& M, const Op& op, const int32_t* gate, const Red& red) {
         auto kern = csr_tma<STREAM, Op, F32>;
         CsrTma m = M;
-        m.smem_stage = (int32_t)tcsr_stage_bytes(M.tile_ent, F32);
-        const size_t smem = (size_t)kTmaStages * m.smem_stage + 2 * kTmaStages * 8;
+        const bool vix = !F32 && M.vi8 != nullptr;
+        m.smem_stage = (int32_t)tcsr_stage_bytes(M.tile_ent, F32, vix);
+        const size_t smem = (vix ? kVTabBytes : 0) + (size_t)kTmaStages * m.smem_stage + 2 * kTmaStages * 8;
         static size_t configured = 0;  // per instantiation
         if (smem > configured) {
             ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
@@ -961,117 +971,6 @@ struct Handle {
         }
         launch(AMG_PROF_VECTOR, 8.0 * n * Op::STREAMS, what,
                [&] { klaunch(vec_kernel<Op>, grid_for(n), kBlock, 0, n, op, gate, p.red); });
-    }
-
-    // ------------------------------------------------------------ tail cycle
-    // The V-cycle below level tail_level runs as one cooperative kernel
-    // (tail.cuh) when every matrix there is in the row-block CSR format and the
-    // smoother is SPAI-0 / Jacobi with one sweep each way; AMGB_NO_TAIL=1 off.
-    int tail_level = -1;
-    int tail_grid = 0;
-    void setup_tail() {
-        tail_level = -1;
-        if (distributed() || parts.size() != 1 || prm.relax == 2 || prm.npre != 1 || prm.npost != 1 ||
-            prm.precision != 0 || std::getenv("AMGB_NO_TAIL"))
-            return;
-        const auto& lv = parts[0].lv;
-        const int nlev = (int)lv.size();
-        if (nlev < 2 || nlev - 1 > kTailMax / 4) return;
-        int lt = nlev - 1;
-        while (lt > 0 && lv[lt - 1].A.fmt == Fmt::CSR && lv[lt - 1].P.fmt == Fmt::CSR &&
-               lv[lt - 1].R.fmt == Fmt::CSR && lv[lt - 1].m)
-            --lt;
-        if (lt >= nlev - 1) return;  // nothing but the coarse solve
-        int per_sm = 0;
-        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tail_cycle<FinRho>, kBlock, 0), "occupancy");
-        if (per_sm < 1) return;
-        tail_grid = num_sms * std::min(per_sm, 2);
-        tail_level = lt;
-    }
-    bool tail_usable(int l) const { return tail_level >= 0 && l >= tail_level; }
-    // algorithmic bytes of one CSR step (the launch it replaces)
-    static double tail_step_bytes(const DMat& M, int gather, int rowv) {
-        return M.mat_bytes(false) + M.ptr_bytes() + 8.0 * M.ncols * gather + 8.0 * M.nrows * rowv;
-    }
-    void tail_vcycle(int l, const double* ftop, double* otop, const int32_t* gate, bool with_rho) {
-        Part& p = parts[0];
-        const int nlev = (int)p.lv.size();
-        TailProg P;
-        double bytes = 0.0;
-        auto add = [&](int op, const DMat* M, const double* a, const double* b, const double* f, const double* m,
-                       double* y, double* y2) {
-            TailStep& t = P.s[P.nsteps++];
-            t.op = op;
-            t.a = a, t.b = b, t.f = f, t.m = m, t.y = y, t.y2 = y2;
-            if (M) {
-                t.G = M->csr.G;
-                t.nrows = M->nrows;
-                t.ptr = M->csr.ptr;
-                t.col = M->csr.col;
-                t.val = M->csr.val;
-            }
-        };
-        for (int k = l; k < nlev - 1; ++k) {  // down: zero-start sweep + residual, restriction
-            DevLevel& L = p.lv[k];
-            DevLevel& C = p.lv[k + 1];
-            const double* fk = k == l ? ftop : L.f;
-            const bool mfk = L.mf != nullptr && (k > l || k > 0 || mf0);
-            if (mfk) {
-                add(kTailRes0MF, &L.A, nullptr, L.mf, fk, nullptr, L.t, nullptr);
-                bytes += tail_step_bytes(L.A, 1, 2);
-            } else {
-                add(kTailRes0, &L.A, nullptr, nullptr, fk, L.m, L.t, nullptr);
-                bytes += tail_step_bytes(L.A, 2, 1);
-            }
-            if (C.mf) {
-                add(kTailSpmvMF, &L.R, L.t, nullptr, nullptr, C.m, C.f, C.mf);
-                bytes += tail_step_bytes(L.R, 1, 3);
-            } else {
-                add(kTailSpmv, &L.R, L.t, nullptr, nullptr, nullptr, C.f, nullptr);
-                bytes += tail_step_bytes(L.R, 1, 1);
-            }
-        }
-        {  // coarsest: dense inverse
-            DevLevel& Lc = p.lv[nlev - 1];
-            TailStep& t = P.s[P.nsteps++];
-            t.op = kTailGemv;
-            t.nrows = Lc.n;
-            t.val = p.coarse_inv;
-            t.f = Lc.f;
-            t.y = Lc.o;
-            bytes += 8.0 * Lc.n * Lc.n + 16.0 * Lc.n;
-        }
-        for (int k = nlev - 2; k >= l; --k) {  // up: prolongation-correction, post-smoothing
-            DevLevel& L = p.lv[k];
-            DevLevel& C = p.lv[k + 1];
-            const double* fk = k == l ? ftop : L.f;
-            const bool mfk = L.mf != nullptr && (k > l || k > 0 || mf0);
-            if (mfk) {
-                add(kTailProl0MF, &L.P, C.o, L.mf, nullptr, nullptr, L.x, nullptr);
-                bytes += tail_step_bytes(L.P, 1, 2);
-            } else {
-                add(kTailProl0, &L.P, C.o, nullptr, fk, L.m, L.x, nullptr);
-                bytes += tail_step_bytes(L.P, 1, 3);
-            }
-            if (k == l && with_rho) P.rho_step = P.nsteps;
-            add(kTailRelax, &L.A, nullptr, L.x, fk, L.m, k == l ? otop : L.o, nullptr);
-            bytes += tail_step_bytes(L.A, 1, 3);
-        }
-        launch(AMG_PROF_COARSE_SOLVE, bytes, "tail cycle", [&] {
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(tail_grid);
-            cfg.blockDim = dim3(kBlock);
-            cfg.stream = stream;
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeCooperative;
-            at[0].val.cooperative = 1;
-            cfg.attrs = at;
-            cfg.numAttrs = 1;
-            if (with_rho)
-                ck(cudaLaunchKernelEx(&cfg, tail_cycle<FinRho>, P, gate, p.red.partial, FinRho{p.ks}), "tail cycle");
-            else
-                ck(cudaLaunchKernelEx(&cfg, tail_cycle<NoFin>, P, gate, p.red.partial, NoFin{}), "tail cycle");
-        });
     }
 
     // ------------------------------------------------------------ collectives
@@ -1263,11 +1162,6 @@ struct Handle {
 // FinRho).  Returns true if the dot was fused.
 bool Handle::vcycle(int l, const CSel& fsel, const Sel& osel, const GSel& gate, bool with_rho) {
     const int nlev = (int)parts[0].lv.size();
-    if (l < nlev - 1 && tail_usable(l)) {
-        Part& p = parts[0];
-        tail_vcycle(l, fsel(p), osel(p), gate(p), with_rho);
-        return with_rho;
-    }
     if (l == nlev - 1) {  // coarsest: out = A_L^-1 f, replicated
         for (Part& p : parts) {
             DevLevel& L = p.lv[l];
@@ -2529,9 +2423,10 @@ int64_t tcsr_tile_ent(const Csr& A) {
     for (int64_t r0 = 0; r0 < A.nrows; r0 += kTcRows) {
         const int64_t r1 = std::min<int64_t>(r0 + kTcRows, A.nrows);
         const int64_t e0 = A.ptr[r0], e1 = A.ptr[r1];
-        te = std::max<int64_t>(te, ((e1 - (e0 & ~(int64_t)3)) + 3) & ~(int64_t)3);  // columns (values need <= this)
+        te = std::max<int64_t>(te, ((e1 - (e0 & ~(int64_t)3)) + 3) & ~(int64_t)3);     // columns, fp64 values
+        te = std::max<int64_t>(te, ((e1 - (e0 & ~(int64_t)15)) + 15) & ~(int64_t)15);  // 1-byte value indices
     }
-    return te;
+    return (te + 15) & ~(int64_t)15;
 }
 
 Fmt pick_format(const Csr& A) {
@@ -2773,6 +2668,99 @@ bool sigma_sort(const Csr& A, std::vector<uint8_t>& rp, Csr& B) {
     return true;
 }
 
+// Value-indexed storage (CSR-VI, Kourtis, Goumas & Koziris 2008): a matrix whose
+// stored values take at most 256 (65536) distinct bit patterns is stored as a
+// table of those values plus a 1-byte (2-byte) index per entry, on the device:
+// sort the bit patterns, keep the unique ones, binary-search every entry.
+// Lossless (bit patterns, so -0.0 and 0.0 stay distinct): every kernel reads
+// exactly the stored values, and results are bitwise those of the plain store.
+// Smoothed-aggregation hierarchies of constant-coefficient operators qualify
+// (256^3 Poisson: A0 has 2 distinct values, P0 / R0 9, A1 2641 -> 16-bit);
+// log-random coefficients do not.  AMGB_NO_VIDX=1 disables it.
+__global__ void k_vidx(int64_t n, const unsigned long long* __restrict__ v, const unsigned long long* __restrict__ tab,
+                       int32_t ntab, uint8_t* i8, uint16_t* i16) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long x = v[k];
+        int32_t a = 0, b = ntab;
+        while (a < b) {
+            const int32_t m = (a + b) >> 1;
+            if (tab[m] < x) a = m + 1;
+            else b = m;
+        }
+        if (i8) i8[k] = (uint8_t)a;
+        else i16[k] = (uint16_t)a;
+    }
+}
+
+// dval: n device values; on success *tab (table, 256 or 65536 entries padded
+// with zeros) and exactly one of *i8 / *i16 (n + pad entries) are handle
+// allocations.  max_u: 256 or 65536.
+bool value_index(Handle& H, const double* dval, int64_t n, int64_t pad, int64_t max_u, const double** tab,
+                 const uint8_t** i8, const uint16_t** i16) {
+    *tab = nullptr, *i8 = nullptr, *i16 = nullptr;
+    if (n <= 0 || std::getenv("AMGB_NO_VIDX")) return false;
+    DevTmp tmp;
+    auto* keys = tmp.get<unsigned long long>(n);
+    auto* sorted = tmp.get<unsigned long long>(n);
+    auto* uniq = tmp.get<unsigned long long>(n);
+    int* nu = tmp.get<int>(1);
+    size_t t1 = 0, t2 = 0;
+    ck(cub::DeviceRadixSort::SortKeys(nullptr, t1, keys, sorted, (int)n), "vidx sort size");
+    ck(cub::DeviceSelect::Unique(nullptr, t2, sorted, uniq, nu, (int)n), "vidx unique size");
+    void* tt = tmp.get<unsigned char>((int64_t)std::max(t1, t2));
+    ck(cudaMemcpy(keys, dval, n * sizeof(double), cudaMemcpyDeviceToDevice), "vidx copy");
+    ck(cub::DeviceRadixSort::SortKeys(tt, t1, keys, sorted, (int)n), "vidx sort");
+    ck(cub::DeviceSelect::Unique(tt, t2, sorted, uniq, nu, (int)n), "vidx unique");
+    int h_nu = 0;
+    ck(cudaMemcpy(&h_nu, nu, sizeof(int), cudaMemcpyDeviceToHost), "D2H");
+    if (h_nu < 1 || h_nu > max_u) return false;
+    const int64_t tab_n = h_nu <= 256 ? 256 : 65536;
+    double* t = H.talloc<double>(tab_n);
+    ck(cudaMemset(t, 0, tab_n * sizeof(double)), "memset");
+    ck(cudaMemcpy(t, uniq, h_nu * sizeof(double), cudaMemcpyDeviceToDevice), "vidx table");
+    uint8_t* a8 = nullptr;
+    uint16_t* a16 = nullptr;
+    if (h_nu <= 256) {
+        a8 = H.talloc<uint8_t>(n + pad);
+        ck(cudaMemset(a8, 0, n + pad), "memset");
+    } else {
+        a16 = H.talloc<uint16_t>(n + pad);
+        ck(cudaMemset(a16, 0, (n + pad) * sizeof(uint16_t)), "memset");
+    }
+    k_vidx<<<cv_grid(n), 256>>>(n, reinterpret_cast<const unsigned long long*>(dval), uniq, h_nu, a8, a16);
+    ck(cudaGetLastError(), "vidx");
+    ck(cudaDeviceSynchronize(), "vidx sync");
+    *tab = t, *i8 = a8, *i16 = a16;
+    return true;
+}
+
+// value-index a freshly uploaded SELL / TMA / TMA-CSR store (fp64 V-cycle only)
+void index_store(Handle& H, DMat& d, int64_t* bytes) {
+    const double* tab = nullptr;
+    const uint8_t* i8 = nullptr;
+    const uint16_t* i16 = nullptr;
+    if (d.fmt == Fmt::TMA) {  // 1-byte indices only (the table lives in shared memory)
+        if (!value_index(H, d.tma.val, d.stored, 16, 256, &tab, &i8, &i16)) return;
+        H.tfree(d.tma.val);
+        d.tma.val = nullptr;
+        d.tma.vtab = tab, d.tma.vi8 = i8;
+    } else if (d.fmt == Fmt::TMACSR) {
+        if (!value_index(H, d.tcsr.val, d.nnz, 16, 256, &tab, &i8, &i16)) return;
+        H.tfree(d.tcsr.val);
+        d.tcsr.val = nullptr;
+        d.tcsr.vtab = tab, d.tcsr.vi8 = i8;
+    } else if (d.fmt == Fmt::SELL) {
+        if (!value_index(H, d.sell.val, d.stored, 16, 65536, &tab, &i8, &i16)) return;
+        H.tfree(d.sell.val);
+        d.sell.val = nullptr;
+        d.sell.vtab = tab, d.sell.vi8 = i8, d.sell.vi16 = i16;
+    } else {
+        return;
+    }
+    d.vbytes = i8 ? 1 : 2;
+    *bytes -= (8 - d.vbytes) * d.stored;
+}
+
 DMat upload_mat_impl(Handle& H, const Csr& A0, int64_t* bytes, bool f32) {
     DMat d;
     const Csr& A = A0;
@@ -2832,6 +2820,7 @@ DMat upload_mat_impl(Handle& H, const Csr& A0, int64_t* bytes, bool f32) {
         }
         d.stored = nnz;
         *bytes += (int64_t)(p32.size() * 4 + col.size() * 4 + val.size() * 8);
+        if (!f32) index_store(H, d, bytes);
         return d;
     }
     // SELL / TMA: rows sorted by length inside 256-row windows when it pays
@@ -2897,6 +2886,7 @@ DMat upload_mat_impl(Handle& H, const Csr& A0, int64_t* bytes, bool f32) {
         d.sigma = true;
         *bytes += (int64_t)rp.size();
     }
+    if (!f32) index_store(H, d, bytes);
     return d;
 }
 
@@ -3362,7 +3352,6 @@ static void device_upload(amgb::Handle& H) {
         H.d_defer_ptrs = H.upload(ptrs);
     }
     ck(cudaMallocHost(&H.ks_host, sizeof(KState)), "cudaMallocHost");
-    H.setup_tail();
     ck(cudaDeviceSynchronize(), "setup sync");
     if (H.reordered) {
         const int64_t n0 = H.parts[0].lv[0].n;
@@ -3887,7 +3876,9 @@ amg_status amg_level_info_get(amg_handle h, int32_t l, amg_level_info* out) {
                    : M.fmt == amgb::Fmt::SELL   ? (int)AMG_FMT_SELL
                                                 : (int)AMG_FMT_CSR;
         };
-        out->formats = code(L.A, coarsest && l > 0) | code(L.P, coarsest) << 4 | code(L.R, coarsest) << 8;
+        auto vmode = [](const amgb::DMat& M) { return M.vbytes == 1 ? 1 : M.vbytes == 2 ? 2 : 0; };
+        out->formats = code(L.A, coarsest && l > 0) | code(L.P, coarsest) << 4 | code(L.R, coarsest) << 8 |
+                       vmode(L.A) << 12 | vmode(L.P) << 14 | vmode(L.R) << 16;
     }
     return AMG_OK;
 }

@@ -34,6 +34,11 @@ struct Sell {
     // SELL-C-sigma (amgb.cu sigma_sort): slot s holds row (s & ~255) + rperm[s];
     // nullptr = slots are rows
     const uint8_t* rperm = nullptr;
+    // value-indexed storage (amgb.cu value_index): entry k's value is
+    // vtab[vi8[k]] (<= 256 distinct values) or vtab[vi16[k]] (<= 65536); val unused
+    const double* vtab = nullptr;
+    const uint8_t* vi8 = nullptr;
+    const uint16_t* vi16 = nullptr;
 };
 
 // stored slot -> matrix row of a SELL-C-sigma matrix (rows sorted by length
@@ -77,6 +82,17 @@ __device__ __forceinline__ float ld_mat(const float* p) {
 template <bool STREAM, bool F32, class M>
 __device__ __forceinline__ double ld_val(const M& A, int64_t k) {
     if constexpr (F32) return (double)ld_mat<STREAM>(A.valf + k); else return ld_mat<STREAM>(A.val + k);
+}
+__device__ __forceinline__ uint32_t ld_idx8(const uint8_t* p) { return __ldcs(reinterpret_cast<const unsigned char*>(p)); }
+__device__ __forceinline__ uint32_t ld_idx16(const uint16_t* p) { return __ldcs(reinterpret_cast<const unsigned short*>(p)); }
+// value k of a SELL store in its storage mode (VM: 0 = the value array / its
+// fp32 copy, 1 = 8-bit index into vtab, 2 = 16-bit index); the table is small
+// and read through L1
+template <int VM, bool STREAM, bool F32>
+__device__ __forceinline__ double ld_sell_val(const Sell& A, int64_t k) {
+    if constexpr (VM == 1) return __ldg(A.vtab + ld_idx8(A.vi8 + k));
+    else if constexpr (VM == 2) return __ldg(A.vtab + ld_idx16(A.vi16 + k));
+    else return ld_val<STREAM, F32>(A, k);
 }
 
 // Accumulator of a row kernel: one double (single right-hand side) or Vk<K> (K
@@ -217,17 +233,8 @@ __device__ __forceinline__ bool gated(const int32_t* gate) {
 // PIPE = false: all U entries of the (narrow, w <= U) row in one chunk, no
 // prefetch registers; launch bounds ask for >= 6 resident blocks (48 warps) so
 // enough loads are in flight per SM.
-template <int U1, bool STREAM, bool PIPE, class Op, bool F32 = false>
-__global__ void __launch_bounds__(kBlock, minb_of<Op>(PIPE ? 4 : 6)) sell_rows(Sell A, Op op, const int32_t* gate,
-                                                                                 Red red) {
-    constexpr int U = unroll_of<Op>(U1);
-    pdl_wait();
-    if (gated(gate)) return;
-    op.prepare();
-    constexpr int ND = Op::NDOT > 0 ? Op::NDOT : 1;
-    double dots[ND];
-#pragma unroll
-    for (int k = 0; k < ND; ++k) dots[k] = 0.0;
+template <int VM, int U, bool STREAM, bool PIPE, bool F32, class Op, int ND>
+__device__ __forceinline__ void sell_rows_body(const Sell& A, Op& op, double (&dots)[ND]) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < A.nrows; row += stride) {
         // row-local epilogue operands are requested first, so their latency
@@ -247,7 +254,7 @@ __global__ void __launch_bounds__(kBlock, minb_of<Op>(PIPE ? 4 : 6)) sell_rows(S
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             c[u] = u < w ? ld_mat<STREAM>(cp + 32 * u) : 0;
-            v[u] = u < w ? ld_val<STREAM, F32>(A, vb + 32 * u) : 0.0;
+            v[u] = u < w ? ld_sell_val<VM, STREAM, F32>(A, vb + 32 * u) : 0.0;
         }
         if constexpr (!PIPE) {
             acc_t<Op> xv[U];
@@ -269,7 +276,7 @@ __global__ void __launch_bounds__(kBlock, minb_of<Op>(PIPE ? 4 : 6)) sell_rows(S
             for (int u = 0; u < U; ++u) {
                 const int k = k0 + U + u;
                 cn[u] = k < w ? ld_mat<STREAM>(cp + 32 * k) : 0;
-                vn[u] = k < w ? ld_val<STREAM, F32>(A, vb + 32 * k) : 0.0;
+                vn[u] = k < w ? ld_sell_val<VM, STREAM, F32>(A, vb + 32 * k) : 0.0;
             }
 #pragma unroll
             for (int u = 0; u < U; ++u)
@@ -283,6 +290,25 @@ __global__ void __launch_bounds__(kBlock, minb_of<Op>(PIPE ? 4 : 6)) sell_rows(S
         if constexpr (cols_of<Op>() > 1) rr = op.load(grow);
         op.row(grow, sum, rr, dots);
     }
+}
+
+template <int U1, bool STREAM, bool PIPE, class Op, bool F32 = false>
+__global__ void __launch_bounds__(kBlock, minb_of<Op>(PIPE ? 4 : 6)) sell_rows(Sell A, Op op, const int32_t* gate,
+                                                                                 Red red) {
+    constexpr int U = unroll_of<Op>(U1);
+    pdl_wait();
+    if (gated(gate)) return;
+    op.prepare();
+    constexpr int ND = Op::NDOT > 0 ? Op::NDOT : 1;
+    double dots[ND];
+#pragma unroll
+    for (int k = 0; k < ND; ++k) dots[k] = 0.0;
+    if (A.vi8 && !F32)
+        sell_rows_body<1, U, STREAM, PIPE, F32>(A, op, dots);
+    else if (A.vi16 && !F32)
+        sell_rows_body<2, U, STREAM, PIPE, F32>(A, op, dots);
+    else
+        sell_rows_body<0, U, STREAM, PIPE, F32>(A, op, dots);
     pdl_trigger();
     if constexpr (Op::NDOT > 0) grid_reduce<Op::NDOT>(dots, red, op.fin);
 }
@@ -313,7 +339,14 @@ struct SellTma {
     int32_t T = 1;          // lanes per row; slice height C = 32 / T
     int32_t tile_ent = 0;   // capacity of one stage in entries (max over tiles)
     const uint8_t* rperm = nullptr;  // SELL-C-sigma slot -> row (T = 1: window = tile); see Sell
+    // value-indexed storage (<= 256 distinct values): the stage carries 1-byte
+    // indices, the kernel keeps the table in shared memory; val unused
+    const double* vtab = nullptr;
+    const uint8_t* vi8 = nullptr;
 };
+
+// shared-memory bytes of the value table of an indexed TMA store
+constexpr int kVTabBytes = 256 * 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -365,12 +398,19 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sel
     op.prepare();
     constexpr int C = 32 / T;  // slice height
     constexpr int NS = 8;      // slices per tile (one per consumer warp)
-    extern __shared__ __align__(128) unsigned char smem[];
-    // layout: kTmaStages x { val[tile_ent] (VB bytes), col[tile_ent] (4 B) } | barriers
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    // layout: [value table (indexed stores)] kTmaStages x { val[tile_ent] (VB bytes, or
+    // 1-byte indices), col[tile_ent] (4 B) } | barriers
+    const bool vix = !F32 && A.vi8 != nullptr;
+    double* vtab_s = reinterpret_cast<double*>(smem_raw);
+    unsigned char* smem = smem_raw + (vix ? kVTabBytes : 0);
+    const int vbytes = vix ? 1 : VB;
     const int te = A.tile_ent;
-    const size_t stage_bytes = (size_t)te * (VB + 4);
+    const size_t stage_bytes = (size_t)te * (vbytes + 4);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTmaStages * stage_bytes);  // full[S], empty[S]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (vix)
+        for (int k = threadIdx.x; k < 256; k += blockDim.x) vtab_s[k] = __ldg(A.vtab + k);
     if (threadIdx.x == 0) {
         for (int s = 0; s < kTmaStages; ++s) {
             mbar_init(smem_u32(bars + s), 1);
@@ -399,12 +439,14 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sel
                 const uint32_t n = (uint32_t)(e1 - e0), nc = (uint32_t)(c1 - c0);
                 const uint32_t full = smem_u32(bars + s);
                 unsigned char* st = smem + (size_t)s * stage_bytes;
-                mbar_expect_tx(full, n * (uint32_t)VB + nc * 4u);
-                if constexpr (F32)
+                mbar_expect_tx(full, n * (uint32_t)vbytes + nc * 4u);
+                if (vix)
+                    bulk_g2s<STREAM>(smem_u32(st), A.vi8 + e0, n, full, policy);
+                else if constexpr (F32)
                     bulk_g2s<STREAM>(smem_u32(st), A.valf + e0, n * 4u, full, policy);
                 else
                     bulk_g2s<STREAM>(smem_u32(st), A.val + e0, n * 8u, full, policy);
-                if (nc) bulk_g2s<STREAM>(smem_u32(st + (size_t)te * VB), A.col + c0, nc * 4u, full, policy);
+                if (nc) bulk_g2s<STREAM>(smem_u32(st + (size_t)te * vbytes), A.col + c0, nc * 4u, full, policy);
             }
         }
     } else {  // ------------------------------------ consumer warps
@@ -434,13 +476,16 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sel
             }
             mbar_wait(smem_u32(bars + s), (i / kTmaStages) & 1);
             const VT* sv = reinterpret_cast<const VT*>(smem + (size_t)s * stage_bytes) + off + r;
-            const int32_t* sc = reinterpret_cast<const int32_t*>(smem + (size_t)s * stage_bytes + (size_t)te * VB) +
+            const uint8_t* si = smem + (size_t)s * stage_bytes + off + r;
+            const int32_t* sc = reinterpret_cast<const int32_t*>(smem + (size_t)s * stage_bytes + (size_t)te * vbytes) +
                                 coff + (dict ? 0 : r);
             acc_t<Op> sum{};
             // entry k's column: sc[CS k] (+ row for a dictionary slice); the
-            // stride is a template constant so every load is an immediate offset
-            auto run = [&](auto cs, int32_t cbase) {
+            // stride is a template constant so every load is an immediate offset;
+            // its value: sv[C k], or the table entry of the index si[C k]
+            auto run = [&](auto cs, int32_t cbase, auto vx) {
                 constexpr int CS = decltype(cs)::value;
+                constexpr bool VX = decltype(vx)::value;
                 for (int k0 = pt; k0 < w; k0 += UN * T) {
                     acc_t<Op> xv[UN];
                     int32_t c[UN];
@@ -454,14 +499,27 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sel
 #pragma unroll
                     for (int u = 0; u < UN; ++u) {
                         const int k = k0 + u * T;
-                        if (k < w) fma_acc(sum, (double)sv[C * k], xv[u]);
+                        if constexpr (VX) {
+                            if (k < w) fma_acc(sum, vtab_s[si[C * k]], xv[u]);
+                        } else {
+                            if (k < w) fma_acc(sum, (double)sv[C * k], xv[u]);
+                        }
                     }
                 }
             };
-            if (dict)
-                run(std::integral_constant<int, 1>{}, (int32_t)row);
-            else
-                run(std::integral_constant<int, C>{}, 0);
+            using one = std::integral_constant<int, 1>;
+            using cc = std::integral_constant<int, C>;
+            if (vix) {
+                if (dict)
+                    run(one{}, (int32_t)row, std::true_type{});
+                else
+                    run(cc{}, 0, std::true_type{});
+            } else {
+                if (dict)
+                    run(one{}, (int32_t)row, std::false_type{});
+                else
+                    run(cc{}, 0, std::false_type{});
+            }
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(bars + kTmaStages + s));  // stage free
             if constexpr (T > 1) {
@@ -501,6 +559,8 @@ struct CsrTma {
     const float* valf = nullptr;  // fp32 copy (mixed precision), padded by 4
     int32_t tile_ent = 0;         // stage capacity in entries (max over tiles, incl. alignment slack)
     int32_t smem_stage = 0;       // bytes of one stage
+    const double* vtab = nullptr; // value-indexed storage (<= 256 distinct values): 1-byte indices,
+    const uint8_t* vi8 = nullptr; // padded by 16; the table in shared memory; val unused
 };
 
 template <bool STREAM, class Op, bool F32 = false>
@@ -513,12 +573,19 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(2)) csr_tma(CsrTma A,
     pdl_wait();
     if (gated(gate)) return;
     op.prepare();
-    extern __shared__ __align__(128) unsigned char smem[];
-    // stage layout: val[tile_ent] | col[tile_ent] | ptr[kTcRows + 8]; barriers after the stages
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    // layout: [value table] stages { val[tile_ent] (VB bytes or 1-byte indices) | col[tile_ent] |
+    // ptr[kTcRows + 8] }; barriers after the stages
+    const bool vix = !F32 && A.vi8 != nullptr;
+    double* vtab_s = reinterpret_cast<double*>(smem_raw);
+    unsigned char* smem = smem_raw + (vix ? kVTabBytes : 0);
+    const int vbytes = vix ? 1 : VB;
     const int te = A.tile_ent;
     const size_t sb = (size_t)A.smem_stage;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTmaStages * sb);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (vix)
+        for (int k = threadIdx.x; k < 256; k += blockDim.x) vtab_s[k] = __ldg(A.vtab + k);
     if (threadIdx.x == 0) {
         for (int s = 0; s < kTmaStages; ++s) {
             mbar_init(smem_u32(bars + s), 1);
@@ -543,21 +610,24 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(2)) csr_tma(CsrTma A,
                 const int64_t r0 = t * kTcRows;
                 const int64_t r1 = r0 + kTcRows < A.nrows ? r0 + kTcRows : A.nrows;
                 const int32_t e0 = A.ptr[r0], e1 = A.ptr[r1];
-                const int32_t va = e0 & ~(VA - 1), ca = e0 & ~3;
-                const uint32_t nv = (uint32_t)(((e1 - va) + VA - 1) & ~(VA - 1));
+                const int32_t vau = vix ? 16 : VA;  // value alignment unit (entries)
+                const int32_t va = e0 & ~(vau - 1), ca = e0 & ~3;
+                const uint32_t nv = (uint32_t)(((e1 - va) + vau - 1) & ~(vau - 1));
                 const uint32_t nc = (uint32_t)(((e1 - ca) + 3) & ~3);
                 const uint32_t np = (uint32_t)(((r1 - r0 + 1) + 3) & ~3);
                 const uint32_t full = smem_u32(bars + s);
                 unsigned char* st = smem + (size_t)s * sb;
-                mbar_expect_tx(full, nv * (uint32_t)VB + nc * 4u + np * 4u);
+                mbar_expect_tx(full, nv * (uint32_t)vbytes + nc * 4u + np * 4u);
                 if (nv) {
-                    if constexpr (F32)
+                    if (vix)
+                        bulk_g2s<STREAM>(smem_u32(st), A.vi8 + va, nv, full, policy);
+                    else if constexpr (F32)
                         bulk_g2s<STREAM>(smem_u32(st), A.valf + va, nv * 4u, full, policy);
                     else
                         bulk_g2s<STREAM>(smem_u32(st), A.val + va, nv * 8u, full, policy);
                 }
-                if (nc) bulk_g2s<STREAM>(smem_u32(st + (size_t)te * VB), A.col + ca, nc * 4u, full, policy);
-                bulk_g2s<STREAM>(smem_u32(st + (size_t)te * (VB + 4)), A.ptr + r0, np * 4u, full, policy);
+                if (nc) bulk_g2s<STREAM>(smem_u32(st + (size_t)te * vbytes), A.col + ca, nc * 4u, full, policy);
+                bulk_g2s<STREAM>(smem_u32(st + (size_t)te * (vbytes + 4)), A.ptr + r0, np * 4u, full, policy);
             }
         }
     } else {  // ------------------------------------ consumer warps
@@ -572,12 +642,14 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(2)) csr_tma(CsrTma A,
                 if (has_row) rr = op.load(row);  // in flight during the wait
             mbar_wait(smem_u32(bars + s), (i / kTmaStages) & 1);
             const unsigned char* st = smem + (size_t)s * sb;
-            const int32_t* sp = reinterpret_cast<const int32_t*>(st + (size_t)te * (VB + 4));
+            const int32_t* sp = reinterpret_cast<const int32_t*>(st + (size_t)te * (vbytes + 4));
             const int32_t e0 = sp[0];
             const VT* sv = reinterpret_cast<const VT*>(st) - (e0 & ~(VA - 1));
-            const int32_t* sc = reinterpret_cast<const int32_t*>(st + (size_t)te * VB) - (e0 & ~3);
+            const uint8_t* si = st - (e0 & ~15);
+            const int32_t* sc = reinterpret_cast<const int32_t*>(st + (size_t)te * vbytes) - (e0 & ~3);
             acc_t<Op> sum{};
-            if (has_row) {
+            auto run = [&](auto vx) {
+                constexpr bool VX = decltype(vx)::value;
                 const int32_t pb = sp[warp * 32 + lane], pe = sp[warp * 32 + lane + 1];
                 for (int32_t k0 = pb; k0 < pe; k0 += UN) {
                     acc_t<Op> xv[UN];
@@ -587,9 +659,20 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(2)) csr_tma(CsrTma A,
 #pragma unroll
                     for (int u = 0; u < UN; ++u) xv[u] = (k0 + u < pe) ? op.gather(c[u]) : acc_t<Op>{};
 #pragma unroll
-                    for (int u = 0; u < UN; ++u)
-                        if (k0 + u < pe) fma_acc(sum, (double)sv[k0 + u], xv[u]);
+                    for (int u = 0; u < UN; ++u) {
+                        if constexpr (VX) {
+                            if (k0 + u < pe) fma_acc(sum, vtab_s[si[k0 + u]], xv[u]);
+                        } else {
+                            if (k0 + u < pe) fma_acc(sum, (double)sv[k0 + u], xv[u]);
+                        }
+                    }
                 }
+            };
+            if (has_row) {
+                if (vix)
+                    run(std::true_type{});
+                else
+                    run(std::false_type{});
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(bars + kTmaStages + s));  // stage free

@@ -372,3 +372,38 @@ def test_batched_columns_match_oracle(gen, n, kw, k, monkeypatch):
         if iters[j] != oc["iters"]:  # compare at equal iteration count (§8c)
             oc = oracle.cg(A, F[j], tol=0.0, maxiter=int(iters[j]), hier=hier)
         assert np.linalg.norm(Xh[j] - oc["x"]) <= 1e-8 * np.linalg.norm(oc["x"]), j
+
+
+@pytest.mark.parametrize("gen,n,kw", [("poisson", 48, {}), ("convdiff", 48, {"relax": "damped_jacobi",
+                                                                             "solver": "bicgstab"}),
+                                      ("poisson", 41, {"AMGB_FORMAT": "sell"})])
+def test_value_indexed_store_is_bitwise_the_plain_store(gen, n, kw, monkeypatch):
+    """Value-indexed storage (a table of the distinct values + 1- or 2-byte
+    indices, amgb.cu value_index) is lossless: every level op, the V-cycle and the
+    whole solve are bitwise those of the fp64-array store (AMGB_NO_VIDX=1)."""
+    for k in ("AMGB_FORMAT", "AMGB_NO_DICT", "AMGB_NO_VIDX"):
+        monkeypatch.delenv(k, raising=False)
+    kw = dict(kw)
+    if "AMGB_FORMAT" in kw:
+        monkeypatch.setenv("AMGB_FORMAT", kw.pop("AMGB_FORMAT"))
+    p, c, v, f = synth.problem(gen, n)
+    hv = amgb.setup(p, c, v, **kw)
+    monkeypatch.setenv("AMGB_NO_VIDX", "1")
+    hp = amgb.setup(p, c, v, **kw)
+    i0 = hv.level_info(0)
+    assert i0["vidx_A"] == 1 and hp.level_info(0)["vidx_A"] == 0  # constant coefficients: <= 256 values
+    assert i0["dev_bytes"] < hp.level_info(0)["dev_bytes"]
+    rng = np.random.default_rng(5)
+    for l in range(hv.nlevels - 1):
+        inf = hv.level_info(l)
+        x = dev(rng.standard_normal(inf["rows"]))
+        e = dev(rng.standard_normal(inf["cols_P"]))
+        for op, vin, ny in ((amgb.OP_SPMV_A, x, inf["rows"]), (amgb.OP_SPMV_P, e, inf["rows"]),
+                            (amgb.OP_SPMV_R, x, inf["cols_P"])):
+            assert np.array_equal(host(hv.level_op(l, op, x=vin, ny=ny)), host(hp.level_op(l, op, x=vin, ny=ny)))
+    r = dev(synth.random_vector(len(f)))
+    assert np.array_equal(host(hv.precond(r)), host(hp.precond(r)))
+    xv, itv, relv, stv = hv.solve(dev(f), tol=1e-8, maxiter=200)
+    xp, itp, relp, stp = hp.solve(dev(f), tol=1e-8, maxiter=200)
+    assert stv == stp == amgb.OK and itv == itp and relv == relp
+    assert np.array_equal(host(xv), host(xp))
