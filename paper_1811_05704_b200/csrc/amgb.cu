@@ -2676,7 +2676,8 @@ bool sigma_sort(const Csr& A, std::vector<uint8_t>& rp, Csr& B) {
 // exactly the stored values, and results are bitwise those of the plain store.
 // Smoothed-aggregation hierarchies of constant-coefficient operators qualify
 // (256^3 Poisson: A0 has 2 distinct values, P0 / R0 9, A1 2641 -> 16-bit);
-// log-random coefficients do not.  AMGB_NO_VIDX=1 disables it.
+// log-random coefficients do not.  Opt-in (AMGB_VIDX=1): the level-0 passes are
+// not limited by their matrix bytes once those are TMA-staged.
 __global__ void k_vidx(int64_t n, const unsigned long long* __restrict__ v, const unsigned long long* __restrict__ tab,
                        int32_t ntab, uint8_t* i8, uint16_t* i16) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
@@ -2698,7 +2699,8 @@ __global__ void k_vidx(int64_t n, const unsigned long long* __restrict__ v, cons
 bool value_index(Handle& H, const double* dval, int64_t n, int64_t pad, int64_t max_u, const double** tab,
                  const uint8_t** i8, const uint16_t** i16) {
     *tab = nullptr, *i8 = nullptr, *i16 = nullptr;
-    if (n <= 0 || std::getenv("AMGB_NO_VIDX")) return false;
+    const char* ve = std::getenv("AMGB_VIDX");  // opt-in: measured no faster
+    if (n <= 0 || !(ve && ve[0] == '1')) return false;
     DevTmp tmp;
     auto* keys = tmp.get<unsigned long long>(n);
     auto* sorted = tmp.get<unsigned long long>(n);

@@ -1,4 +1,8 @@
-"""Small runs of every device path, for compute-sanitizer (memcheck/racecheck)."""
+"""Small runs of every device path, for compute-sanitizer (memcheck / racecheck /
+synccheck / initcheck): GPU setup incl. device aggregation, TMA (dictionary, value
+index), TMA-CSR, SELL (8- and 16-bit value index), row-block CSR, the fused level
+ops, batched, mixed precision, BiCGStab / GMRES / IDR(s), Chebyshev, virtual ranks
+(split passes), host formats."""
 import os
 import sys
 
@@ -21,6 +25,23 @@ X, its, rels, st = h.solve_batched(torch.stack([dev(f)] * 8), tol=1e-8)
 print("batched8", list(its), st)
 hm = amgb.setup(p, c, v, coarse_enough=300, precision="mixed")
 print("mixed", hm.solve(dev(f), tol=1e-8)[1:])
+# the fused production kernels one launch each (amg_level_op_ex)
+n0 = len(f)
+fv = dev(np.linspace(1.0, 2.0, n0))
+y, y2, y3 = (torch.empty(n0, dtype=torch.float64, device="cuda") for _ in range(3))
+h.level_op_ex(0, amgb.OP_RES0, in0=fv, out0=y)
+h.level_op_ex(0, amgb.OP_RELAX_RHO, in0=fv, in1=fv, out0=y)
+h.level_op_ex(0, amgb.OP_CG_DIR, in0=fv, in1=fv, out0=y, out1=y2, scalar=0.5)
+h.level_op_ex(0, amgb.OP_CG_UPDATE, in0=fv, in1=fv, out0=y, out1=y2, out2=y3, scalar=0.5)
+print("level ops", h.level_info(0)["formats"])
+# every format forced: TMA-CSR everywhere, SELL everywhere (16-bit value indices on level 1)
+os.environ["AMGB_VIDX"] = "1"
+for fmt in ("tmacsr", "sell", "tma"):
+    os.environ["AMGB_FORMAT"] = fmt
+    hf = amgb.setup(p, c, v, coarse_enough=300)
+    print(fmt, hf.solve(dev(f), tol=1e-8)[1:], [hf.level_info(l)["formats"] for l in range(hf.nlevels)])
+os.environ.pop("AMGB_FORMAT")
+os.environ.pop("AMGB_VIDX")
 # non-symmetric: BiCGStab, GMRES, IDR(s)
 p2, c2, v2, f2 = synth.problem("convdiff", 16)
 for solver, extra in (("bicgstab", {}), ("gmres", {}), ("idrs", {"idrs_s": 4})):

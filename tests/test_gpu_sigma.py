@@ -60,11 +60,12 @@ def level_ops_equal(ha, hb):
             assert np.array_equal(ya, yb), (l, op)
 
 
-# 48^3: P0 (TMA format) has rows of 1..6 entries -> sorted; 41^3: the last
-# 256-row window is ragged (68921 rows).  fmt forces SELL-32 / TMA on every
-# level, so the sorted layout runs in both kernels on A, P and R (a forced TMA
-# format falls back to SELL-32 for rows too wide for its shared-memory stages).
-@pytest.mark.parametrize("n,fmt", [(48, None), (41, None), (41, "sell"), (30, "sell"), (30, "tma")])
+# 48^3: P0 has rows of 1..6 entries -> sorted; 41^3: the last 256-row window
+# is ragged (68921 rows).  fmt forces SELL-32 / TMA on every level, so the
+# sorted layout runs in both kernels on A, P and R (a forced TMA format falls
+# back to SELL-32 for rows too wide for its shared-memory stages; the default
+# policy stores P0 padding-free in the TMA-CSR format, which needs no sorting).
+@pytest.mark.parametrize("n,fmt", [(48, "tma"), (41, "tma"), (41, "sell"), (30, "sell"), (30, "tma")])
 def test_sigma_bitwise_equal(n, fmt):
     p, c, v, f = synth.problem("poisson", n)
     hs, hp = setup_pair(p, c, v, fmt=fmt, coarse_enough=200)
@@ -107,7 +108,7 @@ def test_sigma_bitwise_equal_variants(kw):
 @pytest.mark.parametrize("k", [2, 4, 8])
 def test_sigma_batched(k):
     p, c, v, f = synth.problem("poisson", 44)
-    hs, hp = setup_pair(p, c, v, coarse_enough=200)  # P0 sorted in the TMA format
+    hs, hp = setup_pair(p, c, v, fmt="tma", coarse_enough=200)  # P0 sorted in the TMA format
     assert hs.level_info(0)["sigma_mask"] & 2
     F = torch.stack([dev(f * (1.0 + 0.25 * j)) if j % 2 == 0 else dev(synth.random_vector(len(f)))
                      for j in range(k)])
