@@ -507,19 +507,52 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sel
                     }
                 }
             };
+            // slices of exactly W entries (the 7-point stencil: W = 7, 6 on a
+            // boundary plane): fully unrolled, no per-entry predicates (T = 1)
+            auto run_w = [&](auto wc, auto cs, int32_t cbase, auto vx) {
+                constexpr int W = decltype(wc)::value;
+                constexpr int CS = decltype(cs)::value;
+                constexpr bool VX = decltype(vx)::value;
+                int32_t c[W];
+                acc_t<Op> xv[W];
+#pragma unroll
+                for (int u = 0; u < W; ++u) c[u] = sc[CS * u] + cbase;
+#pragma unroll
+                for (int u = 0; u < W; ++u) xv[u] = op.gather(c[u]);
+#pragma unroll
+                for (int u = 0; u < W; ++u) {
+                    if constexpr (VX)
+                        fma_acc(sum, vtab_s[si[C * u]], xv[u]);
+                    else
+                        fma_acc(sum, (double)sv[C * u], xv[u]);
+                }
+            };
             using one = std::integral_constant<int, 1>;
             using cc = std::integral_constant<int, C>;
-            if (vix) {
+            using w7 = std::integral_constant<int, 7>;
+            using w6 = std::integral_constant<int, 6>;
+            auto dispatch = [&](auto vx) {
+                if constexpr (T == 1) {
+                    if (w == 7) {
+                        if (dict) run_w(w7{}, one{}, (int32_t)row, vx);
+                        else run_w(w7{}, cc{}, 0, vx);
+                        return;
+                    }
+                    if (w == 6) {
+                        if (dict) run_w(w6{}, one{}, (int32_t)row, vx);
+                        else run_w(w6{}, cc{}, 0, vx);
+                        return;
+                    }
+                }
                 if (dict)
-                    run(one{}, (int32_t)row, std::true_type{});
+                    run(one{}, (int32_t)row, vx);
                 else
-                    run(cc{}, 0, std::true_type{});
-            } else {
-                if (dict)
-                    run(one{}, (int32_t)row, std::false_type{});
-                else
-                    run(cc{}, 0, std::false_type{});
-            }
+                    run(cc{}, 0, vx);
+            };
+            if (vix)
+                dispatch(std::true_type{});
+            else
+                dispatch(std::false_type{});
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(bars + kTmaStages + s));  // stage free
             if constexpr (T > 1) {
