@@ -764,7 +764,8 @@ struct Handle {
         auto kern = sell_tma<T, STREAM, Op, F32>;
         const bool vix = !F32 && M.vi8 != nullptr;
         const size_t smem =
-            (vix ? kVTabBytes : 0) + (size_t)kTmaStages * M.tile_ent * (vix ? 5 : F32 ? 8 : 12) + 2 * kTmaStages * 8;
+            (vix ? kVTabBytes : 0) +
+            (size_t)kTmaStages * (kTmaDescBytes + (size_t)M.tile_ent * (vix ? 5 : F32 ? 8 : 12)) + 2 * kTmaStages * 8;
         static size_t configured = 0;  // per instantiation
         if (smem > configured) {
             ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
@@ -2438,7 +2439,8 @@ Fmt pick_format(const Csr& A) {
     for (int64_t r = 0; r < A.nrows; ++r) lmax = std::max<int64_t>(lmax, A.ptr[r + 1] - A.ptr[r]);
     // a TMA stage holds a tile of 8 slices x 32 rows x (longest row) entries at
     // 12 B, kTmaStages of them must fit the 227 KB of shared memory per CTA
-    const bool tma_fits = (int64_t)kTmaStages * 256 * 12 * std::max<int64_t>(lmax, 1) + 64 <= 227 * 1024;
+    const bool tma_fits =
+        (int64_t)kTmaStages * (256 * 12 * std::max<int64_t>(lmax, 1) + kTmaDescBytes) + kVTabBytes + 64 <= 227 * 1024;
     const bool tcsr_fits = A.nrows > 0 && A.nnz() < INT32_MAX &&
                            (int64_t)kTmaStages * (int64_t)tcsr_stage_bytes(tcsr_tile_ent(A), false) + 64 <= 227 * 1024;
     if (f == "tma") return tma_fits ? Fmt::TMA : Fmt::SELL;
@@ -2676,8 +2678,8 @@ bool sigma_sort(const Csr& A, std::vector<uint8_t>& rp, Csr& B) {
 // exactly the stored values, and results are bitwise those of the plain store.
 // Smoothed-aggregation hierarchies of constant-coefficient operators qualify
 // (256^3 Poisson: A0 has 2 distinct values, P0 / R0 9, A1 2641 -> 16-bit);
-// log-random coefficients do not.  Opt-in (AMGB_VIDX=1): the level-0 passes are
-// not limited by their matrix bytes once those are TMA-staged.
+// log-random coefficients do not.  On by default (256^3 Poisson: 35.5 vs 40.3 ms
+// per solve); AMGB_VIDX=0 turns it off.
 __global__ void k_vidx(int64_t n, const unsigned long long* __restrict__ v, const unsigned long long* __restrict__ tab,
                        int32_t ntab, uint8_t* i8, uint16_t* i16) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
@@ -2699,8 +2701,8 @@ __global__ void k_vidx(int64_t n, const unsigned long long* __restrict__ v, cons
 bool value_index(Handle& H, const double* dval, int64_t n, int64_t pad, int64_t max_u, const double** tab,
                  const uint8_t** i8, const uint16_t** i16) {
     *tab = nullptr, *i8 = nullptr, *i16 = nullptr;
-    const char* ve = std::getenv("AMGB_VIDX");  // opt-in: measured no faster
-    if (n <= 0 || !(ve && ve[0] == '1')) return false;
+    const char* ve = std::getenv("AMGB_VIDX");  // default on; AMGB_VIDX=0 keeps fp64 value arrays
+    if (n <= 0 || (ve && ve[0] == '0')) return false;
     DevTmp tmp;
     auto* keys = tmp.get<unsigned long long>(n);
     auto* sorted = tmp.get<unsigned long long>(n);

@@ -4,7 +4,7 @@ OUT=gpurun_out/${TAG:-ncuv}; mkdir -p $OUT
 export AMGB_NO_DEVICE_LOOP=1
 PCMD="python scripts/profile_solve.py --solves 2"
 for v in vidx novidx; do
-  if [ $v = vidx ]; then export AMGB_VIDX=1; else unset AMGB_VIDX; fi
+  if [ $v = vidx ]; then unset AMGB_VIDX; else export AMGB_VIDX=0; fi
   $PCMD > $OUT/plain_$v.log 2>&1 && \
   ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:sell_tma.*OpRelax" -s 30 -c 2 -o $OUT/prof_$v $PCMD > $OUT/ncu_$v.log 2>&1
   echo "ncu $v rc=$?"

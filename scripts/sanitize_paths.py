@@ -35,12 +35,13 @@ h.level_op_ex(0, amgb.OP_CG_DIR, in0=fv, in1=fv, out0=y, out1=y2, scalar=0.5)
 h.level_op_ex(0, amgb.OP_CG_UPDATE, in0=fv, in1=fv, out0=y, out1=y2, out2=y3, scalar=0.5)
 print("level ops", h.level_info(0)["formats"])
 # every format forced: TMA-CSR everywhere, SELL everywhere (16-bit value indices on level 1)
-os.environ["AMGB_VIDX"] = "1"
 for fmt in ("tmacsr", "sell", "tma"):
     os.environ["AMGB_FORMAT"] = fmt
     hf = amgb.setup(p, c, v, coarse_enough=300)
     print(fmt, hf.solve(dev(f), tol=1e-8)[1:], [hf.level_info(l)["formats"] for l in range(hf.nlevels)])
 os.environ.pop("AMGB_FORMAT")
+os.environ["AMGB_VIDX"] = "0"  # the fp64-array stores
+print("fp64 arrays", amgb.setup(p, c, v, coarse_enough=300).solve(dev(f), tol=1e-8)[1:])
 os.environ.pop("AMGB_VIDX")
 # non-symmetric: BiCGStab, GMRES, IDR(s)
 p2, c2, v2, f2 = synth.problem("convdiff", 16)

@@ -378,18 +378,17 @@ def test_batched_columns_match_oracle(gen, n, kw, k, monkeypatch):
                                                                              "solver": "bicgstab"}),
                                       ("poisson", 41, {"AMGB_FORMAT": "sell"})])
 def test_value_indexed_store_is_bitwise_the_plain_store(gen, n, kw, monkeypatch):
-    """Value-indexed storage (AMGB_VIDX=1: a table of the distinct values + 1- or
+    """Value-indexed storage (the default: a table of the distinct values + 1- or
     2-byte indices, amgb.cu value_index) is lossless: every level op, the V-cycle
-    and the whole solve are bitwise those of the fp64-array store (the default)."""
+    and the whole solve are bitwise those of the fp64-array store (AMGB_VIDX=0)."""
     for k in ("AMGB_FORMAT", "AMGB_NO_DICT", "AMGB_VIDX"):
         monkeypatch.delenv(k, raising=False)
     kw = dict(kw)
     if "AMGB_FORMAT" in kw:
         monkeypatch.setenv("AMGB_FORMAT", kw.pop("AMGB_FORMAT"))
     p, c, v, f = synth.problem(gen, n)
-    monkeypatch.setenv("AMGB_VIDX", "1")  # opt-in
-    hv = amgb.setup(p, c, v, **kw)
-    monkeypatch.delenv("AMGB_VIDX")
+    hv = amgb.setup(p, c, v, **kw)  # the default
+    monkeypatch.setenv("AMGB_VIDX", "0")
     hp = amgb.setup(p, c, v, **kw)
     i0 = hv.level_info(0)
     assert i0["vidx_A"] == 1 and hp.level_info(0)["vidx_A"] == 0  # constant coefficients: <= 256 values
