@@ -536,6 +536,9 @@ def main():
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "traffic_source": traffic_src,
                 "kernel": "level-0 A-pass kernels (one kernel template on A0 in the format pick_format chose: sell_tma at 256^3; res0 / relax+rho / cg-dir+sigma / initial and true residual)",
+                "store": "A0 %s values, %s column indices (bytes_per_launch counts what this store moves)" % (
+                    {0: "fp64", 1: "8-bit indexed", 2: "16-bit indexed"}[infos[0].get("vidx_A", 0)],
+                    "offset-dictionary" if infos[0]["dict_slices_A"] else "explicit"),
                 "launches_timed": prof_launch, "bytes_per_launch": prof_bytes / max(prof_launch, 1),
                 "ms_per_launch": prof_ms / max(prof_launch, 1), "peak_source": peak_src,
                 "timed_in": "a second timed region of the same K solves with CUDA-event record nodes "

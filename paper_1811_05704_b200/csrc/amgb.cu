@@ -764,8 +764,7 @@ struct Handle {
         auto kern = sell_tma<T, STREAM, Op, F32>;
         const bool vix = !F32 && M.vi8 != nullptr;
         const size_t smem =
-            (vix ? kVTabBytes : 0) +
-            (size_t)kTmaStages * (kTmaDescBytes + (size_t)M.tile_ent * (vix ? 5 : F32 ? 8 : 12)) + 2 * kTmaStages * 8;
+            (vix ? kVTabBytes : 0) + (size_t)kTmaStages * M.tile_ent * (vix ? 5 : F32 ? 8 : 12) + 2 * kTmaStages * 8;
         static size_t configured = 0;  // per instantiation
         if (smem > configured) {
             ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
@@ -2440,7 +2439,7 @@ Fmt pick_format(const Csr& A) {
     // a TMA stage holds a tile of 8 slices x 32 rows x (longest row) entries at
     // 12 B, kTmaStages of them must fit the 227 KB of shared memory per CTA
     const bool tma_fits =
-        (int64_t)kTmaStages * (256 * 12 * std::max<int64_t>(lmax, 1) + kTmaDescBytes) + kVTabBytes + 64 <= 227 * 1024;
+        (int64_t)kTmaStages * 256 * 12 * std::max<int64_t>(lmax, 1) + kVTabBytes + 64 <= 227 * 1024;
     const bool tcsr_fits = A.nrows > 0 && A.nnz() < INT32_MAX &&
                            (int64_t)kTmaStages * (int64_t)tcsr_stage_bytes(tcsr_tile_ent(A), false) + 64 <= 227 * 1024;
     if (f == "tma") return tma_fits ? Fmt::TMA : Fmt::SELL;

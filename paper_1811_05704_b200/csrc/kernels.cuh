@@ -347,8 +347,6 @@ struct SellTma {
 
 // shared-memory bytes of the value table of an indexed TMA store
 constexpr int kVTabBytes = 256 * 8;
-// per-stage header of sell_tma: one int4 descriptor per slice of the tile
-constexpr int kTmaDescBytes = 8 * 16;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -412,10 +410,8 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sel
     unsigned char* smem = smem_raw + (vix ? kVTabBytes : 0);
     const int vbytes = vix ? 1 : VB;
     const int te = A.tile_ent;
-    // stage: [NS slice descriptors (int4)] values | columns
-    const size_t stage_bytes = kTmaDescBytes + (size_t)te * (vbytes + 4);
+    const size_t stage_bytes = (size_t)te * (vbytes + 4);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTmaStages * stage_bytes);  // full[S], empty[S]
-    const uint32_t bar_full0 = smem_u32(bars), bar_empty0 = smem_u32(bars + kTmaStages);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (vix)
         for (int k = threadIdx.x; k < 256; k += blockDim.x) vtab_s[k] = __ldg(A.vtab + k);
@@ -433,46 +429,52 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sel
     for (int k = 0; k < ND; ++k) dots[k] = 0.0;
 
     if (warp == kBlock / 32) {  // ---------------- producer warp
-        // the whole warp reads the tile's slice offsets and writes one descriptor
-        // per slice (offset of its values / columns in the stage, width, offset
-        // dictionary flag) into the stage header; lane 0 issues the bulk copies
-        uint64_t policy = 0;
-        if constexpr (STREAM) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-        int i = 0;
-        for (int64_t t = blockIdx.x; t < A.ntiles; t += gridDim.x, ++i) {
-            const int s = i % kTmaStages;
-            if (i >= kTmaStages) mbar_wait(bar_empty0 + 8 * s, ((i / kTmaStages) & 1) ^ 1);
-            const int64_t s0 = t * NS;
-            const int64_t sl = s0 + (lane <= NS ? lane : NS) < A.nslices ? s0 + (lane <= NS ? lane : NS) : A.nslices;
-            const int64_t ep = A.sptr[sl], cp = A.cptr[sl];
-            const int64_t e0 = __shfl_sync(0xffffffffu, ep, 0), c0 = __shfl_sync(0xffffffffu, cp, 0);
-            const int64_t en = __shfl_down_sync(0xffffffffu, ep, 1), cn = __shfl_down_sync(0xffffffffu, cp, 1);
-            const int64_t e1 = __shfl_sync(0xffffffffu, ep, NS), c1 = __shfl_sync(0xffffffffu, cp, NS);
-            unsigned char* st = smem + (size_t)s * stage_bytes;
-            if (lane < NS) {
-                const int w = (int)((en - ep) / C);
-                const int dict = (cn - cp) < (int64_t)C * w ? 1 : 0;
-                reinterpret_cast<int4*>(st)[lane] = make_int4((int)(ep - e0), w, (int)(cp - c0), dict);
-                __threadfence_block();
-            }
-            __syncwarp();  // the descriptors precede lane 0's arrive (release) on the full barrier
-            if (lane == 0) {
+        if (lane == 0) {
+            uint64_t policy = 0;
+            if constexpr (STREAM) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+            int i = 0;
+            for (int64_t t = blockIdx.x; t < A.ntiles; t += gridDim.x, ++i) {
+                const int s = i % kTmaStages;
+                if (i >= kTmaStages) mbar_wait(smem_u32(bars + kTmaStages + s), ((i / kTmaStages) & 1) ^ 1);
+                const int64_t s0 = t * NS;
+                const int64_t s1 = s0 + NS < A.nslices ? s0 + NS : A.nslices;
+                const int64_t e0 = A.sptr[s0], e1 = A.sptr[s1];
+                const int64_t c0 = A.cptr[s0], c1 = A.cptr[s1];
                 const uint32_t n = (uint32_t)(e1 - e0), nc = (uint32_t)(c1 - c0);
-                const uint32_t full = bar_full0 + 8 * s;
-                unsigned char* sd = st + kTmaDescBytes;
+                const uint32_t full = smem_u32(bars + s);
+                unsigned char* st = smem + (size_t)s * stage_bytes;
                 mbar_expect_tx(full, n * (uint32_t)vbytes + nc * 4u);
                 if (vix)
-                    bulk_g2s<STREAM>(smem_u32(sd), A.vi8 + e0, n, full, policy);
+                    bulk_g2s<STREAM>(smem_u32(st), A.vi8 + e0, n, full, policy);
                 else if constexpr (F32)
-                    bulk_g2s<STREAM>(smem_u32(sd), A.valf + e0, n * 4u, full, policy);
+                    bulk_g2s<STREAM>(smem_u32(st), A.valf + e0, n * 4u, full, policy);
                 else
-                    bulk_g2s<STREAM>(smem_u32(sd), A.val + e0, n * 8u, full, policy);
-                if (nc) bulk_g2s<STREAM>(smem_u32(sd + (size_t)te * vbytes), A.col + c0, nc * 4u, full, policy);
+                    bulk_g2s<STREAM>(smem_u32(st), A.val + e0, n * 8u, full, policy);
+                if (nc) bulk_g2s<STREAM>(smem_u32(st + (size_t)te * vbytes), A.col + c0, nc * 4u, full, policy);
             }
         }
     } else {  // ------------------------------------ consumer warps
         const int r = lane % C;  // row within the slice
         const int pt = lane / C; // part of the row
+        // this warp's slice offsets of the next tile are loaded one tile ahead,
+        // so their latency is off the critical path
+        struct SliceOff {
+            int64_t e0 = 0, e1 = 0, eb = 0, c0 = 0, c1 = 0, cb = 0;
+        };
+        auto load_off = [&](int64_t t) {
+            SliceOff o;
+            const int64_t slice = t * NS + warp;
+            if (t < A.ntiles && slice < A.nslices) {
+                o.e0 = A.sptr[slice];
+                o.e1 = A.sptr[slice + 1];
+                o.eb = A.sptr[t * NS];
+                o.c0 = A.cptr[slice];
+                o.c1 = A.cptr[slice + 1];
+                o.cb = A.cptr[t * NS];
+            }
+            return o;
+        };
+        SliceOff nxt = load_off(blockIdx.x);
         int i = 0;
         for (int64_t t = blockIdx.x; t < A.ntiles; t += gridDim.x, ++i) {
             const int s = i % kTmaStages;
@@ -485,15 +487,21 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sel
             typename Op::Row rr{};
             if constexpr (cols_of<Op>() == 1)
                 if (pt == 0 && has_row) rr = op.load(row);  // in flight during the wait
-            mbar_wait(bar_full0 + 8 * s, (i / kTmaStages) & 1);
-            const unsigned char* st = smem + (size_t)s * stage_bytes;
-            const int4 d = reinterpret_cast<const int4*>(st)[warp];  // this slice's descriptor
-            const int off = d.x, w = d.y, coff = d.z;
-            const bool dict = d.w != 0;  // the slice's columns are row + a shared offset list
-            const unsigned char* sd = st + kTmaDescBytes;
-            const VT* sv = reinterpret_cast<const VT*>(sd) + off + r;
-            const uint8_t* si = sd + off + r;
-            const int32_t* sc = reinterpret_cast<const int32_t*>(sd + (size_t)te * vbytes) + coff + (dict ? 0 : r);
+            const SliceOff cur = nxt;
+            nxt = load_off(t + gridDim.x);
+            int off = 0, w = 0, coff = 0;
+            bool dict = false;  // the slice's columns are row + a shared offset list
+            if (slice < A.nslices) {
+                off = (int)(cur.e0 - cur.eb);
+                w = (int)((cur.e1 - cur.e0) / C);
+                coff = (int)(cur.c0 - cur.cb);
+                dict = cur.c1 - cur.c0 < (int64_t)C * w;
+            }
+            mbar_wait(smem_u32(bars + s), (i / kTmaStages) & 1);
+            const VT* sv = reinterpret_cast<const VT*>(smem + (size_t)s * stage_bytes) + off + r;
+            const uint8_t* si = smem + (size_t)s * stage_bytes + off + r;
+            const int32_t* sc = reinterpret_cast<const int32_t*>(smem + (size_t)s * stage_bytes + (size_t)te * vbytes) +
+                                coff + (dict ? 0 : r);
             acc_t<Op> sum{};
             // entry k's column: sc[CS k] (+ row for a dictionary slice); the
             // stride is a template constant so every load is an immediate offset;
@@ -569,7 +577,7 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sel
             else
                 dispatch(std::false_type{});
             __syncwarp();
-            if (lane == 0) mbar_arrive(bar_empty0 + 8 * s);  // stage free
+            if (lane == 0) mbar_arrive(smem_u32(bars + kTmaStages + s));  // stage free
             if constexpr (T > 1) {
 #pragma unroll
                 for (int o = C; o < 32; o <<= 1) add_acc(sum, shfl_xor_acc(0xffffffffu, sum, o));
