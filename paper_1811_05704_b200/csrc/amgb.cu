@@ -555,6 +555,14 @@ struct Handle {
         const char* e = std::getenv("AMGB_PDL");
         return e && std::string(e) == "1";
     }();
+    // PDL pays only where every pass is a few microseconds of launch-latency-bound
+    // work: measured 0.72 vs 0.77 ms per 32^3 solve, but 8.4 vs 7.5 ms at 150^3 and
+    // 41.5 vs 35.7 ms at 256^3 (profiles/r02_misc).  On by default for hierarchies
+    // whose finest level has fewer than 65,536 rows; AMGB_PDL=0 / 1 forces it.
+    void choose_pdl(int64_t n0) {
+        const char* e = std::getenv("AMGB_PDL");
+        pdl = e ? std::string(e) == "1" : n0 < 65536;
+    }
     template <class... KArgs, class... Args>
     void klaunch(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, Args&&... args) {
         cudaLaunchConfig_t cfg = {};
@@ -781,9 +789,20 @@ struct Handle {
         else
             rows_tma_impl<T, false, F32>(M, op, gate, red);
     }
+    int tcsr_un = [] {
+        const char* e = std::getenv("AMGB_TCSR_UN");
+        return e && e[0] == '8' ? 8 : 4;
+    }();
     template <bool STREAM, bool F32, class Op>
     void rows_tcsr_impl(const CsrTma& M, const Op& op, const int32_t* gate, const Red& red) {
-        auto kern = csr_tma<STREAM, Op, F32>;
+        if (tcsr_un == 8)
+            rows_tcsr_un<STREAM, F32, 8>(M, op, gate, red);
+        else
+            rows_tcsr_un<STREAM, F32, 4>(M, op, gate, red);
+    }
+    template <bool STREAM, bool F32, int UN1, class Op>
+    void rows_tcsr_un(const CsrTma& M, const Op& op, const int32_t* gate, const Red& red) {
+        auto kern = csr_tma<STREAM, Op, F32, UN1>;
         CsrTma m = M;
         const bool vix = !F32 && M.vi8 != nullptr;
         m.smem_stage = (int32_t)tcsr_stage_bytes(M.tile_ent, F32, vix);
@@ -2797,33 +2816,40 @@ DMat upload_mat_impl(Handle& H, const Csr& A0, int64_t* bytes, bool f32) {
         *bytes += (int64_t)(ptr32.size() * 4 + A.col.size() * 12 + blocks.size() * 4);
         return d;
     }
-    if (d.fmt == Fmt::TMACSR) {  // CSR with padded arrays (csr_tma reads 16-B aligned ranges)
+    if (d.fmt == Fmt::TMACSR) {  // CSR with padded arrays (csr_tma reads 16-B aligned ranges), built on the device
         const int64_t n = A.nrows, nnz = A.nnz();
-        std::vector<int32_t> p32(n + 1 + 8);
-        for (int64_t i = 0; i <= n; ++i) p32[i] = (int32_t)A.ptr[i];
-        for (int64_t i = n + 1; i < n + 9; ++i) p32[i] = (int32_t)nnz;
-        hvec<int32_t> col(nnz + 4);
-        hvec<double> val(nnz + 2);
-        std::copy(A.col.begin(), A.col.end(), col.begin());
-        std::copy(A.val.begin(), A.val.end(), val.begin());
-        for (int k = 0; k < 4; ++k) col[nnz + k] = 0;
-        val[nnz] = val[nnz + 1] = 0.0;
+        DevTmp tmp;
+        int64_t* p64 = tmp.get<int64_t>(n + 1);
+        ck(cudaMemcpy(p64, A.ptr.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice), "H2D ptr");
+        int32_t* p32 = H.talloc<int32_t>(n + 1 + 8);
+        cv_ptr32<<<cv_grid(n + 1), 256>>>(n + 1, p64, p32);
+        const std::vector<int32_t> tailp(8, (int32_t)nnz);  // readable past the last row
+        ck(cudaMemcpy(p32 + n + 1, tailp.data(), 8 * sizeof(int32_t), cudaMemcpyHostToDevice), "H2D ptr tail");
+        int32_t* col = H.talloc<int32_t>(nnz + 4);
+        double* val = H.talloc<double>(nnz + 2);
+        ck(cudaMemcpy(col, A.col.data(), nnz * sizeof(int32_t), cudaMemcpyHostToDevice), "H2D col");
+        ck(cudaMemcpy(val, A.val.data(), nnz * sizeof(double), cudaMemcpyHostToDevice), "H2D val");
+        ck(cudaMemset(col + nnz, 0, 4 * sizeof(int32_t)), "memset");
+        ck(cudaMemset(val + nnz, 0, 2 * sizeof(double)), "memset");
         CsrTma& t = d.tcsr;
         t.nrows = n;
         t.ncols = A.ncols;
         t.ntiles = (n + kTcRows - 1) / kTcRows;
         t.tile_ent = (int32_t)tcsr_tile_ent(A);
-        t.ptr = H.upload(p32);
-        t.col = H.upload(col);
-        t.val = H.upload(val);
+        t.ptr = p32;
+        t.col = col;
+        t.val = val;
         if (f32) {
-            std::vector<float> vf(nnz + 4, 0.0f);
-            for (int64_t k = 0; k < nnz; ++k) vf[k] = (float)A.val[k];
-            t.valf = H.upload(vf);
+            float* vf = H.talloc<float>(nnz + 4);
+            ck(cudaMemset(vf, 0, (nnz + 4) * sizeof(float)), "memset");
+            cv_to_f32<<<cv_grid(nnz), 256>>>(nnz, val, vf);
+            t.valf = vf;
         }
+        ck(cudaGetLastError(), "convert");
         d.stored = nnz;
-        *bytes += (int64_t)(p32.size() * 4 + col.size() * 4 + val.size() * 8);
+        *bytes += (n + 9) * 4 + (nnz + 4) * 4 + (nnz + 2) * 8;
         if (!f32) index_store(H, d, bytes);
+        ck(cudaDeviceSynchronize(), "convert sync");
         return d;
     }
     // SELL / TMA: rows sorted by length inside 256-row windows when it pays
@@ -3355,6 +3381,7 @@ static void device_upload(amgb::Handle& H) {
         H.d_defer_ptrs = H.upload(ptrs);
     }
     ck(cudaMallocHost(&H.ks_host, sizeof(KState)), "cudaMallocHost");
+    H.choose_pdl(H.meta.empty() ? 0 : H.meta[0].rows);
     ck(cudaDeviceSynchronize(), "setup sync");
     if (H.reordered) {
         const int64_t n0 = H.parts[0].lv[0].n;

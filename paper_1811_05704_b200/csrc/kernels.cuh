@@ -619,13 +619,15 @@ struct CsrTma {
     const uint8_t* vi8 = nullptr; // padded by 16; the table in shared memory; val unused
 };
 
-template <bool STREAM, class Op, bool F32 = false>
+// UN1: entries per unrolled step for one right-hand side (P rows hold 1-6
+// entries: 4 wastes fewer predicated slots than 8; AMGB_TCSR_UN=8 for the other)
+template <bool STREAM, class Op, bool F32 = false, int UN1 = 4>
 __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(2)) csr_tma(CsrTma A, Op op, const int32_t* gate,
                                                                          Red red) {
     using VT = std::conditional_t<F32, float, double>;
     constexpr int VB = (int)sizeof(VT);
     constexpr int VA = 16 / VB;  // value alignment unit (entries)
-    constexpr int UN = unroll_of<Op>(8);
+    constexpr int UN = cols_of<Op>() == 1 ? UN1 : unroll_of<Op>(8);
     pdl_wait();
     if (gated(gate)) return;
     op.prepare();
