@@ -20,7 +20,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libamgb.so")
+LIB_PATH = os.environ.get("AMGB_LIB_PATH") or os.path.join(_HERE, "_lib", "libamgb.so")  # override: checked build
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -15,11 +15,22 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cassert>
 #include <cstdint>
 #include <type_traits>
 #include <utility>
 
 namespace amgb {
+
+// Bounds-checked build (make check -> _lib_chk/libamgb.so, -DAMGB_BOUNDS_CHECK):
+// every gathered column index and every TMA stage range is asserted on the
+// device (a failing assert aborts the kernel with cudaErrorAssert), in lieu of
+// compute-sanitizer, which is closed on this pool.
+#ifdef AMGB_BOUNDS_CHECK
+#define AMGB_ASSERT(c) assert(c)
+#else
+#define AMGB_ASSERT(c) ((void)0)
+#endif
 
 constexpr int kBlock = 256;  // threads per block of every kernel
 constexpr int kWarp = 32;
@@ -104,6 +115,13 @@ struct Vk {
 };
 template <class Op>
 using acc_t = decltype(std::declval<Op>().gather(0));
+// gather with the bounds check of the checked build (column in [0, ncols))
+template <class Op>
+__device__ __forceinline__ acc_t<Op> gather_chk(const Op& op, int32_t c, int64_t ncols) {
+    AMGB_ASSERT(c >= 0 && (int64_t)c < ncols);
+    (void)ncols;
+    return op.gather(c);
+}
 // columns carried by an op's accumulator (1 = single right-hand side)
 template <class Op>
 constexpr int cols_of() { return (int)(sizeof(acc_t<Op>) / sizeof(double)); }
@@ -259,7 +277,7 @@ __device__ __forceinline__ void sell_rows_body(const Sell& A, Op& op, double (&d
         if constexpr (!PIPE) {
             acc_t<Op> xv[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) xv[u] = u < w ? op.gather(c[u]) : acc_t<Op>{};
+            for (int u = 0; u < U; ++u) xv[u] = u < w ? gather_chk(op, c[u], A.ncols) : acc_t<Op>{};
 #pragma unroll
             for (int u = 0; u < U; ++u)
                 if (u < w) fma_acc(sum, v[u], xv[u]);
@@ -267,7 +285,7 @@ __device__ __forceinline__ void sell_rows_body(const Sell& A, Op& op, double (&d
         for (int k0 = 0; PIPE && k0 < w; k0 += U) {
             acc_t<Op> xv[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) xv[u] = (k0 + u < w) ? op.gather(c[u]) : acc_t<Op>{};
+            for (int u = 0; u < U; ++u) xv[u] = (k0 + u < w) ? gather_chk(op, c[u], A.ncols) : acc_t<Op>{};
             // software pipelining: the next chunk's entries are in flight while
             // this chunk's gathers complete
             int32_t cn[U];
@@ -441,6 +459,7 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sel
                 const int64_t e0 = A.sptr[s0], e1 = A.sptr[s1];
                 const int64_t c0 = A.cptr[s0], c1 = A.cptr[s1];
                 const uint32_t n = (uint32_t)(e1 - e0), nc = (uint32_t)(c1 - c0);
+                AMGB_ASSERT(e1 >= e0 && c1 >= c0 && n <= (uint32_t)te && nc <= (uint32_t)te);
                 const uint32_t full = smem_u32(bars + s);
                 unsigned char* st = smem + (size_t)s * stage_bytes;
                 mbar_expect_tx(full, n * (uint32_t)vbytes + nc * 4u);
@@ -518,7 +537,7 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sel
                         c[u] = k < w ? sc[CS * k] + cbase : 0;
                     }
 #pragma unroll
-                    for (int u = 0; u < UN; ++u) xv[u] = (k0 + u * T < w) ? op.gather(c[u]) : acc_t<Op>{};
+                    for (int u = 0; u < UN; ++u) xv[u] = (k0 + u * T < w) ? gather_chk(op, c[u], A.ncols) : acc_t<Op>{};
 #pragma unroll
                     for (int u = 0; u < UN; ++u) {
                         const int k = k0 + u * T;
@@ -541,7 +560,7 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sel
 #pragma unroll
                 for (int u = 0; u < W; ++u) c[u] = sc[CS * u] + cbase;
 #pragma unroll
-                for (int u = 0; u < W; ++u) xv[u] = op.gather(c[u]);
+                for (int u = 0; u < W; ++u) xv[u] = gather_chk(op, c[u], A.ncols);
 #pragma unroll
                 for (int u = 0; u < W; ++u) {
                     if constexpr (VX)
@@ -673,6 +692,7 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(2)) csr_tma(CsrTma A,
                 const uint32_t nv = (uint32_t)(((e1 - va) + vau - 1) & ~(vau - 1));
                 const uint32_t nc = (uint32_t)(((e1 - ca) + 3) & ~3);
                 const uint32_t np = (uint32_t)(((r1 - r0 + 1) + 3) & ~3);
+                AMGB_ASSERT(e1 >= e0 && nv <= (uint32_t)te && nc <= (uint32_t)te);
                 const uint32_t full = smem_u32(bars + s);
                 unsigned char* st = smem + (size_t)s * sb;
                 mbar_expect_tx(full, nv * (uint32_t)vbytes + nc * 4u + np * 4u);
@@ -715,7 +735,7 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(2)) csr_tma(CsrTma A,
 #pragma unroll
                     for (int u = 0; u < UN; ++u) c[u] = k0 + u < pe ? sc[k0 + u] : 0;
 #pragma unroll
-                    for (int u = 0; u < UN; ++u) xv[u] = (k0 + u < pe) ? op.gather(c[u]) : acc_t<Op>{};
+                    for (int u = 0; u < UN; ++u) xv[u] = (k0 + u < pe) ? gather_chk(op, c[u], A.ncols) : acc_t<Op>{};
 #pragma unroll
                     for (int u = 0; u < UN; ++u) {
                         if constexpr (VX) {
@@ -787,7 +807,7 @@ __global__ void __launch_bounds__(kBlock) csr_rows(CsrDev A, Op op, const int32_
         for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + tid) / G; r < A.nrows; r += groups) {
             acc_t<Op> s{};
             for (int k = A.ptr[r] + lig; k < A.ptr[r + 1]; k += G)
-                fma_acc(s, ld_val<STREAM, F32>(A, k), op.gather(ld_mat<STREAM>(A.col + k)));
+                fma_acc(s, ld_val<STREAM, F32>(A, k), gather_chk(op, ld_mat<STREAM>(A.col + k), A.ncols));
             if constexpr (G > 1) {
 #pragma unroll
                 for (int o = G / 2; o > 0; o >>= 1) add_acc(s, shfl_xor_acc(gmask, s, o));
@@ -816,7 +836,7 @@ __global__ void __launch_bounds__(kBlock) csr_rows(CsrDev A, Op op, const int32_
 #pragma unroll
             for (int k = 0; k < PER; ++k) {
                 const int e = tid + k * kBlock;
-                if (e < ne) prod[e] = v[k] * op.gather(c[k]);
+                if (e < ne) prod[e] = v[k] * gather_chk(op, c[k], A.ncols);
             }
             __syncthreads();
             for (int r = rb + tid / G; r < re; r += kBlock / G) {
@@ -834,7 +854,7 @@ __global__ void __launch_bounds__(kBlock) csr_rows(CsrDev A, Op op, const int32_
         } else {  // one long row
             double s = 0.0;
             for (int e = tid; e < ne; e += kBlock)
-                s += ld_val<STREAM, F32>(A, eb + e) * op.gather(ld_mat<STREAM>(A.col + eb + e));
+                s += ld_val<STREAM, F32>(A, eb + e) * gather_chk(op, ld_mat<STREAM>(A.col + eb + e), A.ncols);
             s = warp_sum(s);
             if ((tid & 31) == 0) prod[tid >> 5] = s;
             __syncthreads();
