@@ -321,9 +321,20 @@ def main():
 
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TEST ONLY (AMGB_BENCH_ONE_GPU=1): every rank on GPU 0, torch.distributed over
+    # gloo and the library's host shared-memory transport (AMGB_TRANSPORT=shm), so
+    # this N > 1 path runs end to end on a one-GPU box; numbers from it are not
+    # multi-GPU measurements
+    one_gpu = world > 1 and os.environ.get("AMGB_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
+        os.environ["AMGB_TRANSPORT"] = "shm"
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
         if world > 1:
@@ -352,9 +363,10 @@ def main():
     else:
         # strong scaling: the global system row-partitioned over the ranks, halo
         # exchange / all-reduce / coarse all-gather over NCCL
-        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        uid = torch.zeros(128, dtype=torch.uint8, device="cpu" if one_gpu else "cuda")
         if rank == 0:
-            uid.copy_(torch.tensor(list(amgb.nccl_unique_id()), dtype=torch.uint8))
+            uid.copy_(torch.tensor(list(amgb.nccl_unique_id() if not one_gpu else os.urandom(128)),
+                                   dtype=torch.uint8))
         dist.broadcast(uid, 0)
         h = amgb.setup_dist(ptr, col, val, nranks=world, rank=rank, nccl_id=bytes(uid.cpu().tolist()),
                             params=prm, device=local, use_graph=0 if args.no_graph else 1, n=n)
@@ -424,7 +436,8 @@ def main():
                                                                  A["alg_bytes"], A["status"], A["rel"])
     prof_ms, prof_bytes, prof_launch = B["prof_ms"], B["prof_bytes"], B["prof_launch"]
     clk_summary = A["clocks"]
-    t_local = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
+    tdev = "cpu" if one_gpu else "cuda"  # gloo (test only) reduces host tensors
+    t_local = torch.tensor([elapsed_ms], dtype=torch.float64, device=tdev)
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
     t_max_ms = float(t_local.item())
@@ -451,7 +464,7 @@ def main():
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
             vc_e = sum(vcs)
-        te = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        te = torch.tensor([dt], dtype=torch.float64, device=tdev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": float(vc_e) / float(te.item()) * (n if weak else 1),
