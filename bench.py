@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="amgb", choices=["amgb", "reference"])
     ap.add_argument("--problem", default="poisson")
-    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--n", "--size", dest="n", type=int, default=256)
     ap.add_argument("--relax", default=None)
     ap.add_argument("--solver", default=None)
     ap.add_argument("--tol", type=float, default=1e-8)
@@ -221,6 +221,10 @@ def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    # rank 0 alone runs the oracle: give it the host cores (torchrun exports
+    # OMP_NUM_THREADS=1 to every rank; libgomp reads it when the oracle loads)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
     import oracle
     ptr, col, val, f = problem_arrays(args.problem, args.n)
     A = oracle.Csr(ptr, col, val)
@@ -312,7 +316,12 @@ def main():
         return run_reference(args, cfg)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     # host setup threads: share the host cores between the ranks of this node
-    os.environ.setdefault("OMP_NUM_THREADS", str(max(1, (os.cpu_count() or 1) // world)))
+    # (multi-GPU: rank 0 alone builds and partitions the hierarchy -- the scattered
+    # setup -- so it gets the cores; torchrun exports OMP_NUM_THREADS=1 to every rank)
+    if world > 1 and int(os.environ.get("RANK", "0")) == 0:
+        os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
+    else:
+        os.environ.setdefault("OMP_NUM_THREADS", str(max(1, (os.cpu_count() or 1) // world)))
 
     import torch
     import torch.distributed as dist
@@ -535,7 +544,7 @@ def main():
                 "levels": len(infos), "rows_per_level": [i["rows"] for i in infos],
                 "nnz_per_level": [i["nnz_A"] for i in infos],
                 "reordered_store": bool(A.get("flags", 0) & 2),
-                "dict_slice_frac_A0": round(infos[0]["dict_slices_A"] / max(1, (infos[0]["rows"] + 31) // 32), 4),
+                "dict_slice_frac_A0": round(infos[0]["dict_slices_A"] / max(1, (h.vec_len + 31) // 32), 4),
                 "iters_per_solve": iters_all[-1], "rel_resid": rels[-1], "status": statuses[-1],
                 "solve_ms": t_max_ms / args.steps, "setup_s": setup_s,
                 "setup": "numeric steps on the GPU (strength, P, R, RAP, smoother), aggregation + coarse inverse on "
