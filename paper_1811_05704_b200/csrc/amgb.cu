@@ -555,13 +555,14 @@ struct Handle {
         const char* e = std::getenv("AMGB_PDL");
         return e && std::string(e) == "1";
     }();
-    // PDL pays only where every pass is a few microseconds of launch-latency-bound
-    // work: measured 0.72 vs 0.77 ms per 32^3 solve, but 8.4 vs 7.5 ms at 150^3 and
-    // 41.5 vs 35.7 ms at 256^3 (profiles/r02_misc).  On by default for hierarchies
-    // whose finest level has fewer than 65,536 rows; AMGB_PDL=0 / 1 forces it.
+    // PDL pays only where the passes are short, launch-latency-bound work:
+    // measured 0.69 vs 0.75 ms per 32^3 solve and 1.53 vs 1.56 ms at 64^3, but
+    // 8.4 vs 7.5 ms at 150^3 and 41.5 vs 35.7 ms at 256^3 (profiles/r02_misc).  On
+    // by default for hierarchies whose finest level has fewer than 500,000 rows;
+    // AMGB_PDL=0 / 1 forces it.
     void choose_pdl(int64_t n0) {
         const char* e = std::getenv("AMGB_PDL");
-        pdl = e ? std::string(e) == "1" : n0 < 65536;
+        pdl = e ? std::string(e) == "1" : n0 < 500000;
     }
     template <class... KArgs, class... Args>
     void klaunch(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, Args&&... args) {

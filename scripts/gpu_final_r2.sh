@@ -23,6 +23,8 @@ PY
 if [ -z "$SKIP_REF" ]; then
 timeout 1200 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > $OUT/ref.json 2> $OUT/ref.err; echo "ref rc=$?"; tail -c 400 $OUT/ref.json
 fi
+# the other BASELINE configs with clock records
+[ -n "$SKIP_CFG" ] || TAG=$TAG bash scripts/gpu_configs_r2.sh
 # ncu: launch list of the bench command (host loop over the iteration graph: ncu does not
 # enumerate kernels inside conditional graph nodes), then --set full on the level-0 A passes
 export AMGB_NO_DEVICE_LOOP=1
