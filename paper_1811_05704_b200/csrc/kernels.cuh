@@ -475,52 +475,59 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sel
     } else {  // ------------------------------------ consumer warps
         const int r = lane % C;  // row within the slice
         const int pt = lane / C; // part of the row
-        // this warp's slice offsets of the next tile are loaded one tile ahead,
-        // so their latency is off the critical path
+        // loop-invariant addresses and flags, hoisted out of the tile loop
+        const uint32_t bar_full0 = smem_u32(bars), bar_empty0 = smem_u32(bars + kTmaStages);
+        const bool sorted = A.rperm != nullptr;
+        const int nslices = (int)A.nslices, nrows = (int)A.nrows, ntiles = (int)A.ntiles;
+        // slice offsets as 32-bit low words (their differences fit in 32 bits;
+        // the arrays are little-endian int64), loaded one tile ahead so their
+        // latency is off the critical path
+        const uint32_t* sp32 = reinterpret_cast<const uint32_t*>(A.sptr);
+        const uint32_t* cp32 = reinterpret_cast<const uint32_t*>(A.cptr);
         struct SliceOff {
-            int64_t e0 = 0, e1 = 0, eb = 0, c0 = 0, c1 = 0, cb = 0;
+            uint32_t e0 = 0, e1 = 0, eb = 0, c0 = 0, c1 = 0, cb = 0;
         };
-        auto load_off = [&](int64_t t) {
+        auto load_off = [&](int t) {
             SliceOff o;
-            const int64_t slice = t * NS + warp;
-            if (t < A.ntiles && slice < A.nslices) {
-                o.e0 = A.sptr[slice];
-                o.e1 = A.sptr[slice + 1];
-                o.eb = A.sptr[t * NS];
-                o.c0 = A.cptr[slice];
-                o.c1 = A.cptr[slice + 1];
-                o.cb = A.cptr[t * NS];
+            const int slice = t * NS + warp;
+            if (t < ntiles && slice < nslices) {
+                o.e0 = __ldg(sp32 + 2 * slice);
+                o.e1 = __ldg(sp32 + 2 * slice + 2);
+                o.eb = __ldg(sp32 + 2 * (t * NS));
+                o.c0 = __ldg(cp32 + 2 * slice);
+                o.c1 = __ldg(cp32 + 2 * slice + 2);
+                o.cb = __ldg(cp32 + 2 * (t * NS));
             }
             return o;
         };
-        SliceOff nxt = load_off(blockIdx.x);
+        SliceOff nxt = load_off((int)blockIdx.x);
         int i = 0;
-        for (int64_t t = blockIdx.x; t < A.ntiles; t += gridDim.x, ++i) {
+        for (int t = (int)blockIdx.x; t < ntiles; t += (int)gridDim.x, ++i) {
             const int s = i % kTmaStages;
-            const int64_t slice = t * NS + warp;
-            const int64_t lrow = slice * C + r;
-            const bool has_row = slice < A.nslices && lrow < A.nrows;
+            const int slice = t * NS + warp;
+            const int lrow = slice * C + r;
+            const bool has_row = slice < nslices && lrow < nrows;
             // global row (views of a split pass); a sorted matrix has no
             // dictionary slices, so `row` is only the epilogue's index there
-            const int64_t row = A.row0 + (has_row ? slot_row(A.rperm, lrow) : lrow);
+            const int64_t row = A.row0 + (int64_t)((has_row && sorted) ? (int)slot_row(A.rperm, lrow) : lrow);
             typename Op::Row rr{};
             if constexpr (cols_of<Op>() == 1)
                 if (pt == 0 && has_row) rr = op.load(row);  // in flight during the wait
             const SliceOff cur = nxt;
-            nxt = load_off(t + gridDim.x);
+            nxt = load_off(t + (int)gridDim.x);
             int off = 0, w = 0, coff = 0;
             bool dict = false;  // the slice's columns are row + a shared offset list
-            if (slice < A.nslices) {
+            if (slice < nslices) {
                 off = (int)(cur.e0 - cur.eb);
-                w = (int)((cur.e1 - cur.e0) / C);
+                w = (int)(cur.e1 - cur.e0) / C;
                 coff = (int)(cur.c0 - cur.cb);
-                dict = cur.c1 - cur.c0 < (int64_t)C * w;
+                dict = (int)(cur.c1 - cur.c0) < C * w;
             }
-            mbar_wait(smem_u32(bars + s), (i / kTmaStages) & 1);
-            const VT* sv = reinterpret_cast<const VT*>(smem + (size_t)s * stage_bytes) + off + r;
-            const uint8_t* si = smem + (size_t)s * stage_bytes + off + r;
-            const int32_t* sc = reinterpret_cast<const int32_t*>(smem + (size_t)s * stage_bytes + (size_t)te * vbytes) +
-                                coff + (dict ? 0 : r);
+            mbar_wait(bar_full0 + 8 * s, (i / kTmaStages) & 1);
+            const unsigned char* st = smem + (size_t)s * stage_bytes;
+            const VT* sv = reinterpret_cast<const VT*>(st) + off + r;
+            const uint8_t* si = st + off + r;
+            const int32_t* sc = reinterpret_cast<const int32_t*>(st + (size_t)te * vbytes) + coff + (dict ? 0 : r);
             acc_t<Op> sum{};
             // entry k's column: sc[CS k] (+ row for a dictionary slice); the
             // stride is a template constant so every load is an immediate offset;
@@ -596,7 +603,7 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(kTmaBlocksPerSM)) sel
             else
                 dispatch(std::false_type{});
             __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(bars + kTmaStages + s));  // stage free
+            if (lane == 0) mbar_arrive(bar_empty0 + 8 * s);  // stage free
             if constexpr (T > 1) {
 #pragma unroll
                 for (int o = C; o < 32; o <<= 1) add_acc(sum, shfl_xor_acc(0xffffffffu, sum, o));
