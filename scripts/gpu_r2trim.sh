@@ -1,5 +1,5 @@
 #!/bin/bash
-OUT=gpurun_out/r2trim; mkdir -p $OUT
+OUT=gpurun_out/r2trim2; mkdir -p $OUT
 cp paper_1811_05704_b200/_lib/ab_new.so paper_1811_05704_b200/_lib/libamgb.so
-timeout 1500 python -m pytest tests/test_gpu_formats.py tests/test_gpu_fullsize.py tests/test_gpu_dict.py tests/test_gpu_sigma.py tests/test_gpu_dist.py tests/test_gpu_batched.py -q -m gpu -x > $OUT/tests.log 2>&1; echo "tests rc=$?"; tail -1 $OUT/tests.log
-TAG=r2trim ROUNDS=4 bash scripts/gpu_ab_lib.sh
+timeout 1500 python -m pytest tests/test_gpu_formats.py tests/test_gpu_fullsize.py tests/test_gpu_dict.py tests/test_gpu_sigma.py tests/test_gpu_dist.py tests/test_gpu_batched.py tests/test_gpu_idrs.py tests/test_gpu_mixed.py tests/test_gpu_reorder.py -q -m gpu -x > $OUT/tests.log 2>&1; echo "tests rc=$?"; tail -1 $OUT/tests.log
+TAG=r2trim2 ROUNDS=4 bash scripts/gpu_ab_lib.sh
