@@ -23,6 +23,8 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert "workload" in d["config"]
+    # one step = one full oracle solve (V-cycles / time, as cpu_baseline); host recorded
+    assert "full oracle solve" in d["config"]["step"] and "cpu_model" in d["config"]
 
 
 def test_reference_arm_other_ranks_are_silent():
