@@ -193,7 +193,7 @@ def weak_poisson(nranks, n=256):
     """Weak-scaling configuration (BASELINE.json configs[4], §8c): Poisson
     on the global box n x n x (n nranks), h = 1/(n+1) in every direction, so
     each rank's z-slab is one n^3 block.  Returns (ptr, col, val, f)."""
-    return poisson3d(n, n, n * nranks, h=1.0 / (n + 1))
+    return poisson3d(n, n, n * nranks)  # 1/h^2 = (n+1)^2 exactly (the default of poisson3d)
 
 
 def random_vector(n, seed=SEED_VEC):

@@ -143,3 +143,30 @@ def test_split_and_unsplit_passes_agree():
     r = synth.random_vector(len(f))
     za, zb = host(ms.precond(dev(r))), host(mu.precond(dev(r)))
     assert np.array_equal(za, zb)  # no dots inside a V-cycle: bitwise
+
+
+def test_weak_scaling_virtual_ranks_4_parts():
+    """BASELINE configs[4] (C5) shape at a small size: Poisson on n x n x 4n
+    (synth.weak_poisson: one n^3 z-slab per rank, h = 1/(n+1) everywhere),
+    partitioned over 4 virtual ranks -- each rank's level-0 rows are exactly its
+    slab -- against the single-GPU solve (iterations +-1, x within 1e-10 at equal
+    count) and the oracle (iterations +-1, x within 1e-8)."""
+    n, P = 24, 4
+    p, c, v, f = synth.weak_poisson(P, n)
+    assert len(f) == n * n * n * P
+    kw = {"coarse_enough": 100}
+    single = amgb.setup(p, c, v, **kw)
+    multi = amgb.setup_dist(p, c, v, nranks=P, rank=-1, gather_below=500, **kw)
+    st = multi.dist_info()["row_starts"]
+    assert list(st) == [r * n ** 3 for r in range(P + 1)]  # one slab per rank
+    xs, its, _, sts = single.solve(dev(f), tol=1e-8, maxiter=100)
+    xm, itm, relm, stm = multi.solve(dev(f), tol=1e-8, maxiter=100)
+    assert sts == stm == amgb.OK and abs(its - itm) <= 1 and relm <= 1.01e-8
+    if its == itm:
+        assert np.linalg.norm(host(xs) - host(xm)) <= 1e-10 * np.linalg.norm(host(xs))
+    A = oracle.Csr(p, c, v)
+    o = oracle.cg(A, f, tol=1e-8, maxiter=100, hier=oracle.Hierarchy(A, **kw))
+    assert abs(itm - o["iters"]) <= 1
+    if itm != o["iters"]:
+        xm, itm, relm, stm = multi.solve(dev(f), tol=0.0, maxiter=o["iters"])
+    assert np.linalg.norm(host(xm) - o["x"]) <= 1e-8 * np.linalg.norm(o["x"])

@@ -100,3 +100,18 @@ def test_permutation_roundtrip():
     B = _dense(p2, c2, v2, 64)
     assert np.array_equal(B, A[np.ix_(perm, perm)])
     assert np.array_equal(f2, f[perm])
+
+
+def test_weak_poisson_shape():
+    """configs[4] generator (§8c): n x n x (n P) box, h = 1/(n+1) in every
+    direction, nnz = 7N - 2(nx ny + ny nz + nx nz); P = 1 is the cube problem."""
+    n, P = 6, 3
+    p, c, v, f = synth.weak_poisson(P, n)
+    N = n * n * n * P
+    assert len(f) == N and p[-1] == 7 * N - 2 * (n * n + n * n * P + n * n * P)
+    d = np.repeat(np.arange(N), np.diff(p)) == c
+    assert np.all(v[d] == 6.0 * (n + 1) ** 2) and np.all(v[~d] == -float((n + 1) ** 2))
+    p1, c1, v1, f1 = synth.weak_poisson(1, n)
+    q, e, w, g = synth.poisson3d(n)
+    assert np.array_equal(p1, q) and np.array_equal(c1, e) and np.array_equal(v1, w)
+    assert synth.problem_rows("poisson", n) == n ** 3 and np.array_equal(synth.rhs_slice("poisson", n, 2, 5), np.ones(3))
