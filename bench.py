@@ -547,8 +547,9 @@ def main():
                 "dict_slice_frac_A0": round(infos[0]["dict_slices_A"] / max(1, (h.vec_len + 31) // 32), 4),
                 "iters_per_solve": iters_all[-1], "rel_resid": rels[-1], "status": statuses[-1],
                 "solve_ms": t_max_ms / args.steps, "setup_s": setup_s,
-                "setup": "numeric steps on the GPU (strength, P, R, RAP, smoother), aggregation + coarse inverse on "
-                         "the host; CUDA context created before the timer" if cfg.get("setup_device", 1) else "host",
+                "setup": "hierarchy built on the GPU (strength, aggregation, P, R, RAP, smoother; the coarsest "
+                         "dense inverse on the host), device formats + value indexing; CUDA context created "
+                         "before the timer",
                 "l2": "inputs larger than L2 (level-0 matrix %.2f GB + hierarchy vs 126 MB L2); no flush"
                       % (12e-9 * infos[0]["nnz_A"]),
                 "solve_alg_GBps": solve_gbs, "solve_roofline_frac": solve_gbs / peak,

@@ -5,11 +5,12 @@
  *   the solution of A u = f (Eq. (1)) by a Krylov method (CG, or
  *   BiCGStab for non-symmetric A) preconditioned by one AMG
  *   V-cycle (Algorithm 2; "single V-cycle is used as a
- *   preconditioning step").  The hierarchy is built on the host
- *   inside amg_setup (Algorithm 1; "the AMG hierarchy is always
- *   constructed on the main processor (CPU)") with smoothed (or
- *   plain) aggregation and then uploaded to the GPU, where the
- *   solve phase runs entirely in this library's sm_100a kernels.
+ *   preconditioning step").  The hierarchy is built inside
+ *   amg_setup (Algorithm 1) with smoothed (or plain) aggregation
+ *    -- by default on the GPU, bitwise equal to the host build the
+ *   paper prescribes ("the AMG hierarchy is always constructed on the main
+ *   processor (CPU)"), which params.setup_device = 0 selects --
+ *   and the solve phase runs entirely in this library's sm_100a kernels.
  *   The readings of the paper this implementation commits to are listed in
  *   DESIGN.md §3 (strength test, aggregation order, smoother constants, ...).
  *
@@ -88,10 +89,11 @@ typedef struct {
                                method and its A stay fp64).  SURVEY §8f rank 2; value types
                                "double or float", PAPER.md:186-191 */
     int32_t gmres_m;        /* GMRES restart length m in [1, 64] [30] ("solver.M") */
-    int32_t setup_device;   /* 1: the hierarchy's numeric steps (strength, smoothed P, R = P^T, A P,
-                               R(AP), smoother data) run on the CUDA device, aggregation and the
-                               coarse inverse on the host [1]; 0: everything on the host.  Bitwise
-                               the same hierarchy either way (Algorithm 1,
+    int32_t setup_device;   /* 1: the hierarchy is built on the CUDA device -- strength, the greedy
+                               aggregation (Phase 1 by exact dependency propagation), smoothed P,
+                               R = P^T, A P, R(AP), smoother data; only the coarsest dense inverse
+                               on the host [1]; 0: everything on the host.  Bitwise the same
+                               hierarchy either way (Algorithm 1,
                                PAPER.md:95-107).  Host-only handles (device = -1) use the host. */
     int32_t idrs_s;         /* IDR(s) shadow-space dimension s in {1, 2, 4, 8} [4] ("solver.s") */
     int32_t reorder;        /* locality reordering of the device store (single GPU):

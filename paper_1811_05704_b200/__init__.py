@@ -1,8 +1,9 @@
 """B200-native smoothed-aggregation AMG solve phase (arXiv 1811.05704, AMGCL).
 
 Thin Python binding of ``_lib/libamgb.so`` (C ABI: ``include/amgb.h``).  This
-module only marshals arguments: the hierarchy is built by the library's C++ host
-setup (Algorithm 1) and every step of the solve phase
+module only marshals arguments: the hierarchy is built inside the library
+(Algorithm 1; on the GPU by default, bitwise the C++ host
+build) and every step of the solve phase
 (Algorithm 2, inside CG / BiCGStab) runs in
 the library's sm_100a kernels.  PyTorch is used for device memory and streams
 only.  There is no CPU fallback: if the shared library is missing, importing

@@ -953,7 +953,7 @@ struct Handle {
             const cudaError_t q = cudaStreamQuery(s);
             if (q == cudaSuccess) break;
             if (q != cudaErrorNotReady) ck(q, "sync");
-            if (nc.commGetAsyncError) {
+            if (nc.commGetAsyncError && (spin & 255) == 255) {
                 int ae = 0;
                 nc.commGetAsyncError(nccl, &ae);
                 if (ae != 0 && ae != kNcclInProgress)
@@ -962,7 +962,9 @@ struct Handle {
             }
             if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > nccl_timeout)
                 nccl_fail("no progress for " + std::to_string((int)nccl_timeout) + " s (a peer rank died or stalled)");
-            if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+            // busy-poll (a sleep would add its wake-up slack to every iteration's
+            // host round trip); back off only once the wait is long
+            if (spin > 20000) std::this_thread::sleep_for(std::chrono::microseconds(100));
         }
     }
     // test transport: personalised all-to-all of host bytes (errors -> AMG_E_NCCL)
