@@ -107,3 +107,18 @@ def test_dotted_param_keys():
     prm = amgb.make_params({"solver.type": "bicgstab", "precond.relax.type": "chebyshev",
                             "precond.coarsening.type": "aggregation"})
     assert prm.solver == 1 and prm.relax == 2 and prm.coarsening == 1
+
+
+def test_vector_length_and_host_checks():
+    """amg_vector_length on a host-only handle (the global n) and the binding's
+    host-array checks (no GPU needed: they run before any library call)."""
+    p, c, v, f = synth.poisson3d(10, 11, 12)
+    h = amgb.setup(p, c, v, device=-1)
+    assert h.vec_len == len(f) == 10 * 11 * 12
+    with pytest.raises(ValueError):
+        amgb._host_vec(np.zeros(5), 6, "f")
+    with pytest.raises(ValueError):
+        amgb._host_vec(np.zeros(6, np.float32), 6, "f")
+    with pytest.raises(ValueError):
+        amgb._host_vec(np.zeros((6, 2))[:, 0], 6, "f")
+    assert amgb._host_vec(np.zeros(6), 6, "f").shape == (6,)
