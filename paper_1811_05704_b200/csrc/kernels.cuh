@@ -716,20 +716,16 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(2)) csr_tma(CsrTma A,
             }
         }
     } else {  // ------------------------------------ consumer warps
-        // loop-invariant barrier addresses and 32-bit tile / row indices (the
-        // per-row overhead dominates rows of 1-6 entries)
-        const uint32_t bar_full0 = smem_u32(bars), bar_empty0 = smem_u32(bars + kTmaStages);
-        const int nrows = (int)A.nrows, ntiles = (int)A.ntiles;
         int i = 0;
-        for (int t = (int)blockIdx.x; t < ntiles; t += (int)gridDim.x, ++i) {
+        for (int64_t t = blockIdx.x; t < A.ntiles; t += gridDim.x, ++i) {
             const int s = i % kTmaStages;
-            const int lrow = t * kTcRows + warp * 32 + lane;
-            const bool has_row = lrow < nrows;
+            const int64_t lrow = t * kTcRows + warp * 32 + lane;
+            const bool has_row = lrow < A.nrows;
             const int64_t row = A.row0 + lrow;
             typename Op::Row rr{};
             if constexpr (cols_of<Op>() == 1)
                 if (has_row) rr = op.load(row);  // in flight during the wait
-            mbar_wait(bar_full0 + 8 * s, (i / kTmaStages) & 1);
+            mbar_wait(smem_u32(bars + s), (i / kTmaStages) & 1);
             const unsigned char* st = smem + (size_t)s * sb;
             const int32_t* sp = reinterpret_cast<const int32_t*>(st + (size_t)te * (vbytes + 4));
             const int32_t e0 = sp[0];
@@ -764,7 +760,7 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(2)) csr_tma(CsrTma A,
                     run(std::false_type{});
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(bar_empty0 + 8 * s);  // stage free
+            if (lane == 0) mbar_arrive(smem_u32(bars + kTmaStages + s));  // stage free
             if constexpr (cols_of<Op>() > 1)
                 if (has_row) rr = op.load(row);
             if (has_row) op.row(row, sum, rr, dots);
