@@ -2451,7 +2451,10 @@ int64_t tcsr_tile_ent(const Csr& A) {
     return (te + 15) & ~(int64_t)15;
 }
 
-Fmt pick_format(const Csr& A) {
+// role of a matrix in the V-cycle (the format policy treats wide R differently)
+enum class Role { A, P, R };
+
+Fmt pick_format(const Csr& A, Role role) {
     const char* e = std::getenv("AMGB_FORMAT");
     const std::string f = e ? e : "auto";
     if (f == "csr") return Fmt::CSR;
@@ -2476,15 +2479,21 @@ Fmt pick_format(const Csr& A) {
         stored += 32 * w;
     }
     const double pad = A.nnz() ? (double)stored / (double)A.nnz() : 1.0;
-    // AMGB_TMACSR: 0 never, 1 narrow padded matrices (default), 2 also wide ones
+    // AMGB_TMACSR: 0 never, 1 narrow padded matrices only, 2 also every wide
+    // padded one, 3 (default) narrow ones and wide restrictions
     const char* tc = std::getenv("AMGB_TMACSR");
-    const int tmode = tc ? std::atoi(tc) : 1;
+    const int tmode = tc ? std::atoi(tc) : 3;
     // narrow rows: TMA-staged SELL-32 when its slices are (nearly) unpadded --
     // the level-0 stencil, whose slices also compress to an offset dictionary --
-    // else the padding-free TMA-staged CSR (smoothed-aggregation P).  Wide rows
-    // (coarse A, R): register-pipelined SELL-32, one thread per row.
+    // else the padding-free TMA-staged CSR (smoothed-aggregation P).  Wide rows:
+    // the restrictions R in TMA-CSR too (their few distinct values index to one
+    // byte, which the TMA kernels take), the coarse A in register-pipelined
+    // SELL-32 (its 16-bit value indices do not fit the TMA kernels' table):
+    // 256^3, interleaved A/B: all wide in TMA-CSR moved the transfer class
+    // 10.9 -> 9.5 ms but the coarse A passes 8.4 -> 10.9 ms (profiles/r02_tcsr_wide)
     if (lmax <= 12) return (tmode >= 1 && pad > 1.15 && tcsr_fits) ? Fmt::TMACSR : Fmt::TMA;
-    return (tmode >= 2 && pad > 1.05 && tcsr_fits) ? Fmt::TMACSR : Fmt::SELL;
+    const bool wide_tcsr = tmode == 2 || (tmode == 3 && role == Role::R);
+    return (wide_tcsr && pad > 1.05 && tcsr_fits) ? Fmt::TMACSR : Fmt::SELL;
 }
 
 // Row blocks of the CSR kernel: at most kEnt entries and a row cap chosen from
@@ -2510,13 +2519,13 @@ std::vector<int32_t> row_blocks(const Csr& A, int G) {
     return b;
 }
 
-DMat upload_mat_impl(Handle& H, const Csr& A, int64_t* bytes, bool f32);
+DMat upload_mat_impl(Handle& H, const Csr& A, int64_t* bytes, bool f32, Role role);
 
 // upload_mat with AMGB_SETUP_TIMING: per-matrix conversion + copy time
-DMat upload_mat(Handle& H, const Csr& A, int64_t* bytes, bool f32 = false) {
+DMat upload_mat(Handle& H, const Csr& A, int64_t* bytes, bool f32 = false, Role role = Role::A) {
     const auto t0 = std::chrono::steady_clock::now();
     const double up0 = H.upload_ms;
-    DMat d = upload_mat_impl(H, A, bytes, f32);
+    DMat d = upload_mat_impl(H, A, bytes, f32, role);
     if (std::getenv("AMGB_SETUP_TIMING"))
         std::fprintf(stderr, "[setup]   matrix %lld x %lld, %lld nnz, fmt %d: %.1f ms (H2D %.1f ms)\n",
                      (long long)A.nrows, (long long)A.ncols, (long long)A.nnz(), (int)d.fmt,
@@ -2786,7 +2795,7 @@ void index_store(Handle& H, DMat& d, int64_t* bytes) {
     *bytes -= (8 - d.vbytes) * d.stored;
 }
 
-DMat upload_mat_impl(Handle& H, const Csr& A0, int64_t* bytes, bool f32) {
+DMat upload_mat_impl(Handle& H, const Csr& A0, int64_t* bytes, bool f32, Role role) {
     DMat d;
     const Csr& A = A0;
     d.nrows = A.nrows;
@@ -2794,7 +2803,7 @@ DMat upload_mat_impl(Handle& H, const Csr& A0, int64_t* bytes, bool f32) {
     d.nnz = A.nnz();
     if (d.nnz >= INT32_MAX) throw CudaError{"level has >= 2^31 nonzeros"};
     if (d.nrows == 0) return d;
-    d.fmt = pick_format(A);
+    d.fmt = pick_format(A, role);
     if (d.fmt == Fmt::CSR) {
         const double avg = A.nrows ? (double)A.nnz() / (double)A.nrows : 0.0;
         int G = 1;
@@ -3141,8 +3150,8 @@ void upload_part(Handle& H, const RankPart& RP, Part& P) {
             L.padA = L.nnzA;
         }
         if (!coarsest) {
-            L.P = upload_mat(H, lp.mp(), &L.dev_bytes, f32);
-            L.R = upload_mat(H, lp.mr(), &L.dev_bytes, f32);
+            L.P = upload_mat(H, lp.mp(), &L.dev_bytes, f32, Role::P);
+            L.R = upload_mat(H, lp.mr(), &L.dev_bytes, f32, Role::R);
         }
         // multi-GPU: interior rows (no ghost column) of each pass that follows a
         // halo exchange -- A and R gather this level's vectors, P the next level's

@@ -3,7 +3,8 @@ device format the headline runs (VERDICT r1 "next #1").  GPU only (-m gpu).
 
 pick_format (amgb.cu) stores a matrix with >= 65,536 rows as TMA-staged SELL-32
 (narrow, unpadded rows: A0 at 256^3), TMA-staged CSR (narrow rows that SELL-32
-would pad by > 15 %: P0, P1) or SELL-32 (wide rows: R0, A1, R1), and smaller
+would pad by > 15 %: P0, P1; padded wide restrictions: R0, R1) or SELL-32 (the
+wide coarse A: A1, A2), and smaller
 ones as row-block CSR; AMGB_FORMAT = sell | tma | tmacsr forces a format on
 every level, AMGB_NO_DICT=1 stores the TMA format with explicit column indices
 instead of the per-slice offset dictionary.  Each case runs every op of Algorithm 2
@@ -106,7 +107,7 @@ def sell_padding(M):
     return 32 * pad.reshape(-1, 32).max(axis=1).sum() / max(M.nnz, 1) if M.nrows else 1.0
 
 
-def expected_fmt(fmt, M):
+def expected_fmt(fmt, M, role="A"):
     if fmt == "sell":
         return amgb.FMT_SELL
     if fmt == "tmacsr":
@@ -115,8 +116,8 @@ def expected_fmt(fmt, M):
         return amgb.FMT_SELL if tma_wide(M) else amgb.FMT_TMA
     if M.nrows < 65536:
         return amgb.FMT_CSR
-    if max_row(M) > 12:
-        return amgb.FMT_SELL
+    if max_row(M) > 12:  # wide: restrictions in TMA-CSR when padded, coarse A in SELL-32
+        return amgb.FMT_TMACSR if role == "R" and sell_padding(M) > 1.05 and not tcsr_wide(M) else amgb.FMT_SELL
     return amgb.FMT_TMACSR if sell_padding(M) > 1.15 and not tcsr_wide(M) else amgb.FMT_TMA
 
 
@@ -164,8 +165,8 @@ def test_fused_kernels_per_row(gen, n, kw, fmt, monkeypatch):
         A, P, R = o.matrix(l, "A"), o.matrix(l, "P"), o.matrix(l, "R")
         info = h.level_info(l)
         # the store is in the format this case is about
-        for key, M in (("fmt_A", A), ("fmt_P", P), ("fmt_R", R)):
-            assert info[key] == expected_fmt(fmt, M), (l, key, info["formats"])
+        for key, M, role in (("fmt_A", A, "A"), ("fmt_P", P, "P"), ("fmt_R", R, "R")):
+            assert info[key] == expected_fmt(fmt, M, role), (l, key, info["formats"])
         if fmt == "tma_explicit":
             assert info["dict_slices_A"] == 0
         n_l, nc = A.nrows, P.ncols
@@ -310,8 +311,8 @@ def test_vcycle_and_solve_per_format(fmt, monkeypatch):
 
 def test_level1_in_sell_and_tma_under_auto(monkeypatch):
     """88^3 (681,472 rows): level 1 has >= 65,536 rows, so under the default policy
-    A1 and R0 run sell_rows, A0 sell_tma and P0 csr_tma, as at 256^3; every op
-    of levels 0-1 per row against the oracle."""
+    A1 runs sell_rows, A0 sell_tma and P0 / R0 csr_tma, as at 256^3; every op of
+    levels 0-1 per row against the oracle."""
     for k in ("AMGB_FORMAT", "AMGB_NO_DICT"):
         monkeypatch.delenv(k, raising=False)
     p, c, v, f = synth.problem("poisson", 88)
@@ -320,7 +321,7 @@ def test_level1_in_sell_and_tma_under_auto(monkeypatch):
     i1 = h.level_info(1)
     assert i1["rows"] >= 65536
     assert h.level_info(0)["fmt_A"] == amgb.FMT_TMA and h.level_info(0)["fmt_P"] == amgb.FMT_TMACSR
-    assert h.level_info(0)["fmt_R"] == amgb.FMT_SELL and i1["fmt_A"] == amgb.FMT_SELL
+    assert h.level_info(0)["fmt_R"] == amgb.FMT_TMACSR and i1["fmt_A"] == amgb.FMT_SELL
     rng = np.random.default_rng(7)
     for l in (0, 1):
         A, P, R = o.matrix(l, "A"), o.matrix(l, "P"), o.matrix(l, "R")
