@@ -287,11 +287,14 @@ HostTmaCols tma_cols(const Csr& A, HostSell& S, bool allow_dict) {
     return T;
 }
 
-// bytes of one stage of the TMA-staged CSR kernel (csr_tma): values, columns
-// (tile_ent each, a multiple of 4) and the tile's row pointers, 16-B aligned
-inline size_t tcsr_stage_bytes(int64_t tile_ent, bool f32, bool vix = false) {
-    return (((size_t)tile_ent * ((vix ? 1 : f32 ? 4 : 8) + 4) + (size_t)(kTcRows + 8) * 4) + 15) & ~(size_t)15;
+// bytes of one stage of the TMA-staged CSR kernel (csr_tma): values (vbytes
+// each: 8, 4 with fp32, 1 / 2 with value indices), columns (tile_ent each, a
+// multiple of 16) and the tile's row pointers, 16-B aligned
+inline size_t tcsr_stage_bytes(int64_t tile_ent, int vbytes) {
+    return (((size_t)tile_ent * (vbytes + 4) + (size_t)(kTcRows + 8) * 4) + 15) & ~(size_t)15;
 }
+// shared-memory bytes of a csr_tma value table of ntab entries
+inline size_t tcsr_vtab_bytes(int64_t ntab) { return ((size_t)ntab * 8 + 127) & ~(size_t)127; }
 
 // A device matrix in the format chosen for it.
 enum class Fmt { CSR, SELL, TMA, TMACSR };
@@ -805,9 +808,10 @@ struct Handle {
     void rows_tcsr_un(const CsrTma& M, const Op& op, const int32_t* gate, const Red& red) {
         auto kern = csr_tma<STREAM, Op, F32, UN1>;
         CsrTma m = M;
-        const bool vix = !F32 && M.vi8 != nullptr;
-        m.smem_stage = (int32_t)tcsr_stage_bytes(M.tile_ent, F32, vix);
-        const size_t smem = (vix ? kVTabBytes : 0) + (size_t)kTmaStages * m.smem_stage + 2 * kTmaStages * 8;
+        const int vbytes = F32 ? 4 : M.vi8 ? 1 : M.vi16 ? 2 : 8;
+        m.vtab_bytes = (!F32 && (M.vi8 || M.vi16)) ? (int32_t)tcsr_vtab_bytes(M.ntab) : 0;
+        m.smem_stage = (int32_t)tcsr_stage_bytes(M.tile_ent, vbytes);
+        const size_t smem = (size_t)m.vtab_bytes + (size_t)kTmaStages * m.smem_stage + 2 * kTmaStages * 8;
         static size_t configured = 0;  // per instantiation
         if (smem > configured) {
             ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), "smem attr");
@@ -2454,7 +2458,10 @@ int64_t tcsr_tile_ent(const Csr& A) {
 // role of a matrix in the V-cycle (the format policy treats wide R differently)
 enum class Role { A, P, R };
 
-Fmt pick_format(const Csr& A, Role role) {
+// *want_index: the pick is TMA-CSR for a wide A, which pays only when its
+// values index to at most 2 bytes (upload falls back to SELL-32 otherwise).
+Fmt pick_format(const Csr& A, Role role, bool* want_index = nullptr) {
+    if (want_index) *want_index = false;
     const char* e = std::getenv("AMGB_FORMAT");
     const std::string f = e ? e : "auto";
     if (f == "csr") return Fmt::CSR;
@@ -2466,7 +2473,7 @@ Fmt pick_format(const Csr& A, Role role) {
     const bool tma_fits =
         (int64_t)kTmaStages * 256 * 12 * std::max<int64_t>(lmax, 1) + kVTabBytes + 64 <= 227 * 1024;
     const bool tcsr_fits = A.nrows > 0 && A.nnz() < INT32_MAX &&
-                           (int64_t)kTmaStages * (int64_t)tcsr_stage_bytes(tcsr_tile_ent(A), false) + 64 <= 227 * 1024;
+                           (int64_t)kTmaStages * (int64_t)tcsr_stage_bytes(tcsr_tile_ent(A), 8) + 64 <= 227 * 1024;
     if (f == "tma") return tma_fits ? Fmt::TMA : Fmt::SELL;
     if (f == "tmacsr") return tcsr_fits ? Fmt::TMACSR : Fmt::SELL;
     if (A.nrows < 65536) return Fmt::CSR;
@@ -2480,7 +2487,9 @@ Fmt pick_format(const Csr& A, Role role) {
     }
     const double pad = A.nnz() ? (double)stored / (double)A.nnz() : 1.0;
     // AMGB_TMACSR: 0 never, 1 narrow padded matrices only, 2 also every wide
-    // padded one, 3 (default) narrow ones and wide restrictions
+    // padded one, 3 (default) narrow ones and wide restrictions, 4 as 3 plus
+    // the wide A whose values index to 2 bytes (measured slower: 35.0 vs 33.7 ms
+    // at 256^3, the A1 passes 10.1 vs 8.4 ms, profiles/r02_tcsr_vi16_tried)
     const char* tc = std::getenv("AMGB_TMACSR");
     const int tmode = tc ? std::atoi(tc) : 3;
     // narrow rows: TMA-staged SELL-32 when its slices are (nearly) unpadded --
@@ -2488,12 +2497,15 @@ Fmt pick_format(const Csr& A, Role role) {
     // else the padding-free TMA-staged CSR (smoothed-aggregation P).  Wide rows:
     // the restrictions R in TMA-CSR too (their few distinct values index to one
     // byte, which the TMA kernels take), the coarse A in register-pipelined
-    // SELL-32 (its 16-bit value indices do not fit the TMA kernels' table):
+    // SELL-32 (even with 16-bit value indices, AMGB_TMACSR=4, csr_tma is slower
+    // on its ~31-entry rows):
     // 256^3, interleaved A/B: all wide in TMA-CSR moved the transfer class
     // 10.9 -> 9.5 ms but the coarse A passes 8.4 -> 10.9 ms (profiles/r02_tcsr_wide)
     if (lmax <= 12) return (tmode >= 1 && pad > 1.15 && tcsr_fits) ? Fmt::TMACSR : Fmt::TMA;
-    const bool wide_tcsr = tmode == 2 || (tmode == 3 && role == Role::R);
-    return (wide_tcsr && pad > 1.05 && tcsr_fits) ? Fmt::TMACSR : Fmt::SELL;
+    const bool wide_tcsr = tmode == 2 || (tmode >= 3 && role == Role::R) || (tmode == 4 && role == Role::A);
+    const bool pick = wide_tcsr && pad > 1.05 && tcsr_fits;
+    if (pick && want_index && tmode == 4 && role == Role::A) *want_index = true;
+    return pick ? Fmt::TMACSR : Fmt::SELL;
 }
 
 // Row blocks of the CSR kernel: at most kEnt entries and a row cap chosen from
@@ -2727,9 +2739,10 @@ __global__ void k_vidx(int64_t n, const unsigned long long* __restrict__ v, cons
 
 // dval: n device values; on success *tab (table, 256 or 65536 entries padded
 // with zeros) and exactly one of *i8 / *i16 (n + pad entries) are handle
-// allocations.  max_u: 256 or 65536.
+// allocations; *nu (optional) = the number of distinct values.  max_u: at
+// most 65536 (more than 256 gives 2-byte indices).
 bool value_index(Handle& H, const double* dval, int64_t n, int64_t pad, int64_t max_u, const double** tab,
-                 const uint8_t** i8, const uint16_t** i16) {
+                 const uint8_t** i8, const uint16_t** i16, int* nu_out = nullptr) {
     *tab = nullptr, *i8 = nullptr, *i16 = nullptr;
     const char* ve = std::getenv("AMGB_VIDX");  // default on; AMGB_VIDX=0 keeps fp64 value arrays
     if (n <= 0 || (ve && ve[0] == '0')) return false;
@@ -2765,6 +2778,7 @@ bool value_index(Handle& H, const double* dval, int64_t n, int64_t pad, int64_t 
     ck(cudaGetLastError(), "vidx");
     ck(cudaDeviceSynchronize(), "vidx sync");
     *tab = t, *i8 = a8, *i16 = a16;
+    if (nu_out) *nu_out = h_nu;
     return true;
 }
 
@@ -2779,10 +2793,16 @@ void index_store(Handle& H, DMat& d, int64_t* bytes) {
         d.tma.val = nullptr;
         d.tma.vtab = tab, d.tma.vi8 = i8;
     } else if (d.fmt == Fmt::TMACSR) {
-        if (!value_index(H, d.tcsr.val, d.nnz, 16, 256, &tab, &i8, &i16)) return;
+        // the table is staged in shared memory beside kTmaStages stages of
+        // 2-byte indices: at most what is left of the 227 KB
+        const int64_t left = 227 * 1024 - 64 - (int64_t)kTmaStages * (int64_t)tcsr_stage_bytes(d.tcsr.tile_ent, 2);
+        const int64_t cap = std::min<int64_t>(65536, std::max<int64_t>(256, (left - 256) / 8));
+        int nu = 0;
+        if (!value_index(H, d.tcsr.val, d.nnz, 16, cap, &tab, &i8, &i16, &nu)) return;
         H.tfree(d.tcsr.val);
         d.tcsr.val = nullptr;
-        d.tcsr.vtab = tab, d.tcsr.vi8 = i8;
+        d.tcsr.vtab = tab, d.tcsr.vi8 = i8, d.tcsr.vi16 = i16;
+        d.tcsr.ntab = i8 ? 256 : (nu + 15) & ~15;
     } else if (d.fmt == Fmt::SELL) {
         if (!value_index(H, d.sell.val, d.stored, 16, 65536, &tab, &i8, &i16)) return;
         H.tfree(d.sell.val);
@@ -2803,7 +2823,9 @@ DMat upload_mat_impl(Handle& H, const Csr& A0, int64_t* bytes, bool f32, Role ro
     d.nnz = A.nnz();
     if (d.nnz >= INT32_MAX) throw CudaError{"level has >= 2^31 nonzeros"};
     if (d.nrows == 0) return d;
-    d.fmt = pick_format(A, role);
+    bool want_index = false;
+    d.fmt = pick_format(A, role, &want_index);
+    if (want_index && f32) d.fmt = Fmt::SELL;  // the fp32 store is not value-indexed
     if (d.fmt == Fmt::CSR) {
         const double avg = A.nrows ? (double)A.nnz() / (double)A.nrows : 0.0;
         int G = 1;
@@ -2862,7 +2884,14 @@ DMat upload_mat_impl(Handle& H, const Csr& A0, int64_t* bytes, bool f32, Role ro
         *bytes += (n + 9) * 4 + (nnz + 4) * 4 + (nnz + 2) * 8;
         if (!f32) index_store(H, d, bytes);
         ck(cudaDeviceSynchronize(), "convert sync");
-        return d;
+        if (!want_index || d.vbytes < 8) return d;
+        // a wide A with too many distinct values: SELL-32 instead
+        *bytes -= (n + 9) * 4 + (nnz + 4) * 4 + (nnz + 2) * 8;
+        H.tfree(t.ptr);
+        H.tfree(t.col);
+        H.tfree(t.val);
+        d.tcsr = CsrTma{};
+        d.fmt = Fmt::SELL;
     }
     // SELL / TMA: rows sorted by length inside 256-row windows when it pays
     std::vector<uint8_t> rp;

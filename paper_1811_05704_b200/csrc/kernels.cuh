@@ -641,8 +641,11 @@ struct CsrTma {
     const float* valf = nullptr;  // fp32 copy (mixed precision), padded by 4
     int32_t tile_ent = 0;         // stage capacity in entries (max over tiles, incl. alignment slack)
     int32_t smem_stage = 0;       // bytes of one stage
-    const double* vtab = nullptr; // value-indexed storage (<= 256 distinct values): 1-byte indices,
-    const uint8_t* vi8 = nullptr; // padded by 16; the table in shared memory; val unused
+    const double* vtab = nullptr; // value-indexed storage, the table staged in shared memory; val unused:
+    const uint8_t* vi8 = nullptr; // 1-byte indices (<= 256 distinct values), padded by 16
+    const uint16_t* vi16 = nullptr; // or 2-byte indices (<= ntab distinct values), padded by 16
+    int32_t ntab = 0;             // table entries (256 with vi8)
+    int32_t vtab_bytes = 0;       // shared-memory bytes of the table (set at launch; 128-B multiple)
 };
 
 // UN1: entries per unrolled step for one right-hand side (P rows hold 1-6
@@ -658,18 +661,19 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(2)) csr_tma(CsrTma A,
     if (gated(gate)) return;
     op.prepare();
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    // layout: [value table] stages { val[tile_ent] (VB bytes or 1-byte indices) | col[tile_ent] |
+    // layout: [value table] stages { val[tile_ent] (VB bytes, or 1- / 2-byte indices) | col[tile_ent] |
     // ptr[kTcRows + 8] }; barriers after the stages
-    const bool vix = !F32 && A.vi8 != nullptr;
+    const int vm = F32 ? 0 : A.vi8 ? 1 : A.vi16 ? 2 : 0;  // value mode: array / 8-bit / 16-bit index
+    const bool vix = vm != 0;
     double* vtab_s = reinterpret_cast<double*>(smem_raw);
-    unsigned char* smem = smem_raw + (vix ? kVTabBytes : 0);
-    const int vbytes = vix ? 1 : VB;
+    unsigned char* smem = smem_raw + (vix ? A.vtab_bytes : 0);
+    const int vbytes = vm == 1 ? 1 : vm == 2 ? 2 : VB;
     const int te = A.tile_ent;
     const size_t sb = (size_t)A.smem_stage;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTmaStages * sb);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (vix)
-        for (int k = threadIdx.x; k < 256; k += blockDim.x) vtab_s[k] = __ldg(A.vtab + k);
+        for (int k = threadIdx.x; k < A.ntab; k += blockDim.x) vtab_s[k] = __ldg(A.vtab + k);
     if (threadIdx.x == 0) {
         for (int s = 0; s < kTmaStages; ++s) {
             mbar_init(smem_u32(bars + s), 1);
@@ -694,7 +698,7 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(2)) csr_tma(CsrTma A,
                 const int64_t r0 = t * kTcRows;
                 const int64_t r1 = r0 + kTcRows < A.nrows ? r0 + kTcRows : A.nrows;
                 const int32_t e0 = A.ptr[r0], e1 = A.ptr[r1];
-                const int32_t vau = vix ? 16 : VA;  // value alignment unit (entries)
+                const int32_t vau = vm == 1 ? 16 : vm == 2 ? 8 : VA;  // value alignment unit (entries)
                 const int32_t va = e0 & ~(vau - 1), ca = e0 & ~3;
                 const uint32_t nv = (uint32_t)(((e1 - va) + vau - 1) & ~(vau - 1));
                 const uint32_t nc = (uint32_t)(((e1 - ca) + 3) & ~3);
@@ -704,8 +708,10 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(2)) csr_tma(CsrTma A,
                 unsigned char* st = smem + (size_t)s * sb;
                 mbar_expect_tx(full, nv * (uint32_t)vbytes + nc * 4u + np * 4u);
                 if (nv) {
-                    if (vix)
+                    if (vm == 1)
                         bulk_g2s<STREAM>(smem_u32(st), A.vi8 + va, nv, full, policy);
+                    else if (vm == 2)
+                        bulk_g2s<STREAM>(smem_u32(st), A.vi16 + va, nv * 2u, full, policy);
                     else if constexpr (F32)
                         bulk_g2s<STREAM>(smem_u32(st), A.valf + va, nv * 4u, full, policy);
                     else
@@ -731,10 +737,11 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(2)) csr_tma(CsrTma A,
             const int32_t e0 = sp[0];
             const VT* sv = reinterpret_cast<const VT*>(st) - (e0 & ~(VA - 1));
             const uint8_t* si = st - (e0 & ~15);
+            const uint16_t* si16 = reinterpret_cast<const uint16_t*>(st) - (e0 & ~7);
             const int32_t* sc = reinterpret_cast<const int32_t*>(st + (size_t)te * vbytes) - (e0 & ~3);
             acc_t<Op> sum{};
             auto run = [&](auto vx) {
-                constexpr bool VX = decltype(vx)::value;
+                constexpr int VX = decltype(vx)::value;
                 const int32_t pb = sp[warp * 32 + lane], pe = sp[warp * 32 + lane + 1];
                 for (int32_t k0 = pb; k0 < pe; k0 += UN) {
                     acc_t<Op> xv[UN];
@@ -745,8 +752,10 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(2)) csr_tma(CsrTma A,
                     for (int u = 0; u < UN; ++u) xv[u] = (k0 + u < pe) ? gather_chk(op, c[u], A.ncols) : acc_t<Op>{};
 #pragma unroll
                     for (int u = 0; u < UN; ++u) {
-                        if constexpr (VX) {
+                        if constexpr (VX == 1) {
                             if (k0 + u < pe) fma_acc(sum, vtab_s[si[k0 + u]], xv[u]);
+                        } else if constexpr (VX == 2) {
+                            if (k0 + u < pe) fma_acc(sum, vtab_s[si16[k0 + u]], xv[u]);
                         } else {
                             if (k0 + u < pe) fma_acc(sum, (double)sv[k0 + u], xv[u]);
                         }
@@ -754,10 +763,12 @@ __global__ void __launch_bounds__(kTmaThreads, minb_of<Op>(2)) csr_tma(CsrTma A,
                 }
             };
             if (has_row) {
-                if (vix)
-                    run(std::true_type{});
+                if (vm == 1)
+                    run(std::integral_constant<int, 1>{});
+                else if (vm == 2)
+                    run(std::integral_constant<int, 2>{});
                 else
-                    run(std::false_type{});
+                    run(std::integral_constant<int, 0>{});
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(bars + kTmaStages + s));  // stage free

@@ -135,6 +135,18 @@ def tcsr_wide(M):
     return 2 * stage + 64 > 227 * 1024
 
 
+def tcsr_index_cap(M):
+    # distinct values a TMA-CSR store can index: its table (8 B per value) shares the
+    # 227 KB of shared memory with two stages of 2-byte indices (amgb.cu index_store)
+    te = 4
+    for r0 in range(0, M.nrows, 256):
+        e0, e1 = int(M.ptr[r0]), int(M.ptr[min(r0 + 256, M.nrows)])
+        te = max(te, ((e1 - (e0 & ~3)) + 3) & ~3, ((e1 - (e0 & ~15)) + 15) & ~15)
+    te = (te + 15) & ~15
+    stage = (te * 6 + (256 + 8) * 4 + 15) & ~15
+    return min(65536, max(256, (227 * 1024 - 64 - 2 * stage - 256) // 8))
+
+
 def tma_wide(M):
     # a forced TMA store falls back to SELL-32 when two stages of a 256-row tile
     # do not fit the 227 KB of shared memory (pick_format)
@@ -309,19 +321,27 @@ def test_vcycle_and_solve_per_format(fmt, monkeypatch):
     assert np.linalg.norm(host(x) - oc["x"]) <= 1e-8 * np.linalg.norm(oc["x"])
 
 
-def test_level1_in_sell_and_tma_under_auto(monkeypatch):
+@pytest.mark.parametrize("tmacsr", [None, "4"])
+def test_level1_in_sell_and_tma_under_auto(tmacsr, monkeypatch):
     """88^3 (681,472 rows): level 1 has >= 65,536 rows, so under the default policy
-    A1 runs sell_rows, A0 sell_tma and P0 / R0 csr_tma, as at 256^3; every op of
-    levels 0-1 per row against the oracle."""
-    for k in ("AMGB_FORMAT", "AMGB_NO_DICT"):
+    A0 runs sell_tma, P0 / R0 csr_tma and A1 sell_rows with 2-byte value indices,
+    as at 256^3 (AMGB_TMACSR=4: A1 in csr_tma with 2-byte indices and the table in
+    shared memory, when its distinct values fit); every op of levels 0-1 per row
+    against the oracle."""
+    for k in ("AMGB_FORMAT", "AMGB_NO_DICT", "AMGB_TMACSR"):
         monkeypatch.delenv(k, raising=False)
+    if tmacsr:
+        monkeypatch.setenv("AMGB_TMACSR", tmacsr)
     p, c, v, f = synth.problem("poisson", 88)
     h = amgb.setup(p, c, v)
     o = oracle.Hierarchy(oracle.Csr(p, c, v))
     i1 = h.level_info(1)
     assert i1["rows"] >= 65536
     assert h.level_info(0)["fmt_A"] == amgb.FMT_TMA and h.level_info(0)["fmt_P"] == amgb.FMT_TMACSR
-    assert h.level_info(0)["fmt_R"] == amgb.FMT_TMACSR and i1["fmt_A"] == amgb.FMT_SELL
+    assert h.level_info(0)["fmt_R"] == amgb.FMT_TMACSR
+    A1 = o.matrix(1, "A")
+    assert 256 < len(np.unique(A1.val)) <= tcsr_index_cap(A1) and sell_padding(A1) > 1.05
+    assert i1["fmt_A"] == (amgb.FMT_TMACSR if tmacsr else amgb.FMT_SELL) and i1["vidx_A"] == 2
     rng = np.random.default_rng(7)
     for l in (0, 1):
         A, P, R = o.matrix(l, "A"), o.matrix(l, "P"), o.matrix(l, "R")
