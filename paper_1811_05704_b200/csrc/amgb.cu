@@ -758,11 +758,10 @@ struct Handle {
     void rows_sell(const Sell& M, const Op& op, const int32_t* gate, const Red& red, bool stream_loads) {
         const int g = (int)std::max<int64_t>(
             1, std::min<int64_t>((M.nrows + kBlock - 1) / kBlock, (int64_t)num_sms * minb_of<Op>(PIPE ? 4 : 6)));
-        const size_t smem = (!F32 && M.vi16 && M.ntab > 0) ? (size_t)M.ntab * 8 : 0;  // <= 32 KB
         if (stream_loads)
-            klaunch(sell_rows<U, true, PIPE, Op, F32>, g, kBlock, smem, M, op, gate, red);
+            klaunch(sell_rows<U, true, PIPE, Op, F32>, g, kBlock, 0, M, op, gate, red);
         else
-            klaunch(sell_rows<U, false, PIPE, Op, F32>, g, kBlock, smem, M, op, gate, red);
+            klaunch(sell_rows<U, false, PIPE, Op, F32>, g, kBlock, 0, M, op, gate, red);
     }
     template <int G, bool F32, class Op>
     void rows_csr(const CsrDev& M, const Op& op, const int32_t* gate, const Red& red, bool stream_loads) {
@@ -2805,20 +2804,10 @@ void index_store(Handle& H, DMat& d, int64_t* bytes) {
         d.tcsr.vtab = tab, d.tcsr.vi8 = i8, d.tcsr.vi16 = i16;
         d.tcsr.ntab = i8 ? 256 : (nu + 15) & ~15;
     } else if (d.fmt == Fmt::SELL) {
-        int nu = 0;
-        if (!value_index(H, d.sell.val, d.stored, 16, 65536, &tab, &i8, &i16, &nu)) return;
+        if (!value_index(H, d.sell.val, d.stored, 16, 65536, &tab, &i8, &i16)) return;
         H.tfree(d.sell.val);
         d.sell.val = nullptr;
         d.sell.vtab = tab, d.sell.vi8 = i8, d.sell.vi16 = i16;
-        // 2-byte indices: a table of <= 4096 values (32 KB; 4 resident blocks
-        // per SM take 128 KB) is staged in shared memory by every block when the
-        // matrix is large enough to amortise it (>= 8192 stored entries per table
-        // entry: the table is then <= ~10 % of a block's matrix bytes; 256^3 A1:
-        // 33.45 vs 33.98 ms per solve, C4 29.28 vs 29.83 ms, profiles/r02_smtab);
-        // AMGB_SELL_SMEM_TAB=0: always read through L1, =1: stage whenever it fits
-        const char* st = std::getenv("AMGB_SELL_SMEM_TAB");
-        const bool big = d.stored >= (int64_t)8192 * nu || (st && st[0] == '1');
-        if (i16 && nu <= 4096 && big && !(st && st[0] == '0')) d.sell.ntab = (nu + 1) & ~1;
     } else {
         return;
     }

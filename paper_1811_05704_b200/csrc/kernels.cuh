@@ -50,9 +50,6 @@ struct Sell {
     const double* vtab = nullptr;
     const uint8_t* vi8 = nullptr;
     const uint16_t* vi16 = nullptr;
-    // > 0 (16-bit indices only): sell_rows stages the table's first ntab entries
-    // in shared memory (the launch passes ntab * 8 bytes of dynamic shared memory)
-    int32_t ntab = 0;
 };
 
 // stored slot -> matrix row of a SELL-C-sigma matrix (rows sorted by length
@@ -99,21 +96,13 @@ __device__ __forceinline__ double ld_val(const M& A, int64_t k) {
 }
 __device__ __forceinline__ uint32_t ld_idx8(const uint8_t* p) { return __ldcs(reinterpret_cast<const unsigned char*>(p)); }
 __device__ __forceinline__ uint32_t ld_idx16(const uint16_t* p) { return __ldcs(reinterpret_cast<const unsigned short*>(p)); }
-// the value table sell_rows stages in dynamic shared memory (VM 3)
-__device__ __forceinline__ double* sell_tab_smem() {
-    extern __shared__ __align__(16) double sell_tab_s[];
-    return sell_tab_s;
-}
 // value k of a SELL store in its storage mode (VM: 0 = the value array / its
-// fp32 copy, 1 = 8-bit index into vtab, 2 = 16-bit index, both tables read
-// through L1; 3 = 16-bit index into the table staged in shared memory -- the
-// 32 lanes of a warp index scattered entries, which through L1 cost about one
-// tag lookup per lane (ncu, profiles/r02_a1))
+// fp32 copy, 1 = 8-bit index into vtab, 2 = 16-bit index); the table is small
+// and read through L1
 template <int VM, bool STREAM, bool F32>
 __device__ __forceinline__ double ld_sell_val(const Sell& A, int64_t k) {
     if constexpr (VM == 1) return __ldg(A.vtab + ld_idx8(A.vi8 + k));
     else if constexpr (VM == 2) return __ldg(A.vtab + ld_idx16(A.vi16 + k));
-    else if constexpr (VM == 3) return sell_tab_smem()[ld_idx16(A.vi16 + k)];
     else return ld_val<STREAM, F32>(A, k);
 }
 
@@ -325,12 +314,6 @@ template <int U1, bool STREAM, bool PIPE, class Op, bool F32 = false>
 __global__ void __launch_bounds__(kBlock, minb_of<Op>(PIPE ? 4 : 6)) sell_rows(Sell A, Op op, const int32_t* gate,
                                                                                  Red red) {
     constexpr int U = unroll_of<Op>(U1);
-    const bool smem_tab = !F32 && A.vi16 && A.ntab > 0;
-    if (smem_tab) {  // setup data: staged before the wait on the previous kernel
-        double* t = sell_tab_smem();
-        for (int k = threadIdx.x; k < A.ntab; k += blockDim.x) t[k] = __ldg(A.vtab + k);
-        __syncthreads();
-    }
     pdl_wait();
     if (gated(gate)) return;
     op.prepare();
@@ -340,8 +323,6 @@ __global__ void __launch_bounds__(kBlock, minb_of<Op>(PIPE ? 4 : 6)) sell_rows(S
     for (int k = 0; k < ND; ++k) dots[k] = 0.0;
     if (A.vi8 && !F32)
         sell_rows_body<1, U, STREAM, PIPE, F32>(A, op, dots);
-    else if (smem_tab)
-        sell_rows_body<3, U, STREAM, PIPE, F32>(A, op, dots);
     else if (A.vi16 && !F32)
         sell_rows_body<2, U, STREAM, PIPE, F32>(A, op, dots);
     else

@@ -321,18 +321,17 @@ def test_vcycle_and_solve_per_format(fmt, monkeypatch):
     assert np.linalg.norm(host(x) - oc["x"]) <= 1e-8 * np.linalg.norm(oc["x"])
 
 
-@pytest.mark.parametrize("env", [{}, {"AMGB_TMACSR": "4"}, {"AMGB_SELL_SMEM_TAB": "0"}, {"AMGB_SELL_SMEM_TAB": "1"}])
-def test_level1_in_sell_and_tma_under_auto(env, monkeypatch):
+@pytest.mark.parametrize("tmacsr", [None, "4"])
+def test_level1_in_sell_and_tma_under_auto(tmacsr, monkeypatch):
     """88^3 (681,472 rows): level 1 has >= 65,536 rows, so under the default policy
     A0 runs sell_tma, P0 / R0 csr_tma and A1 sell_rows with 2-byte value indices,
-    as at 256^3, the table staged in shared memory (AMGB_SELL_SMEM_TAB=0: read through
-    L1; AMGB_TMACSR=4: A1 in csr_tma with 2-byte indices); every op of levels 0-1
-    per row against the oracle."""
-    for k in ("AMGB_FORMAT", "AMGB_NO_DICT", "AMGB_TMACSR", "AMGB_SELL_SMEM_TAB"):
+    as at 256^3 (AMGB_TMACSR=4: A1 in csr_tma with 2-byte indices and the table in
+    shared memory, when its distinct values fit); every op of levels 0-1 per row
+    against the oracle."""
+    for k in ("AMGB_FORMAT", "AMGB_NO_DICT", "AMGB_TMACSR"):
         monkeypatch.delenv(k, raising=False)
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
-    tmacsr = env.get("AMGB_TMACSR")
+    if tmacsr:
+        monkeypatch.setenv("AMGB_TMACSR", tmacsr)
     p, c, v, f = synth.problem("poisson", 88)
     h = amgb.setup(p, c, v)
     o = oracle.Hierarchy(oracle.Csr(p, c, v))
@@ -341,7 +340,7 @@ def test_level1_in_sell_and_tma_under_auto(env, monkeypatch):
     assert h.level_info(0)["fmt_A"] == amgb.FMT_TMA and h.level_info(0)["fmt_P"] == amgb.FMT_TMACSR
     assert h.level_info(0)["fmt_R"] == amgb.FMT_TMACSR
     A1 = o.matrix(1, "A")
-    assert 256 < len(np.unique(A1.val)) <= min(4096, tcsr_index_cap(A1)) and sell_padding(A1) > 1.05
+    assert 256 < len(np.unique(A1.val)) <= tcsr_index_cap(A1) and sell_padding(A1) > 1.05
     assert i1["fmt_A"] == (amgb.FMT_TMACSR if tmacsr else amgb.FMT_SELL) and i1["vidx_A"] == 2
     rng = np.random.default_rng(7)
     for l in (0, 1):
